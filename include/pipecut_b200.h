@@ -1,0 +1,169 @@
+/*
+ * pipecut_b200 — C-ABI of the B200-native partition-search hot path.
+ *
+ * Drop-in boundary for the reference package `pipecut` (pure Python,
+ * /root/reference/pkg).  The reference has no native code, so there is no
+ * existing FFI; these entry points are what its Python call sites bind via
+ * ctypes (INTEGRATION.md shows the stubs).  Each entry point names the
+ * reference function it replaces:
+ *
+ *   pc_set_problem      BlockSet + CostModel + ClusterSpec, flattened
+ *                       (pkg/src/pipecut/blocks.py:295-343, costs.py:89-164,
+ *                        graph.py:176-199)
+ *   pc_profile_spans    CostModel.profile(BlockSet.span(lo, hi), m, ckpt)
+ *                       (costs.py:97-160 via stages.py:138-145)
+ *   pc_form_stage_dp    form_stage_dp (stages.py:282-291 -> _run_dp 188-279)
+ *   pc_run_calls        the per-(n, S, MB) _run_dp calls of form_stage plus
+ *                       simulate()-based ranking keys (stages.py:389-411,
+ *                       simulate.py:79-165) -- the unit sharded across GPUs
+ *   pc_form_stage       form_stage (stages.py:372-413), single GPU
+ *   pc_partition_blocks partition_blocks (blocks.py:361-397)
+ *
+ * Conventions: plain pointers and sizes, caller-owned host buffers, valid for
+ * the duration of the call; the library owns device memory behind an opaque
+ * context.  Calls are blocking.  There is no CPU fallback: without a usable
+ * sm_100 device every compute entry point returns PC_ERR_CUDA.
+ */
+#ifndef PIPECUT_B200_H
+#define PIPECUT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes (mapped to the reference exception classes in Python) */
+#define PC_OK                 0
+#define PC_INFEASIBLE         1   /* plan is None (stages.py:122-125) */
+#define PC_ERR_INVALID       (-1) /* InvalidArgs (stages.py:160-168, 382-384) */
+#define PC_ERR_BUDGET        (-2) /* SearchBudgetExceeded (stages.py:33-37, 214-216) */
+#define PC_ERR_ATOM          (-3) /* InfeasibleAtom (blocks.py:22-31, 366-369) */
+#define PC_ERR_STUCK         (-4) /* CompactionStuck (blocks.py:34-42, 291) */
+#define PC_ERR_CUDA          (-5) /* CUDA / device error; see pc_last_error */
+#define PC_ERR_CAPACITY      (-6) /* frontier / table capacity exceeded (never truncated) */
+
+typedef struct pc_ctx pc_ctx;
+
+/*
+ * Flattened span-profile problem (paper_2103_16063_b200/flatten.py builds it).
+ * Arrays are read-only for the call of pc_set_problem, which copies them to
+ * the device.
+ */
+typedef struct pc_problem {
+    int32_t nb;                 /* len(BlockSet) */
+    int32_t n_tasks;            /* tasks in sorted node-id order (costs.py:120) */
+    const int32_t *task_block;  /* [n_tasks] */
+    const double  *task_flops;  /* [n_tasks] flops_per_sample (costs.py:137) */
+    const int64_t *task_fp_fix; /* [n_tasks] produced + span-independent preds */
+    const int64_t *task_fp_ps;  /* [n_tasks] per-sample part */
+    const int32_t *task_dep_off;/* [n_tasks+1] CSR: preds owned in block dep_ob */
+    const int32_t *dep_ob;      /*   count in the footprint iff dep_ob >= lo  */
+    const int64_t *dep_fix;
+    const int64_t *dep_ps;
+    int32_t n_in;               /* values listed in some atom's input_values */
+    const int32_t *in_ob;       /* [n_in] owner block, -1 model input/unowned */
+    const int32_t *in_cons_off; /* [n_in+1] CSR of sorted consumer blocks */
+    const int32_t *in_cons;
+    const int64_t *in_fix;      /* [n_in] */
+    const int64_t *in_ps;       /* [n_in] */
+    const int64_t *blk_param;   /* [nb] parameter bytes owned per block */
+    const int64_t *blk_res_fix; /* [nb] resident bytes per block */
+    const int64_t *blk_res_ps;  /* [nb] */
+    const int64_t *cut_fixed;   /* [nb+1] BlockSet._cut_fixed (blocks.py:310) */
+    const double  *cut_ps;      /* [nb+1] BlockSet._cut_per_sample (blocks.py:311) */
+    /* CostModelConfig (costs.py:27-40) */
+    double flops_per_sec;
+    double bwd_fwd_ratio;
+    double grad_factor;
+    double opt_factor;
+    int32_t checkpointing;
+    /* ClusterSpec (graph.py:176-199) */
+    int32_t num_nodes;
+    int32_t devices_per_node;
+    int32_t monotone;           /* task_block non-decreasing: incremental folds */
+    int64_t mem_budget;
+    double bw_intra;
+    double bw_inter;
+    double latency;
+} pc_problem;
+
+/* One DP call of _run_dp (stages.py:188): S stages on D devices. */
+typedef struct pc_call {
+    int32_t S, D, R, MB;        /* stage count, devices, replica factor, microbatches */
+} pc_call;
+
+/* Plan output (StagePlan/Plan, stages.py:40-57) into caller arrays of
+ * capacity cap_stages.  iteration_time is simulate(plan).iteration_time_sec
+ * (simulate.py:165) when requested. */
+typedef struct pc_plan {
+    int32_t cap_stages;
+    int32_t n_stages;           /* 0 when infeasible */
+    int32_t *lo, *hi, *devices; /* [cap_stages] */
+    double  *t_fwd, *t_bwd;     /* [cap_stages] profile at the plan microbatch, no comm */
+    int64_t *mem;               /* [cap_stages] */
+    int32_t S, D, R, MB;
+    double objective;           /* max fwd + max bwd with comm (stages.py:277-278) */
+    double iteration_time;      /* simulate(plan).iteration_time_sec, or NaN */
+} pc_plan;
+
+typedef struct pc_stats {
+    int64_t visits;             /* SearchStats.visits, pruned as the reference counts */
+    int64_t dp_calls;           /* SearchStats.dp_calls */
+    int64_t visits_unpruned;    /* closed form: the throughput unit */
+    int64_t cells;              /* (s, b, d) table cells computed on device */
+    int64_t entries;            /* Pareto frontier entries written on device */
+    double  device_ms;          /* device time of the DP kernels (CUDA events) */
+    double  span_ms;            /* device time of span/cut table kernels */
+} pc_stats;
+
+/* Per-call result of pc_run_calls (one record per pc_call). */
+typedef struct pc_call_result {
+    int32_t feasible;
+    int32_t n_stages;
+    double  objective;
+    double  iteration_time;
+    int64_t visits;             /* pruned reference visits of this call */
+    int64_t visits_unpruned;
+    int64_t budget_cross;       /* running visits at the first cell exceeding the
+                                   budget within this call given visits_before, or -1 */
+} pc_call_result;
+
+/* ---- context ---------------------------------------------------------- */
+int  pc_ctx_create(int device, pc_ctx **out);
+void pc_ctx_destroy(pc_ctx *ctx);
+const char *pc_last_error(pc_ctx *ctx);
+int  pc_device_info(pc_ctx *ctx, int32_t *sm_count, int32_t *cc_major, int32_t *cc_minor);
+
+/* ---- problem ------------------------------------------------------------ */
+int pc_set_problem(pc_ctx *ctx, const pc_problem *p);
+
+/* CostModel.profile over block spans: n queries (lo, hi, m, ckpt). */
+int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const int32_t *hi,
+                     const int64_t *m, const int32_t *ckpt,
+                     double *t_fwd, double *t_bwd, int64_t *mem);
+
+/* form_stage_dp: one DP call.  visit_budget < 0 means none.  Returns PC_OK,
+ * PC_INFEASIBLE, PC_ERR_BUDGET (stats->visits = visits at the crossing). */
+int pc_form_stage_dp(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_size,
+                     int32_t R, int32_t MB, int32_t disable_pruning,
+                     int64_t visit_budget, pc_plan *plan, pc_stats *stats);
+
+/* Batch of independent DP calls (the sharded unit of form_stage).  Every
+ * call's plan is simulated for its ranking key when want_iteration != 0.
+ * plans may be NULL (results only); otherwise n entries. */
+int pc_run_calls(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
+                 int32_t disable_pruning, int32_t want_iteration,
+                 pc_call_result *results, pc_plan *plans, pc_stats *stats);
+
+/* form_stage on one GPU.  speculative != 0 evaluates every widening level in
+ * one batch and then applies the reference's first-feasible-level rule;
+ * results and stats are identical either way. */
+int pc_form_stage(pc_ctx *ctx, int32_t num_nodes, int32_t devices_per_node,
+                  int64_t batch_size, int32_t disable_pruning, int64_t visit_budget,
+                  int32_t speculative, pc_plan *plan, pc_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPECUT_B200_H */

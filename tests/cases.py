@@ -1,0 +1,156 @@
+"""Problem families shared by the parity tests, goldens and bench.
+
+The random families replay the reference tests' generators with the same RNG
+call order so seeds give the same instances:
+  * stages_random_instance   <- pkg/tests/test_stages.py:158-183
+  * search_instance          <- pkg/tests/test_acceptance.py:92-122
+The configs C1-C5 follow SURVEY.md §8(d) / BASELINE.md §2.
+"""
+
+from __future__ import annotations
+
+import random
+
+from paper_2103_16063_b200._host import pipecut as pc
+
+Node, TaskGraph, TaskInfo, ValueInfo = pc.graph.Node, pc.TaskGraph, pc.graph.TaskInfo, pc.graph.ValueInfo
+
+
+def _val(vid, fixed=0, per_sample=0, param=False):
+    return Node(vid, value=ValueInfo(fixed_bytes=fixed, bytes_per_sample=per_sample,
+                                     is_param=param))
+
+
+def _task(tid, flops=0.0, op="op"):
+    return Node(tid, task=TaskInfo(op=op, flops_per_sample=flops, attrs={}))
+
+
+def chain(flops, sizes=None, params=None, x_bytes=0):
+    """x -> t00 -> v00 -> t01 ...; optional weight per task (test_stages.py:25-42)."""
+    n = len(flops)
+    sizes = sizes or [0] * n
+    params = params or [0] * n
+    nodes, edges, prev = [_val("x", per_sample=x_bytes)], [], "x"
+    for i in range(n):
+        t, v = f"t{i:02d}", f"v{i:02d}"
+        nodes.append(_task(t, flops[i]))
+        nodes.append(_val(v, per_sample=sizes[i]))
+        edges.append((prev, t))
+        edges.append((t, v))
+        if params[i]:
+            w = f"w{i:02d}"
+            nodes.append(_val(w, fixed=params[i], param=True))
+            edges.append((w, t))
+        prev = v
+    return TaskGraph(nodes, edges, ["x"], [prev])
+
+
+def one_block_per_task(graph, *, mem=2 ** 40, nodes=1, dpn=4, bw=(1e12, 1e12),
+                       latency=0.0, ckpt=False, flops_per_sec=1.0):
+    """BlockSet with one block per atom (test_stages.py:45-54)."""
+    cl = pc.ClusterSpec(num_nodes=nodes, devices_per_node=dpn, device_memory_bytes=mem,
+                        bw_intra=bw[0], bw_inter=bw[1], link_latency_sec=latency)
+    part = pc.build_atomic_subcomponents(graph)
+    cfg = pc.CostModelConfig(device_flops_per_sec=flops_per_sec, checkpointing=ckpt)
+    return pc.partition_blocks(part, pc.CostModel(part.graph, cfg, cl), k=10 ** 6)
+
+
+def stages_random_instance(rng):
+    """Same RNG sequence as test_stages.random_instance."""
+    n = rng.randint(2, 8)
+    flops = [round(rng.uniform(0.5, 4.0), 3) for _ in range(n)]
+    sizes = [rng.choice([0, 0, 64, 256, 1024]) for _ in range(n)]
+    params = [rng.choice([0, 0, 0, 512, 2048]) for _ in range(n)]
+    S = rng.randint(1, min(4, n))
+    D = rng.randint(S, 6)
+    R = rng.choice([1, 2])
+    MB = rng.choice([1, 2, 4])
+    BS = R * MB * D * rng.randint(1, 3)
+    state = sum(p * 4 for p in params)
+    acts = sum(sizes) * (BS // (MB * R)) + 64
+    budget = rng.choice([2 ** 40, max(int((state + acts) * rng.uniform(0.4, 1.1)), 64)])
+    nodes_cfg = rng.choice([(1, 6), (2, 2), (2, 3)])
+    graph = chain(flops, sizes, params, x_bytes=rng.choice([0, 16]))
+    while True:
+        try:
+            bs = one_block_per_task(graph, mem=budget, nodes=nodes_cfg[0], dpn=nodes_cfg[1],
+                                    bw=(1e3, 5e2), latency=rng.choice([0.0, 0.01]),
+                                    ckpt=rng.random() < 0.5)
+            break
+        except pc.InfeasibleAtom:
+            budget *= 4
+    return bs, S, D, BS, R, MB
+
+
+def search_instance(rng):
+    """Same RNG sequence as test_acceptance._search_instance."""
+    S = rng.randint(1, 4)
+    n = rng.randint(max(6, S + 2), 10)
+    nodes, dpn = rng.choice([(1, 6), (2, 3), (3, 2)])
+    D = rng.randint(min(S + 1, 6), 6)
+    R = rng.choice([1, 2])
+    MB = rng.choice([1, 2, 4])
+    BS = R * MB * D * rng.randint(2, 4)
+    flops = [round(rng.uniform(0.5, 4.0), 3) for _ in range(n)]
+    sizes = [rng.choice([64, 128, 256, 512, 1024]) for _ in range(n)]
+    params = [rng.choice([0, 256, 1024]) for _ in range(n)]
+    g = chain(flops, sizes=sizes, params=params)
+    need = 4 * sum(params) + sum(sizes) * (BS // (MB * R))
+    budget = max(int(need * rng.uniform(0.25, 0.50)), 256)
+    for _ in range(4):
+        cl = pc.ClusterSpec(num_nodes=nodes, devices_per_node=dpn, device_memory_bytes=budget,
+                            bw_intra=1e3, bw_inter=5e2,
+                            link_latency_sec=rng.choice([0.0, 0.01]))
+        part = pc.build_atomic_subcomponents(g)
+        model = pc.CostModel(part.graph, pc.CostModelConfig(device_flops_per_sec=1.0,
+                                                            checkpointing=False), cl)
+        try:
+            return pc.partition_blocks(part, model, 10 ** 6), S, D, BS, R, MB
+        except pc.InfeasibleAtom:
+            budget *= 4
+    raise RuntimeError("could not build a feasible random instance")
+
+
+# ---------------------------------------------------------------- configs
+CONFIGS = {
+    # name: (generator, args, (nodes, dpn, memory), k, batch)
+    "C1": ("bert", (1024, 24, 512, 30522), (1, 8, 2 ** 35), 32, 256),
+    "C2": ("bert", (2048, 96, 512, 30522), (4, 8, 32e9), 32, 256),
+    "C3": ("resnet", (152, 8), (1, 8, 180e9), 32, 128),
+    "C4": ("bert", (4096, 256, 512, 30522), (32, 8, 32e9), 32, 2048),
+}
+
+
+def config_partition(name):
+    """(partition, model, k, batch, cluster) for C1-C4."""
+    kind, args, (nodes, dpn, mem), k, batch = CONFIGS[name]
+    g = pc.gen_bert_like(*args) if kind == "bert" else pc.gen_resnet_like(*args)
+    cl = pc.ClusterSpec(nodes, dpn, int(mem), 50e9, 10e9)
+    part = pc.build_atomic_subcomponents(g)
+    model = pc.CostModel(part.graph, pc.CostModelConfig(), cl)
+    return part, model, k, batch, cl
+
+
+def bert_layer_chain(nb, hidden=1024, seq=512, jitter_seed=None):
+    """C5: one task per BERT layer, ids t%05d so sorted order is chain order."""
+    h, s = hidden, seq
+    heads = max(1, h // 64)
+    flops = 24.0 * s * h * h + 4.0 * s * s * h + 5.0 * s * s * heads + 52.0 * s * h
+    rng = random.Random(jitter_seed) if jitter_seed is not None else None
+    nodes, edges, prev = [_val("x", per_sample=s * 8)], [], "x"
+    for i in range(nb):
+        t, v, w = f"t{i:05d}", f"v{i:05d}", f"w{i:05d}"
+        f = flops if rng is None else flops * rng.uniform(0.9, 1.1)
+        nodes += [_task(t, f, op="layer"), _val(v, per_sample=s * h * 4),
+                  _val(w, fixed=(12 * h * h + 13 * h) * 4, param=True)]
+        edges += [(prev, t), (w, t), (t, v)]
+        prev = v
+    return TaskGraph(nodes, edges, ["x"], [prev])
+
+
+def c5_blockset(nb, D, jitter_seed=None):
+    g = bert_layer_chain(nb, jitter_seed=jitter_seed)
+    cl = pc.ClusterSpec(max(1, D // 8), min(8, D), int(32e9), 50e9, 10e9)
+    part = pc.build_atomic_subcomponents(g)
+    model = pc.CostModel(part.graph, pc.CostModelConfig(), cl)
+    return pc.partition_blocks(part, model, k=10 ** 6)
