@@ -1,0 +1,999 @@
+// Host orchestration and the C-ABI of include/pipecut_b200.h.
+//
+// The device does all search arithmetic (span tables, DP levels, visit
+// accounting, backtrack, stage records, simulation); the host code here only
+// sizes buffers, orders launches and applies the reference's enumeration and
+// selection rules over per-call records (form_stage, stages.py:372-413).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace pcb;
+
+namespace {
+
+struct DBuf {
+    void *p = nullptr;
+    size_t n = 0;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= n && p) return cudaSuccess;
+        release();
+        size_t want = bytes + bytes / 4 + 256;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            return e;
+        }
+        n = want;
+        return cudaSuccess;
+    }
+    template <class T>
+    T *as() const { return (T *)p; }
+};
+
+struct CachedKey {
+    int64_t m;
+    int ckpt;
+    double *tfc = nullptr;
+    double *tbc = nullptr;
+};
+
+}  // namespace
+
+struct pc_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    std::string err;
+    int sm_count = 0;
+    // problem
+    bool has_problem = false;
+    DevProblem P;
+    int nb = 0;
+    std::vector<int64_t> pre_param;
+    DBuf prob;       // all problem arrays in one allocation
+    DBuf in_tab;     // in_tab_fix | in_tab_ps
+    // key cache
+    std::vector<CachedKey> keys;
+    std::map<std::pair<int64_t, int>, int> key_map;
+    DBuf key_ptrs;   // [2][n_keys] device pointers
+    size_t key_bytes = 0;
+    // batch scratch
+    DBuf calls_d, warp_prefix_d, keyidx_d, val_d, hist_d, overflow_d;
+    DBuf level_off_d, level_sums_d, row_prefix_d;
+    DBuf plan_off_d, seg_d, objective_d, feasible_d;
+    DBuf q_d, q_out_d, sim_d;
+    DBuf raw_d, keys_m_d, keys_ckpt_d;
+    // last batch (for budget crossing queries)
+    std::vector<CallDesc> last_calls;   // sorted order
+    std::vector<int> last_pos;          // orig -> sorted position
+    std::vector<std::vector<int64_t>> last_level_sums;  // by orig
+    int last_pruning = 1;
+    int last_FL = 4;
+    DPBatch last_batch{};
+    // timing of the last batch
+    double last_dp_ms = 0, last_span_ms = 0;
+    int64_t last_dp_launches = 0;
+};
+
+#define CUDA_TRY(ctx, expr)                                                       \
+    do {                                                                          \
+        cudaError_t e__ = (expr);                                                 \
+        if (e__ != cudaSuccess) {                                                 \
+            (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(e__);    \
+            return PC_ERR_CUDA;                                                   \
+        }                                                                         \
+    } while (0)
+
+static int fail(pc_ctx *ctx, int code, const std::string &msg) {
+    ctx->err = msg;
+    return code;
+}
+
+static int check_launch(pc_ctx *ctx, const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, PC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return PC_OK;
+}
+
+// =========================================================================== context
+extern "C" int pc_ctx_create(int device, pc_ctx **out) {
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n <= device) {
+        cudaGetLastError();
+        return PC_ERR_CUDA;
+    }
+    pc_ctx *ctx = new pc_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return PC_ERR_CUDA;
+    }
+    cudaEventCreate(&ctx->ev0);
+    cudaEventCreate(&ctx->ev1);
+    cudaEventCreate(&ctx->ev2);
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major != 10) {
+        ctx->err = "pipecut_b200 is built for sm_100a only";
+        pc_ctx_destroy(ctx);
+        return PC_ERR_CUDA;
+    }
+    *out = ctx;
+    return PC_OK;
+}
+
+static void free_keys(pc_ctx *ctx) {
+    for (auto &k : ctx->keys) {
+        if (k.tfc) cudaFree(k.tfc);
+        if (k.tbc) cudaFree(k.tbc);
+    }
+    ctx->keys.clear();
+    ctx->key_map.clear();
+    ctx->key_bytes = 0;
+}
+
+extern "C" void pc_ctx_destroy(pc_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->st);
+    free_keys(ctx);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+    if (ctx->st) cudaStreamDestroy(ctx->st);
+    delete ctx;
+}
+
+extern "C" const char *pc_last_error(pc_ctx *ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+extern "C" int pc_device_info(pc_ctx *ctx, int32_t *sm_count, int32_t *cc_major, int32_t *cc_minor) {
+    int ma = 0, mi = 0;
+    cudaDeviceGetAttribute(&ma, cudaDevAttrComputeCapabilityMajor, ctx->device);
+    cudaDeviceGetAttribute(&mi, cudaDevAttrComputeCapabilityMinor, ctx->device);
+    *sm_count = ctx->sm_count;
+    *cc_major = ma;
+    *cc_minor = mi;
+    return PC_OK;
+}
+
+// =========================================================================== problem
+extern "C" int pc_set_problem(pc_ctx *ctx, const pc_problem *p) {
+    cudaSetDevice(ctx->device);
+    if (p->nb < 1 || p->nb > MAX_NB_KEY) return fail(ctx, PC_ERR_CAPACITY, "block count out of range");
+    if (p->n_tasks < 0 || p->n_in < 0) return fail(ctx, PC_ERR_INVALID, "negative sizes");
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    free_keys(ctx);
+    ctx->has_problem = false;
+    const int nb = p->nb, T = p->n_tasks, V = p->n_in;
+    const int ndep = p->task_dep_off[T];
+    const int ncons = p->in_cons_off[V];
+    // block -> task CSR (stable: task indices ascending within a block)
+    std::vector<int32_t> blk_off(nb + 1, 0), blk_tasks(T);
+    for (int t = 0; t < T; ++t) {
+        int b = p->task_block[t];
+        if (b < 0 || b >= nb) return fail(ctx, PC_ERR_INVALID, "task block out of range");
+        blk_off[b + 1]++;
+    }
+    for (int b = 0; b < nb; ++b) blk_off[b + 1] += blk_off[b];
+    {
+        std::vector<int32_t> fill(blk_off.begin(), blk_off.end() - 1);
+        for (int t = 0; t < T; ++t) blk_tasks[fill[p->task_block[t]]++] = t;
+    }
+    std::vector<int64_t> pre_param(nb + 1, 0), pre_rf(nb + 1, 0), pre_rp(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) {
+        pre_param[b + 1] = pre_param[b] + p->blk_param[b];
+        pre_rf[b + 1] = pre_rf[b] + p->blk_res_fix[b];
+        pre_rp[b + 1] = pre_rp[b] + p->blk_res_ps[b];
+    }
+    // one allocation, 8-byte aligned sub-arrays
+    struct Part { const void *src; size_t bytes; size_t off; };
+    std::vector<Part> parts;
+    size_t total = 0;
+    auto add = [&](const void *src, size_t bytes) {
+        size_t off = (total + 15) & ~size_t(15);
+        parts.push_back({src, bytes, off});
+        total = off + bytes;
+        return parts.size() - 1;
+    };
+    size_t i_tb = add(p->task_block, 4 * (size_t)T);
+    size_t i_tf = add(p->task_flops, 8 * (size_t)T);
+    size_t i_ff = add(p->task_fp_fix, 8 * (size_t)T);
+    size_t i_fp = add(p->task_fp_ps, 8 * (size_t)T);
+    size_t i_do = add(p->task_dep_off, 4 * (size_t)(T + 1));
+    size_t i_dob = add(p->dep_ob, 4 * (size_t)ndep);
+    size_t i_df = add(p->dep_fix, 8 * (size_t)ndep);
+    size_t i_dp = add(p->dep_ps, 8 * (size_t)ndep);
+    size_t i_bo = add(blk_off.data(), 4 * (size_t)(nb + 1));
+    size_t i_bt = add(blk_tasks.data(), 4 * (size_t)T);
+    size_t i_io = add(p->in_ob, 4 * (size_t)V);
+    size_t i_ico = add(p->in_cons_off, 4 * (size_t)(V + 1));
+    size_t i_ic = add(p->in_cons, 4 * (size_t)ncons);
+    size_t i_if = add(p->in_fix, 8 * (size_t)V);
+    size_t i_ip = add(p->in_ps, 8 * (size_t)V);
+    size_t i_pp = add(pre_param.data(), 8 * (size_t)(nb + 1));
+    size_t i_prf = add(pre_rf.data(), 8 * (size_t)(nb + 1));
+    size_t i_prp = add(pre_rp.data(), 8 * (size_t)(nb + 1));
+    size_t i_cf = add(p->cut_fixed, 8 * (size_t)(nb + 1));
+    size_t i_cp = add(p->cut_ps, 8 * (size_t)(nb + 1));
+    CUDA_TRY(ctx, ctx->prob.ensure(total + 16));
+    std::vector<char> staging(total + 16, 0);
+    for (auto &pt : parts)
+        if (pt.bytes) memcpy(staging.data() + pt.off, pt.src, pt.bytes);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->prob.p, staging.data(), total, cudaMemcpyHostToDevice, ctx->st));
+    char *base = (char *)ctx->prob.p;
+    auto at = [&](size_t i) { return (void *)(base + parts[i].off); };
+    DevProblem &D = ctx->P;
+    D = DevProblem();
+    D.nb = nb;
+    D.n_tasks = T;
+    D.n_in = V;
+    D.num_nodes = p->num_nodes;
+    D.dpn = p->devices_per_node;
+    D.checkpointing = p->checkpointing;
+    D.monotone = p->monotone;
+    D.n_inter = p->num_nodes > 1 ? 2 : 1;
+    D.mem_budget = p->mem_budget;
+    D.flops = p->flops_per_sec;
+    D.beta = p->bwd_fwd_ratio;
+    D.factor = (1.0 + p->grad_factor) + p->opt_factor;   // costs.py:158
+    D.bw_intra = p->bw_intra;
+    D.bw_inter = p->bw_inter;
+    D.lat = p->latency;
+    D.task_block = (const int32_t *)at(i_tb);
+    D.task_flops = (const double *)at(i_tf);
+    D.fp_fix = (const int64_t *)at(i_ff);
+    D.fp_ps = (const int64_t *)at(i_fp);
+    D.dep_off = (const int32_t *)at(i_do);
+    D.dep_ob = (const int32_t *)at(i_dob);
+    D.dep_fix = (const int64_t *)at(i_df);
+    D.dep_ps = (const int64_t *)at(i_dp);
+    D.blk_off = (const int32_t *)at(i_bo);
+    D.blk_tasks = (const int32_t *)at(i_bt);
+    D.in_ob = (const int32_t *)at(i_io);
+    D.in_cons_off = (const int32_t *)at(i_ico);
+    D.in_cons = (const int32_t *)at(i_ic);
+    D.in_fix = (const int64_t *)at(i_if);
+    D.in_ps = (const int64_t *)at(i_ip);
+    D.pre_param = (const int64_t *)at(i_pp);
+    D.pre_res_fix = (const int64_t *)at(i_prf);
+    D.pre_res_ps = (const int64_t *)at(i_prp);
+    D.cut_fixed = (const int64_t *)at(i_cf);
+    D.cut_ps = (const double *)at(i_cp);
+    const int64_t tri = tri_size(nb);
+    CUDA_TRY(ctx, ctx->in_tab.ensure(sizeof(int64_t) * 2 * (size_t)tri));
+    int64_t *inf = ctx->in_tab.as<int64_t>();
+    D.in_tab_fix = inf;
+    D.in_tab_ps = inf + tri;
+    launch_in_tables(D, inf, inf + tri, ctx->st);
+    if (int rc = check_launch(ctx, "in_tables")) return rc;
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    ctx->pre_param = pre_param;
+    ctx->nb = nb;
+    ctx->has_problem = true;
+    return PC_OK;
+}
+
+// =========================================================================== key tables
+static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &want) {
+    const DevProblem &P = ctx->P;
+    const int64_t tri = tri_size(P.nb);
+    const size_t per_key = sizeof(double) * 2 * (size_t)P.n_inter * (size_t)tri;
+    std::vector<std::pair<int64_t, int>> fresh;
+    for (auto &k : want)
+        if (!ctx->key_map.count(k)) fresh.push_back(k);
+    if (fresh.empty()) return PC_OK;
+    // bounded cache: drop keys the current batch does not need when the cache
+    // would outgrow a third of free device memory
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (ctx->key_bytes + fresh.size() * per_key > (ctx->key_bytes + free_b) / 3) {
+        std::map<std::pair<int64_t, int>, int> need;
+        for (auto &k : want) need[k] = 1;
+        std::vector<CachedKey> kept;
+        for (auto &k : ctx->keys) {
+            if (need.count({k.m, k.ckpt})) {
+                kept.push_back(k);
+            } else {
+                cudaFree(k.tfc);
+                cudaFree(k.tbc);
+                ctx->key_bytes -= per_key;
+            }
+        }
+        ctx->keys = kept;
+        ctx->key_map.clear();
+        for (size_t i = 0; i < ctx->keys.size(); ++i)
+            ctx->key_map[{ctx->keys[i].m, ctx->keys[i].ckpt}] = (int)i;
+    }
+    const int nf = (int)fresh.size();
+    std::vector<int64_t> km(nf);
+    std::vector<int32_t> kc(nf);
+    std::vector<double *> pf(nf), pb(nf);
+    for (int i = 0; i < nf; ++i) {
+        km[i] = fresh[i].first;
+        kc[i] = fresh[i].second;
+        CUDA_TRY(ctx, cudaMalloc(&pf[i], per_key / 2));
+        CUDA_TRY(ctx, cudaMalloc(&pb[i], per_key / 2));
+        ctx->key_bytes += per_key;
+    }
+    CUDA_TRY(ctx, ctx->keys_m_d.ensure(sizeof(int64_t) * nf + sizeof(int32_t) * nf + sizeof(double *) * 2 * nf + 64));
+    char *kb = ctx->keys_m_d.as<char>();
+    int64_t *d_km = (int64_t *)kb;
+    int32_t *d_kc = (int32_t *)(kb + sizeof(int64_t) * nf);
+    double **d_pf = (double **)(kb + ((sizeof(int64_t) * nf + sizeof(int32_t) * nf + 15) & ~size_t(15)));
+    double **d_pb = d_pf + nf;
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_km, km.data(), sizeof(int64_t) * nf, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_kc, kc.data(), sizeof(int32_t) * nf, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_pf, pf.data(), sizeof(double *) * nf, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_pb, pb.data(), sizeof(double *) * nf, cudaMemcpyHostToDevice, ctx->st));
+    const double *raw_tf = nullptr, *raw_tb = nullptr;
+    if (!P.monotone) {
+        CUDA_TRY(ctx, ctx->raw_d.ensure(sizeof(double) * 2 * (size_t)nf * tri));
+        double *r = ctx->raw_d.as<double>();
+        launch_span_time_general(P, nf, d_km, r, r + (size_t)nf * tri, ctx->st);
+        if (int rc = check_launch(ctx, "span_time_general")) return rc;
+        raw_tf = r;
+        raw_tb = r + (size_t)nf * tri;
+    }
+    launch_span_dp_tables(P, nf, d_km, d_kc, raw_tf, raw_tb, d_pf, d_pb, ctx->st);
+    if (int rc = check_launch(ctx, "span_dp_tables")) return rc;
+    for (int i = 0; i < nf; ++i) {
+        CachedKey ck;
+        ck.m = km[i];
+        ck.ckpt = kc[i];
+        ck.tfc = pf[i];
+        ck.tbc = pb[i];
+        ctx->key_map[{km[i], kc[i]}] = (int)ctx->keys.size();
+        ctx->keys.push_back(ck);
+    }
+    // device pointer arrays for the DP kernels
+    const size_t nk = ctx->keys.size();
+    std::vector<const double *> ptrs(2 * nk);
+    for (size_t i = 0; i < nk; ++i) {
+        ptrs[i] = ctx->keys[i].tfc;
+        ptrs[nk + i] = ctx->keys[i].tbc;
+    }
+    CUDA_TRY(ctx, ctx->key_ptrs.ensure(sizeof(double *) * 2 * nk));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->key_ptrs.p, ptrs.data(), sizeof(double *) * 2 * nk,
+                                  cudaMemcpyHostToDevice, ctx->st));
+    // keep staging vectors alive until the copies complete
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    return PC_OK;
+}
+
+// =========================================================================== batch
+struct CallOut {
+    int feasible = 0;
+    double objective = NAN;
+    double iteration = NAN;
+    int64_t visits = 0, visits_unpruned = 0;
+    std::vector<int32_t> lo, hi, dev;
+    std::vector<double> tf, tb;
+    std::vector<int64_t> mem;
+    std::vector<int64_t> level_sums;
+};
+
+static int validate_call(pc_ctx *ctx, const pc_call &c, int64_t BS) {
+    if (c.S < 1 || c.D < 1 || BS < 1 || c.R < 1 || c.MB < 1)
+        return fail(ctx, PC_ERR_INVALID, "stage count, devices, batch size, replicas and microbatches must all be at least 1");
+    if (c.S > c.D) return fail(ctx, PC_ERR_INVALID, "cannot run more stages than devices");
+    if (c.S > ctx->nb) return fail(ctx, PC_ERR_INVALID, "cannot cut the blocks into that many stages");
+    if (c.D > MAX_D_KEY) return fail(ctx, PC_ERR_CAPACITY, "device count beyond the packed back-pointer range");
+    return PC_OK;
+}
+
+static inline int64_t tri_sum(int64_t n) { return n * (n + 1) / 2; }
+
+// Runs one batch of DP calls whose buffers fit; fills outs[orig] for each.
+static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::vector<int> &idx,
+                     int64_t BS, int pruning, int want_iter, std::vector<CallOut> &outs) {
+    const DevProblem &P = ctx->P;
+    const int nb = ctx->nb;
+    const int n = (int)idx.size();
+    // order by S descending (stable)
+    std::vector<int> order(idx);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return calls[a].S > calls[b].S; });
+    // keys
+    std::vector<std::pair<int64_t, int>> want;
+    std::vector<std::vector<std::pair<int64_t, int>>> call_keys(n);
+    for (int i = 0; i < n; ++i) {
+        const pc_call &c = calls[order[i]];
+        const int ckpt = P.checkpointing && c.S > 1;
+        const int B = c.D - c.S + 1;
+        call_keys[i].resize(B + 1, {0, -1});
+        for (int dev = 1; dev <= B; ++dev) {
+            const int64_t m = BS / ((int64_t)c.MB * c.R * dev);
+            if (m >= 1) {
+                call_keys[i][dev] = {m, ckpt};
+                want.push_back({m, ckpt});
+            }
+        }
+    }
+    std::sort(want.begin(), want.end());
+    want.erase(std::unique(want.begin(), want.end()), want.end());
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->st));
+    if (int rc = ensure_keys(ctx, want)) return rc;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->st));
+    // call descriptors
+    std::vector<CallDesc> cds(n);
+    std::vector<int16_t> keyidx;
+    std::vector<int64_t> warp_prefix(n + 1, 0);
+    int64_t val_cells = 0, hist_cells = 0;
+    int maxS = 0;
+    for (int i = 0; i < n; ++i) {
+        const pc_call &c = calls[order[i]];
+        CallDesc &cd = cds[i];
+        cd.S = c.S; cd.D = c.D; cd.R = c.R; cd.MB = c.MB;
+        cd.A = nb - c.S + 1;
+        cd.B = c.D - c.S + 1;
+        cd.ckpt = P.checkpointing && c.S > 1;
+        cd.key_off = (int32_t)keyidx.size();
+        for (int dev = 0; dev <= cd.B; ++dev) {
+            int16_t k = -1;
+            if (dev >= 1 && call_keys[i][dev].second >= 0) k = (int16_t)ctx->key_map[call_keys[i][dev]];
+            keyidx.push_back(k);
+        }
+        cd.val_off = val_cells;
+        cd.hist_off = hist_cells;
+        cd.orig = order[i];
+        cd.pad = 0;
+        const int64_t cells = (int64_t)cd.A * cd.B;
+        val_cells += cells;
+        hist_cells += cells * cd.S;
+        warp_prefix[i + 1] = warp_prefix[i] + (int64_t)((cd.A + 31) / 32) * cd.B;
+        maxS = std::max(maxS, cd.S);
+    }
+    CUDA_TRY(ctx, ctx->calls_d.ensure(sizeof(CallDesc) * n));
+    CUDA_TRY(ctx, ctx->warp_prefix_d.ensure(sizeof(int64_t) * (n + 1)));
+    CUDA_TRY(ctx, ctx->keyidx_d.ensure(sizeof(int16_t) * keyidx.size() + 16));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->calls_d.p, cds.data(), sizeof(CallDesc) * n, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->warp_prefix_d.p, warp_prefix.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->keyidx_d.p, keyidx.data(), sizeof(int16_t) * keyidx.size(), cudaMemcpyHostToDevice, ctx->st));
+
+    const size_t nk = ctx->keys.size();
+    int FL = 4;
+    DPBatch bt{};
+    float dp_ms = 0;
+    bool first_pass = true;
+    for (;;) {
+        // buffers for this frontier capacity
+        const size_t val_bytes = 2 * ((size_t)val_cells * (16 * (size_t)FL + 1) + 64);
+        const size_t hist_bytes = (size_t)hist_cells * (4 * (size_t)FL + 1) + 64;
+        CUDA_TRY(ctx, ctx->val_d.ensure(val_bytes));
+        CUDA_TRY(ctx, ctx->hist_d.ensure(hist_bytes));
+        CUDA_TRY(ctx, ctx->overflow_d.ensure(sizeof(int)));
+        char *vb = ctx->val_d.as<char>();
+        bt.nb = nb;
+        bt.n_calls = n;
+        bt.calls = ctx->calls_d.as<CallDesc>();
+        bt.warp_prefix = ctx->warp_prefix_d.as<int64_t>();
+        bt.keyidx = ctx->keyidx_d.as<int16_t>();
+        bt.key_tfc = (const double *const *)ctx->key_ptrs.p;
+        bt.key_tbc = ((const double *const *)ctx->key_ptrs.p) + nk;
+        bt.tri = tri_size(nb);
+        bt.n_inter = P.n_inter;
+        bt.num_nodes = P.num_nodes;
+        bt.dpn = P.dpn;
+        bt.val_cells = val_cells;
+        for (int par = 0; par < 2; ++par) {
+            char *base = vb + par * (val_bytes / 2);
+            bt.val_tf[par] = (double *)base;
+            bt.val_tb[par] = (double *)(base + 8 * (size_t)FL * val_cells);
+            bt.val_cnt[par] = (uint8_t *)(base + 16 * (size_t)FL * val_cells);
+        }
+        char *hb = ctx->hist_d.as<char>();
+        bt.hist_key = (uint32_t *)hb;
+        bt.hist_cnt = (uint8_t *)(hb + 4 * (size_t)FL * hist_cells);
+        bt.hist_cells = hist_cells;
+        bt.overflow = ctx->overflow_d.as<int>();
+        CUDA_TRY(ctx, cudaMemsetAsync(bt.overflow, 0, sizeof(int), ctx->st));
+        int64_t launches = 0;
+        for (int s = 1; s <= maxS; ++s) {
+            int n_active = 0;
+            while (n_active < n && cds[n_active].S >= s) ++n_active;
+            launch_dp_level(bt, s, n_active, warp_prefix[n_active], FL, ctx->st);
+            ++launches;
+        }
+        if (int rc = check_launch(ctx, "dp_level")) return rc;
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev2, ctx->st));
+        int ovf = 0;
+        CUDA_TRY(ctx, cudaMemcpyAsync(&ovf, bt.overflow, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ctx->ev1, ctx->ev2);
+        dp_ms += ms;
+        if (first_pass) {
+            float sms = 0;
+            cudaEventElapsedTime(&sms, ctx->ev0, ctx->ev1);
+            ctx->last_span_ms += sms;
+            first_pass = false;
+        }
+        ctx->last_dp_launches = launches;
+        if (!ovf) break;
+        if (FL == 4) FL = 16;
+        else if (FL == 16) FL = 32;
+        else return fail(ctx, PC_ERR_CAPACITY, "a Pareto frontier exceeded 32 entries");
+        CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->st));
+    }
+    ctx->last_dp_ms += dp_ms;
+
+    // ---- visits per (call, level)
+    std::vector<int64_t> level_off(n + 1, 0), row_prefix(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        level_off[i + 1] = level_off[i] + cds[i].S;
+        row_prefix[i + 1] = row_prefix[i] + (int64_t)cds[i].S * cds[i].A;
+    }
+    CUDA_TRY(ctx, ctx->level_off_d.ensure(sizeof(int64_t) * (n + 1)));
+    CUDA_TRY(ctx, ctx->row_prefix_d.ensure(sizeof(int64_t) * (n + 1)));
+    CUDA_TRY(ctx, ctx->level_sums_d.ensure(sizeof(int64_t) * level_off[n] + 8));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->level_off_d.p, level_off.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->row_prefix_d.p, row_prefix.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->level_sums_d.p, 0, sizeof(int64_t) * level_off[n], ctx->st));
+    launch_row_visits(bt, pruning, ctx->level_sums_d.as<int64_t>(), ctx->row_prefix_d.as<int64_t>(),
+                      ctx->level_off_d.as<int64_t>(), row_prefix[n], ctx->st);
+    if (int rc = check_launch(ctx, "visits")) return rc;
+
+    // ---- backtrack (plan offsets in sorted order, compact)
+    std::vector<int32_t> plan_off_orig(calls.size(), 0);
+    int32_t seg_total = 0;
+    for (int i = 0; i < n; ++i) {
+        plan_off_orig[cds[i].orig] = seg_total;
+        seg_total += cds[i].S;
+    }
+    CUDA_TRY(ctx, ctx->plan_off_d.ensure(sizeof(int32_t) * calls.size()));
+    CUDA_TRY(ctx, ctx->seg_d.ensure(sizeof(int32_t) * 3 * (size_t)seg_total + 16));
+    CUDA_TRY(ctx, ctx->objective_d.ensure(sizeof(double) * calls.size()));
+    CUDA_TRY(ctx, ctx->feasible_d.ensure(sizeof(int32_t) * calls.size()));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->plan_off_d.p, plan_off_orig.data(), sizeof(int32_t) * calls.size(), cudaMemcpyHostToDevice, ctx->st));
+    int32_t *seg = ctx->seg_d.as<int32_t>();
+    launch_backtrack(bt, FL, BS, ctx->plan_off_d.as<int32_t>(), seg, seg + seg_total, seg + 2 * seg_total,
+                     ctx->objective_d.as<double>(), ctx->feasible_d.as<int32_t>(), ctx->st);
+    if (int rc = check_launch(ctx, "backtrack")) return rc;
+    std::vector<int64_t> level_sums(level_off[n]);
+    std::vector<int32_t> segs(3 * (size_t)seg_total), feas(calls.size(), 0);
+    std::vector<double> objs(calls.size(), NAN);
+    CUDA_TRY(ctx, cudaMemcpyAsync(level_sums.data(), ctx->level_sums_d.p, sizeof(int64_t) * level_off[n], cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(segs.data(), seg, sizeof(int32_t) * 3 * (size_t)seg_total, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(feas.data(), ctx->feasible_d.p, sizeof(int32_t) * calls.size(), cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(objs.data(), ctx->objective_d.p, sizeof(double) * calls.size(), cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+
+    // ---- stage records + simulation for feasible calls
+    std::vector<int32_t> qlo, qhi, qck, poff, pS, pR, pMB;
+    std::vector<int64_t> qm;
+    std::vector<int> feas_orig;
+    int maxS_f = 1;
+    for (int i = 0; i < n; ++i) {
+        const int o = cds[i].orig;
+        if (!feas[o]) continue;
+        feas_orig.push_back(o);
+        poff.push_back((int32_t)qlo.size());
+        pS.push_back(cds[i].S);
+        pR.push_back(cds[i].R);
+        pMB.push_back(cds[i].MB);
+        maxS_f = std::max(maxS_f, cds[i].S);
+        const int32_t off = plan_off_orig[o];
+        for (int k = 0; k < cds[i].S; ++k) {
+            const int32_t dev = segs[2 * (size_t)seg_total + off + k];
+            qlo.push_back(segs[off + k]);
+            qhi.push_back(segs[(size_t)seg_total + off + k]);
+            qm.push_back(BS / ((int64_t)cds[i].MB * cds[i].R * dev));
+            qck.push_back(cds[i].ckpt);
+        }
+    }
+    const int nq = (int)qlo.size();
+    const int np = (int)feas_orig.size();
+    std::vector<double> qtf(nq), qtb(nq), iters(np, NAN);
+    std::vector<int64_t> qmem(nq);
+    if (nq > 0) {
+        // inputs: lo hi ck poff pS pR pMB (int32), m (int64); outputs tf tb (f64) mem (i64) iter (f64)
+        size_t in_bytes = 4 * ((size_t)3 * nq + 4 * (size_t)np) + 8 * (size_t)nq + 64;
+        size_t out_bytes = 8 * (3 * (size_t)nq + (size_t)np) + 64;
+        CUDA_TRY(ctx, ctx->q_d.ensure(in_bytes));
+        CUDA_TRY(ctx, ctx->q_out_d.ensure(out_bytes));
+        char *qb = ctx->q_d.as<char>();
+        int64_t *d_m = (int64_t *)qb;
+        int32_t *d_lo = (int32_t *)(qb + 8 * (size_t)nq);
+        int32_t *d_hi = d_lo + nq;
+        int32_t *d_ck = d_hi + nq;
+        int32_t *d_poff = d_ck + nq;
+        int32_t *d_S = d_poff + np;
+        int32_t *d_R = d_S + np;
+        int32_t *d_MB = d_R + np;
+        double *o_tf = ctx->q_out_d.as<double>();
+        double *o_tb = o_tf + nq;
+        int64_t *o_mem = (int64_t *)(o_tb + nq);
+        double *o_it = (double *)(o_mem + nq);
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_m, qm.data(), 8 * (size_t)nq, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_lo, qlo.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_hi, qhi.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_ck, qck.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_poff, poff.data(), 4 * (size_t)np, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_S, pS.data(), 4 * (size_t)np, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_R, pR.data(), 4 * (size_t)np, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_MB, pMB.data(), 4 * (size_t)np, cudaMemcpyHostToDevice, ctx->st));
+        launch_profile_queries(P, nq, d_lo, d_hi, d_m, d_ck, o_tf, o_tb, o_mem, ctx->st);
+        if (int rc = check_launch(ctx, "profile_queries")) return rc;
+        if (want_iter) {
+            // seg_dev of the compact layout: rebuild from queries' m? use a device copy
+            std::vector<int32_t> qdev(nq);
+            for (int pi = 0, q = 0; pi < np; ++pi) {
+                const int o = feas_orig[pi];
+                const int32_t off = plan_off_orig[o];
+                for (int k = 0; k < pS[pi]; ++k, ++q) qdev[q] = segs[2 * (size_t)seg_total + off + k];
+            }
+            CUDA_TRY(ctx, ctx->sim_d.ensure(4 * (size_t)nq + 16));
+            CUDA_TRY(ctx, cudaMemcpyAsync(ctx->sim_d.p, qdev.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, ctx->st));
+            launch_simulate(P, np, d_poff, d_S, d_R, d_MB, BS, d_lo, d_hi, ctx->sim_d.as<int32_t>(),
+                            o_tf, o_tb, o_it, ctx->st, maxS_f);
+            if (int rc = check_launch(ctx, "simulate")) return rc;
+            CUDA_TRY(ctx, cudaMemcpyAsync(iters.data(), o_it, 8 * (size_t)np, cudaMemcpyDeviceToHost, ctx->st));
+            CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        }
+        CUDA_TRY(ctx, cudaMemcpyAsync(qtf.data(), o_tf, 8 * (size_t)nq, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(qtb.data(), o_tb, 8 * (size_t)nq, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(qmem.data(), o_mem, 8 * (size_t)nq, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    }
+
+    // ---- fill outputs
+    std::vector<int> fpos(calls.size(), -1);
+    for (int pi = 0; pi < np; ++pi) fpos[feas_orig[pi]] = pi;
+    for (int i = 0; i < n; ++i) {
+        const CallDesc &cd = cds[i];
+        const int o = cd.orig;
+        CallOut &out = outs[o];
+        out.level_sums.assign(level_sums.begin() + level_off[i], level_sums.begin() + level_off[i + 1]);
+        out.visits = 0;
+        for (auto v : out.level_sums) out.visits += v;
+        out.visits_unpruned = (int64_t)cd.S * tri_sum(cd.A) * tri_sum(cd.B);
+        out.feasible = feas[o];
+        out.lo.clear(); out.hi.clear(); out.dev.clear(); out.tf.clear(); out.tb.clear(); out.mem.clear();
+        if (feas[o]) {
+            const int pi = fpos[o];
+            out.objective = objs[o];
+            out.iteration = iters[pi];
+            const int32_t off = plan_off_orig[o];
+            for (int k = 0; k < cd.S; ++k) {
+                out.lo.push_back(segs[off + k]);
+                out.hi.push_back(segs[(size_t)seg_total + off + k]);
+                out.dev.push_back(segs[2 * (size_t)seg_total + off + k]);
+                out.tf.push_back(qtf[poff[pi] + k]);
+                out.tb.push_back(qtb[poff[pi] + k]);
+                out.mem.push_back(qmem[poff[pi] + k]);
+            }
+        }
+    }
+    ctx->last_calls = cds;
+    ctx->last_batch = bt;
+    ctx->last_pruning = pruning;
+    ctx->last_FL = FL;
+    ctx->last_pos.assign(calls.size(), -1);
+    for (int i = 0; i < n; ++i) ctx->last_pos[cds[i].orig] = i;
+    return PC_OK;
+}
+
+// Memory-bounded batching: consecutive calls (list order) are grouped while
+// their level buffers fit in half of the free device memory.
+static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_t BS, int pruning,
+                          int want_iter, std::vector<CallOut> &outs, int *n_chunks) {
+    if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
+    cudaSetDevice(ctx->device);
+    for (auto &c : calls)
+        if (int rc = validate_call(ctx, c, BS)) return rc;
+    outs.assign(calls.size(), CallOut());
+    ctx->last_dp_ms = 0;
+    ctx->last_span_ms = 0;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t cap = free_b / 2;
+    std::vector<int> cur;
+    size_t cur_bytes = 0;
+    *n_chunks = 0;
+    for (size_t i = 0; i < calls.size(); ++i) {
+        const pc_call &c = calls[i];
+        const int64_t A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
+        const size_t bytes = (size_t)A * B * (2 * (16 * 4 + 1) + (size_t)c.S * (4 * 4 + 1));
+        if (!cur.empty() && cur_bytes + bytes > cap) {
+            if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
+            ++*n_chunks;
+            cur.clear();
+            cur_bytes = 0;
+        }
+        cur.push_back((int)i);
+        cur_bytes += bytes;
+    }
+    if (!cur.empty()) {
+        if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
+        ++*n_chunks;
+    }
+    return PC_OK;
+}
+
+// Exact visits at the first cell where the running count exceeds budget,
+// scanning call `orig` of the last chunk in the reference order
+// (stages.py:212-216).  Returns -1 if the budget is not crossed in it.
+static int64_t crossing_in_call(pc_ctx *ctx, int orig, int64_t before, int64_t budget) {
+    if (orig < 0 || orig >= (int)ctx->last_pos.size() || ctx->last_pos[orig] < 0) return -2;
+    const CallDesc cd = ctx->last_calls[ctx->last_pos[orig]];
+    const int64_t cells = (int64_t)cd.A * cd.B;
+    std::vector<uint8_t> flags((size_t)cells * cd.S);
+    if (cudaMemcpy(flags.data(), ctx->last_batch.hist_cnt + cd.hist_off, flags.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -3;
+    int64_t run = before;
+    int d_min = 1;
+    for (int s = 1; s <= cd.S; ++s) {
+        if (s > 1) d_min = 1;
+        const uint8_t *lvl = flags.data() + (size_t)(s - 1) * cells;
+        for (int bi = 0; bi < cd.A; ++bi) {
+            const int b = s + bi;
+            const int bottom = std::max(d_min, s);
+            for (int d = cd.D - (cd.S - s); d >= bottom; --d) {
+                run += (int64_t)(b - s + 1) * (d - s + 1);
+                if (run > budget) return run;
+                const uint8_t v = lvl[(size_t)(d - s) * cd.A + bi];
+                if ((v & CNT_MASK) == 0 && ctx->last_pruning && !(v & CNT_ZERO)) {
+                    if (s == 1) d_min = d + 1;
+                    break;
+                }
+            }
+        }
+    }
+    return -1;
+}
+
+static void fill_plan(const CallOut &o, const pc_call &c, pc_plan *plan) {
+    plan->S = c.S;
+    plan->D = c.D;
+    plan->R = c.R;
+    plan->MB = c.MB;
+    plan->objective = o.objective;
+    plan->iteration_time = o.iteration;
+    plan->n_stages = o.feasible ? (int32_t)o.lo.size() : 0;
+    if (!o.feasible) return;
+    for (size_t k = 0; k < o.lo.size() && (int)k < plan->cap_stages; ++k) {
+        plan->lo[k] = o.lo[k];
+        plan->hi[k] = o.hi[k];
+        plan->devices[k] = o.dev[k];
+        plan->t_fwd[k] = o.tf[k];
+        plan->t_bwd[k] = o.tb[k];
+        plan->mem[k] = o.mem[k];
+    }
+}
+
+static void fill_stats(pc_ctx *ctx, pc_stats *stats, int64_t visits, int64_t calls, int64_t unpruned,
+                       int64_t cells) {
+    if (!stats) return;
+    stats->visits = visits;
+    stats->dp_calls = calls;
+    stats->visits_unpruned = unpruned;
+    stats->cells = cells;
+    stats->entries = 0;
+    stats->device_ms = ctx->last_dp_ms;
+    stats->span_ms = ctx->last_span_ms;
+}
+
+// =========================================================================== entry points
+extern "C" int pc_form_stage_dp(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_size, int32_t R,
+                                int32_t MB, int32_t disable_pruning, int64_t visit_budget,
+                                pc_plan *plan, pc_stats *stats) {
+    std::vector<pc_call> calls = {{S, D, R, MB}};
+    if (plan && S > plan->cap_stages && S <= ctx->nb) return fail(ctx, PC_ERR_CAPACITY, "plan capacity");
+    std::vector<CallOut> outs;
+    int chunks = 0;
+    if (int rc = run_calls_impl(ctx, calls, batch_size, !disable_pruning, 0, outs, &chunks)) return rc;
+    const CallOut &o = outs[0];
+    const int64_t cells = (int64_t)S * (ctx->nb - S + 1) * (D - S + 1);
+    if (visit_budget >= 0 && o.visits > visit_budget) {
+        const int64_t cross = crossing_in_call(ctx, 0, 0, visit_budget);
+        if (cross < 0) return fail(ctx, PC_ERR_CUDA, "budget crossing not found");
+        fill_stats(ctx, stats, cross, 1, o.visits_unpruned, cells);
+        return PC_ERR_BUDGET;
+    }
+    fill_stats(ctx, stats, o.visits, 1, o.visits_unpruned, cells);
+    if (plan) fill_plan(o, calls[0], plan);
+    return o.feasible ? PC_OK : PC_INFEASIBLE;
+}
+
+extern "C" int pc_run_calls(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
+                            int32_t disable_pruning, int32_t want_iteration,
+                            pc_call_result *results, pc_plan *plans, pc_stats *stats) {
+    std::vector<pc_call> cv(calls, calls + n);
+    std::vector<CallOut> outs;
+    int chunks = 0;
+    if (int rc = run_calls_impl(ctx, cv, batch_size, !disable_pruning, want_iteration, outs, &chunks)) return rc;
+    int64_t vis = 0, unp = 0, cells = 0;
+    for (int i = 0; i < n; ++i) {
+        const CallOut &o = outs[i];
+        results[i].feasible = o.feasible;
+        results[i].n_stages = o.feasible ? cv[i].S : 0;
+        results[i].objective = o.objective;
+        results[i].iteration_time = o.iteration;
+        results[i].visits = o.visits;
+        results[i].visits_unpruned = o.visits_unpruned;
+        results[i].budget_cross = -1;
+        if (plans) fill_plan(o, cv[i], &plans[i]);
+        vis += o.visits;
+        unp += o.visits_unpruned;
+        cells += (int64_t)cv[i].S * (ctx->nb - cv[i].S + 1) * (cv[i].D - cv[i].S + 1);
+    }
+    fill_stats(ctx, stats, vis, n, unp, cells);
+    return PC_OK;
+}
+
+// Budget crossing inside call `index` of the last pc_run_calls (single chunk).
+extern "C" int pc_last_crossing(pc_ctx *ctx, int32_t index, int64_t visits_before, int64_t budget,
+                                int64_t *visits_at_cross) {
+    int64_t r = crossing_in_call(ctx, index, visits_before, budget);
+    *visits_at_cross = r;
+    return r >= -1 ? PC_OK : fail(ctx, PC_ERR_INVALID, "call not in the last batch");
+}
+
+extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, int32_t disable_pruning,
+                             int64_t visit_budget, int32_t speculative, pc_plan *plan, pc_stats *stats) {
+    if (N < 1 || dpn < 1 || BS < 1)
+        return fail(ctx, PC_ERR_INVALID, "node count, devices per node and batch size must be at least 1");
+    if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
+    const int nb = ctx->nb;
+    // enumeration in the reference's order (stages.py:389-403)
+    std::vector<pc_call> calls;
+    std::vector<int> level_of;
+    std::vector<int> level_n;
+    for (int n = 1; n <= N; n *= 2) {
+        if (N % n) continue;
+        const int D = dpn * n, R = N / n;
+        const int lv = (int)level_n.size();
+        level_n.push_back(n);
+        for (int S = dpn * (n - 1) + 1; S <= D; ++S) {
+            if (S > nb) continue;
+            for (int64_t MB = 1; MB * R <= BS; MB *= 2) {
+                calls.push_back({S, D, R, (int32_t)MB});
+                level_of.push_back(lv);
+            }
+        }
+    }
+    const int n_levels = (int)level_n.size();
+    int64_t running = 0, calls_counted = 0, unpruned = 0, cells = 0;
+    int best = -1;
+    std::vector<CallOut> outs_all(calls.size());
+    auto process_level = [&](int lv, const std::vector<CallOut> &outs, const std::vector<int> &map) -> int {
+        // map: call index (global) -> index in outs
+        int lvl_best = -1;
+        for (size_t ci = 0; ci < calls.size(); ++ci) {
+            if (level_of[ci] != lv) continue;
+            const CallOut &o = outs[map[ci]];
+            ++calls_counted;
+            unpruned += o.visits_unpruned;
+            cells += (int64_t)calls[ci].S * (nb - calls[ci].S + 1) * (calls[ci].D - calls[ci].S + 1);
+            if (visit_budget >= 0 && running + o.visits > visit_budget) {
+                int64_t cross = crossing_in_call(ctx, map[ci], running, visit_budget);
+                if (cross < -1) {
+                    // flags of an earlier chunk are gone: recompute this call alone
+                    std::vector<pc_call> one = {calls[ci]};
+                    std::vector<CallOut> o1;
+                    int ch = 0;
+                    if (int rc = run_calls_impl(ctx, one, BS, !disable_pruning, 0, o1, &ch)) return rc;
+                    cross = crossing_in_call(ctx, 0, running, visit_budget);
+                }
+                if (cross < 0) return fail(ctx, PC_ERR_CUDA, "budget crossing not found");
+                fill_stats(ctx, stats, cross, calls_counted, unpruned, cells);
+                return PC_ERR_BUDGET;
+            }
+            running += o.visits;
+            if (!o.feasible) continue;
+            if (lvl_best < 0) {
+                lvl_best = (int)ci;
+                continue;
+            }
+            // min by (iteration_time, objective, microbatches), first wins (stages.py:407-411)
+            const CallOut &b = outs[map[lvl_best]];
+            const bool better = o.iteration < b.iteration ||
+                                (o.iteration == b.iteration &&
+                                 (o.objective < b.objective ||
+                                  (o.objective == b.objective && calls[ci].MB < calls[lvl_best].MB)));
+            if (better) lvl_best = (int)ci;
+        }
+        best = lvl_best;
+        return PC_OK;
+    };
+    int chunks = 0;
+    if (speculative) {
+        std::vector<CallOut> outs;
+        if (int rc = run_calls_impl(ctx, calls, BS, !disable_pruning, 1, outs, &chunks)) return rc;
+        if (chunks > 1 && visit_budget >= 0) {
+            // crossing lookups need the flags resident: fall back to per-level batches
+            speculative = 0;
+        } else {
+            std::vector<int> map(calls.size());
+            std::iota(map.begin(), map.end(), 0);
+            for (int lv = 0; lv < n_levels; ++lv) {
+                if (int rc = process_level(lv, outs, map)) return rc;
+                if (best >= 0) {
+                    fill_stats(ctx, stats, running, calls_counted, unpruned, cells);
+                    if (plan) fill_plan(outs[best], calls[best], plan);
+                    return PC_OK;
+                }
+            }
+            fill_stats(ctx, stats, running, calls_counted, unpruned, cells);
+            if (plan) plan->n_stages = 0;
+            return PC_INFEASIBLE;
+        }
+    }
+    running = calls_counted = unpruned = cells = 0;
+    double dp_ms = 0, span_ms = 0;
+    for (int lv = 0; lv < n_levels; ++lv) {
+        std::vector<pc_call> sub;
+        std::vector<int> map(calls.size(), -1);
+        for (size_t ci = 0; ci < calls.size(); ++ci)
+            if (level_of[ci] == lv) {
+                map[ci] = (int)sub.size();
+                sub.push_back(calls[ci]);
+            }
+        if (sub.empty()) continue;
+        std::vector<CallOut> outs;
+        if (int rc = run_calls_impl(ctx, sub, BS, !disable_pruning, 1, outs, &chunks)) return rc;
+        dp_ms += ctx->last_dp_ms;
+        span_ms += ctx->last_span_ms;
+        ctx->last_dp_ms = dp_ms;
+        ctx->last_span_ms = span_ms;
+        if (int rc = process_level(lv, outs, map)) return rc;
+        if (best >= 0) {
+            fill_stats(ctx, stats, running, calls_counted, unpruned, cells);
+            if (plan) fill_plan(outs[map[best]], calls[best], plan);
+            return PC_OK;
+        }
+    }
+    fill_stats(ctx, stats, running, calls_counted, unpruned, cells);
+    if (plan) plan->n_stages = 0;
+    return PC_INFEASIBLE;
+}
+
+extern "C" int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const int32_t *hi,
+                                const int64_t *m, const int32_t *ckpt, double *t_fwd, double *t_bwd,
+                                int64_t *mem) {
+    if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
+    cudaSetDevice(ctx->device);
+    for (int i = 0; i < n; ++i)
+        if (lo[i] < 0 || hi[i] <= lo[i] || hi[i] > ctx->nb || m[i] < 0)
+            return fail(ctx, PC_ERR_INVALID, "span out of range");
+    if (n == 0) return PC_OK;
+    size_t in_bytes = (8 + 4 * 3) * (size_t)n + 64;
+    CUDA_TRY(ctx, ctx->q_d.ensure(in_bytes));
+    CUDA_TRY(ctx, ctx->q_out_d.ensure(24 * (size_t)n + 64));
+    char *qb = ctx->q_d.as<char>();
+    int64_t *d_m = (int64_t *)qb;
+    int32_t *d_lo = (int32_t *)(qb + 8 * (size_t)n);
+    int32_t *d_hi = d_lo + n;
+    int32_t *d_ck = d_hi + n;
+    double *o_tf = ctx->q_out_d.as<double>();
+    double *o_tb = o_tf + n;
+    int64_t *o_mem = (int64_t *)(o_tb + n);
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_m, m, 8 * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_lo, lo, 4 * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_hi, hi, 4 * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_ck, ckpt, 4 * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
+    launch_profile_queries(ctx->P, n, d_lo, d_hi, d_m, d_ck, o_tf, o_tb, o_mem, ctx->st);
+    if (int rc = check_launch(ctx, "profile_queries")) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(t_fwd, o_tf, 8 * (size_t)n, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(t_bwd, o_tb, 8 * (size_t)n, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(mem, o_mem, 8 * (size_t)n, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    return PC_OK;
+}

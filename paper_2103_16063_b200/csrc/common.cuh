@@ -1,0 +1,161 @@
+// Shared declarations of the pipecut_b200 CUDA library (sm_100a).
+//
+// Numeric parity rules, enforced everywhere here:
+//   * every fp64 operation is an explicit __d*_rn intrinsic and the library
+//     is compiled with -fmad=false, so nothing is contracted into an FMA;
+//   * (f*m)/F in that order (costs.py:137), beta*x (costs.py:138);
+//   * comm_time = lat + (double)bytes / bw, division first (costs.py:86);
+//   * boundary bytes = trunc(fixed + m*ps) in fp64 (blocks.py:331);
+//   * mem = (int64)((double)param * ((1+g)+o) + (double)act) (costs.py:158).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pipecut_b200.h"
+
+namespace pcb {
+
+// ------------------------------------------------------------------ device problem
+struct DevProblem {
+    int nb = 0, n_tasks = 0, n_in = 0;
+    int num_nodes = 1, dpn = 1, checkpointing = 0, monotone = 0;
+    int n_inter = 1;                 // 2 when num_nodes > 1 (intra / inter cut variants)
+    int64_t mem_budget = 0;
+    double flops = 1, beta = 2, factor = 4, bw_intra = 1, bw_inter = 1, lat = 0;
+    // tasks (sorted node-id order)
+    const int32_t *task_block = nullptr;
+    const double *task_flops = nullptr;
+    const int64_t *fp_fix = nullptr, *fp_ps = nullptr;
+    const int32_t *dep_off = nullptr, *dep_ob = nullptr;
+    const int64_t *dep_fix = nullptr, *dep_ps = nullptr;
+    // block -> task CSR (task indices ascending)
+    const int32_t *blk_off = nullptr, *blk_tasks = nullptr;
+    // span-input values
+    const int32_t *in_ob = nullptr, *in_cons_off = nullptr, *in_cons = nullptr;
+    const int64_t *in_fix = nullptr, *in_ps = nullptr;
+    // prefix sums over blocks [nb+1]
+    const int64_t *pre_param = nullptr, *pre_res_fix = nullptr, *pre_res_ps = nullptr;
+    // boundary arrays [nb+1]
+    const int64_t *cut_fixed = nullptr;
+    const double *cut_ps = nullptr;
+    // span input tables, triangular [tri(nb)]
+    const int64_t *in_tab_fix = nullptr, *in_tab_ps = nullptr;
+};
+
+// Triangular span index, rows by lo with hi contiguous:
+// row lo holds hi = lo+1 .. nb.
+__host__ __device__ inline int64_t tri_row(int64_t lo, int64_t nb) {
+    return lo * nb - (lo * (lo - 1)) / 2;
+}
+__host__ __device__ inline int64_t tri_idx(int64_t lo, int64_t hi, int64_t nb) {
+    return tri_row(lo, nb) + (hi - lo - 1);
+}
+__host__ __device__ inline int64_t tri_size(int64_t nb) { return nb * (nb + 1) / 2; }
+
+// _Profiler.cut_time (stages.py:147-157) given the inter-node flag.
+__device__ inline double cut_time_dev(const DevProblem &p, int cut, int64_t m, int inter) {
+    double s = __dadd_rn((double)p.cut_fixed[cut], __dmul_rn((double)m, p.cut_ps[cut]));
+    double nbytes = trunc(s);
+    double bw = inter ? p.bw_inter : p.bw_intra;
+    return __dadd_rn(p.lat, __ddiv_rn(nbytes, bw));
+}
+
+__host__ __device__ inline int inter_of(int num_nodes, int dpn, int64_t cum) {
+    return (num_nodes > 1 && (cum % dpn) == 0) ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ key tables
+// One (microbatch share m, checkpointing) key: DP-ready span tables with the
+// boundary transfer already charged (stages.py:232-237):
+//   tfc[inter][tri(lo,hi)] = t_fwd + (hi<nb ? cut_time(hi, m, inter) : 0), NaN if mem > budget
+//   tbc[inter][tri(lo,hi)] = t_bwd + (lo>0  ? cut_time(lo, m, inter) : 0)
+struct KeyTable {
+    int64_t m = 0;
+    int ckpt = 0;
+    double *tfc = nullptr;
+    double *tbc = nullptr;
+};
+
+// ------------------------------------------------------------------ DP batch
+// One DP call in a level-synchronous batch.  Calls are ordered by S
+// descending so the calls still active at level s are a prefix.
+struct CallDesc {
+    int32_t S, D, R, MB;
+    int32_t A, B;              // b-range and d-range sizes: nb-S+1, D-S+1
+    int32_t ckpt;
+    int32_t key_off;           // keyidx[key_off + dev], dev in [1, B]
+    int64_t val_off;           // cell offset of this call in the ping-pong value buffers
+    int64_t hist_off;          // cell offset of level 1 in the history buffers
+    int32_t orig;              // index in the caller's call list
+    int32_t pad;
+};
+
+struct DPBatch {
+    int nb;
+    int n_calls;
+    const CallDesc *calls;
+    const int64_t *warp_prefix;     // [n_calls+1] warps per call (chunks of 32 b x B)
+    const int16_t *keyidx;          // -1 = zero share
+    const double *const *key_tfc;   // device array of per-key table pointers
+    const double *const *key_tbc;
+    int64_t tri;                    // tri_size(nb)
+    int n_inter;
+    int num_nodes, dpn;
+    // ping-pong values: [2][FL][val_cells] doubles, counts [2][val_cells]
+    double *val_tf[2];
+    double *val_tb[2];
+    uint8_t *val_cnt[2];
+    int64_t val_cells;
+    // history: keys [FL][hist_cells] (per level/cell slot), counts [hist_cells]
+    uint32_t *hist_key;
+    uint8_t *hist_cnt;
+    int64_t hist_cells;
+    int *overflow;                  // set when a frontier exceeded FL
+};
+
+// count byte: bits 0-5 entries, bit 6 overflow, bit 7 saw_zero_share
+constexpr uint8_t CNT_MASK = 0x3f;
+constexpr uint8_t CNT_OVF = 0x40;
+constexpr uint8_t CNT_ZERO = 0x80;
+
+// packed back-pointer (bp, dp, idx): lexicographic order == integer order
+__host__ __device__ inline uint32_t pack_key(uint32_t bp, uint32_t dp, uint32_t idx) {
+    return (bp << 17) | (dp << 5) | idx;
+}
+__host__ __device__ inline int key_bp(uint32_t k) { return (int)(k >> 17); }
+__host__ __device__ inline int key_dp(uint32_t k) { return (int)((k >> 5) & 0xfff); }
+__host__ __device__ inline int key_idx(uint32_t k) { return (int)(k & 31); }
+constexpr int MAX_NB_KEY = (1 << 15) - 1;
+constexpr int MAX_D_KEY = (1 << 12) - 1;
+
+// ------------------------------------------------------------------ launchers
+// span.cu
+void launch_in_tables(const DevProblem &p, int64_t *in_fix, int64_t *in_ps, cudaStream_t st);
+void launch_span_time_general(const DevProblem &p, int n_keys, const int64_t *keys_m,
+                              double *raw_tf, double *raw_tb, cudaStream_t st);
+void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_m,
+                           const int32_t *keys_ckpt, const double *raw_tf, const double *raw_tb,
+                           double *const *tfc, double *const *tbc, cudaStream_t st);
+void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
+                            const int64_t *m, const int32_t *ckpt, double *tf, double *tb,
+                            int64_t *mem, cudaStream_t st);
+// dp.cu
+void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_warps, int FL,
+                     cudaStream_t st);
+void launch_row_visits(const DPBatch &b, int pruning, int64_t *level_sums, int64_t *row_sums,
+                       const int64_t *level_row_off, int64_t n_rows_total, cudaStream_t st);
+void launch_backtrack(const DPBatch &b, int FL, int64_t batch_size, const int32_t *plan_off,
+                      int32_t *seg_lo, int32_t *seg_hi, int32_t *seg_dev, double *objective,
+                      int32_t *feasible, cudaStream_t st);
+// sim.cu
+void launch_simulate(const DevProblem &p, int n_plans, const int32_t *plan_off,
+                     const int32_t *plan_S, const int32_t *plan_R, const int32_t *plan_MB,
+                     int64_t batch_size, const int32_t *seg_lo, const int32_t *seg_hi,
+                     const int32_t *seg_dev, const double *st_tf, const double *st_tb,
+                     double *iteration, cudaStream_t st, int max_S);
+
+}  // namespace pcb

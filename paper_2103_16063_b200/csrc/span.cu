@@ -1,0 +1,235 @@
+// K1/K2: span-cost and cut-time tables.
+//
+// Replaces _Profiler.record -> CostModel.profile(BlockSet.span(lo, hi), m, ckpt)
+// (pkg/src/pipecut/stages.py:138-145, costs.py:97-160, blocks.py:333-343) and
+// _Profiler.cut_time (stages.py:147-157) for every span of a BlockSet and every
+// (m, ckpt) key a batch of DP calls needs.  The flat restatement the kernels
+// evaluate is documented in paper_2103_16063_b200/flatten.py.
+#include "common.cuh"
+
+namespace pcb {
+
+// ---------------------------------------------------------------- input tables
+// in(lo, hi) = sum over span-input values v of (fix, ps):
+//   v counts iff ob(v) < lo and cstar(v, lo) < hi, cstar = first consumer block >= lo
+// One CTA per lo scatters every value into a delta array over cstar and
+// prefix-sums it over hi.  Integer sums: order-free, exact.
+__global__ void k_in_tables(DevProblem p, int64_t *out_fix, int64_t *out_ps) {
+    extern __shared__ int64_t sm[];
+    const int nb = p.nb;
+    const int lo = blockIdx.x;
+    int64_t *dfix = sm;            // [nb]
+    int64_t *dps = sm + nb;        // [nb]
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) { dfix[i] = 0; dps[i] = 0; }
+    __syncthreads();
+    for (int v = threadIdx.x; v < p.n_in; v += blockDim.x) {
+        if (p.in_ob[v] >= lo) continue;
+        for (int k = p.in_cons_off[v]; k < p.in_cons_off[v + 1]; ++k) {
+            int c = p.in_cons[k];
+            if (c >= lo) {
+                atomicAdd((unsigned long long *)&dfix[c], (unsigned long long)p.in_fix[v]);
+                atomicAdd((unsigned long long *)&dps[c], (unsigned long long)p.in_ps[v]);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t af = 0, ap = 0;
+        const int64_t row = tri_row(lo, nb);
+        for (int hi = lo + 1; hi <= nb; ++hi) {
+            af += dfix[hi - 1];
+            ap += dps[hi - 1];
+            out_fix[row + (hi - lo - 1)] = af;
+            out_ps[row + (hi - lo - 1)] = ap;
+        }
+    }
+}
+
+void launch_in_tables(const DevProblem &p, int64_t *in_fix, int64_t *in_ps, cudaStream_t st) {
+    size_t smem = sizeof(int64_t) * 2 * (size_t)p.nb;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_in_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_in_tables<<<p.nb, 256, smem, st>>>(p, in_fix, in_ps);
+}
+
+// ---------------------------------------------------------------- time folds
+// General (non-monotone) fold: one warp per (key, lo, 32 consecutive hi).
+// All lanes walk the sorted task list together (costs.py:120) and each lane
+// adds the tasks with lo <= block < its hi, so the fp64 fold order is the
+// reference's exactly.
+__global__ void k_span_time_general(DevProblem p, int n_keys, const int64_t *keys_m,
+                                    double *raw_tf, double *raw_tb) {
+    const int nb = p.nb;
+    const int chunks = (nb + 31) / 32;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t per_key = (int64_t)nb * chunks;
+    if (gw >= per_key * n_keys) return;
+    const int k = (int)(gw / per_key);
+    const int rem = (int)(gw % per_key);
+    const int lo = rem / chunks;
+    const int chunk = rem % chunks;
+    if (lo + 1 + chunk * 32 > nb) return;
+    const int hi = lo + 1 + chunk * 32 + lane;
+    const double m = (double)keys_m[k];
+    double tf = 0.0, tb = 0.0;
+    for (int t = 0; t < p.n_tasks; ++t) {
+        const int b = p.task_block[t];
+        if (b < lo) continue;
+        const double x = __ddiv_rn(__dmul_rn(p.task_flops[t], m), p.flops);
+        const double y = __dmul_rn(p.beta, x);
+        if (b < hi) {
+            tf = __dadd_rn(tf, x);
+            tb = __dadd_rn(tb, y);
+        }
+    }
+    if (hi <= nb) {
+        const int64_t idx = (int64_t)k * tri_size(nb) + tri_idx(lo, hi, nb);
+        raw_tf[idx] = tf;
+        raw_tb[idx] = tb;
+    }
+}
+
+void launch_span_time_general(const DevProblem &p, int n_keys, const int64_t *keys_m,
+                              double *raw_tf, double *raw_tb, cudaStream_t st) {
+    const int chunks = (p.nb + 31) / 32;
+    const int64_t warps = (int64_t)n_keys * p.nb * chunks;
+    const int wpb = 8;
+    const int64_t blocks = (warps + wpb - 1) / wpb;
+    k_span_time_general<<<(unsigned)blocks, wpb * 32, 0, st>>>(p, n_keys, keys_m, raw_tf, raw_tb);
+}
+
+// ---------------------------------------------------------------- span rows
+// One thread per (key, lo) sweeps hi = lo+1..nb:
+//   * running max of task footprints (costs.py:150-155), each task's
+//     footprint counting only predecessors owned in blocks >= lo;
+//   * in the monotone case the time fold itself (blocks in sorted-id order,
+//     so extending hi continues the reference's fold exactly);
+//   * memory (costs.py:157-159) and the DP-ready tables with cut times.
+template <bool MONO>
+__global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
+                            const int32_t *keys_ckpt, const double *raw_tf,
+                            const double *raw_tb, double *const *tfc, double *const *tbc) {
+    const int nb = p.nb;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (int64_t)n_keys * nb) return;
+    const int k = (int)(gid / nb);
+    const int lo = (int)(gid % nb);
+    const int64_t m = keys_m[k];
+    const double md = (double)m;
+    const int ckpt = keys_ckpt[k];
+    const int64_t tri = tri_size(nb);
+    double *out_f = tfc[k];
+    double *out_b = tbc[k];
+    double tf = 0.0, tb = 0.0;
+    int64_t run_fp = 0;
+    double cutb[2] = {0.0, 0.0};
+    if (lo > 0)
+        for (int i = 0; i < p.n_inter; ++i) cutb[i] = cut_time_dev(p, lo, m, i);
+    const int64_t row = tri_row(lo, nb);
+    for (int hi = lo + 1; hi <= nb; ++hi) {
+        const int blk = hi - 1;
+        for (int q = p.blk_off[blk]; q < p.blk_off[blk + 1]; ++q) {
+            const int t = p.blk_tasks[q];
+            int64_t fp = p.fp_fix[t] + m * p.fp_ps[t];
+            for (int d = p.dep_off[t]; d < p.dep_off[t + 1]; ++d)
+                if (p.dep_ob[d] >= lo) fp += p.dep_fix[d] + m * p.dep_ps[d];
+            run_fp = fp > run_fp ? fp : run_fp;
+            if (MONO) {
+                const double x = __ddiv_rn(__dmul_rn(p.task_flops[t], md), p.flops);
+                const double y = __dmul_rn(p.beta, x);
+                tf = __dadd_rn(tf, x);
+                tb = __dadd_rn(tb, y);
+            }
+        }
+        const int64_t idx = row + (hi - lo - 1);
+        double f = tf, b = tb;
+        if (!MONO) {
+            f = raw_tf[(int64_t)k * tri + idx];
+            b = raw_tb[(int64_t)k * tri + idx];
+        }
+        const int64_t param = p.pre_param[hi] - p.pre_param[lo];
+        const int64_t inb = p.in_tab_fix[idx] + m * p.in_tab_ps[idx];
+        const int64_t res = (p.pre_res_fix[hi] - p.pre_res_fix[lo]) +
+                            m * (p.pre_res_ps[hi] - p.pre_res_ps[lo]);
+        const int64_t act = inb + (ckpt ? run_fp : res);
+        const double memd = __dadd_rn(__dmul_rn((double)param, p.factor), (double)act);
+        const int64_t mem = (int64_t)memd;
+        const bool ok = mem <= p.mem_budget;                   // stages.py:230
+        for (int i = 0; i < p.n_inter; ++i) {
+            double ff = f;
+            if (hi < nb) ff = __dadd_rn(f, cut_time_dev(p, hi, m, i));
+            double bb = b;
+            if (lo > 0) bb = __dadd_rn(b, cutb[i]);
+            out_f[(int64_t)i * tri + idx] = ok ? ff : __longlong_as_double(0x7ff8000000000000LL);
+            out_b[(int64_t)i * tri + idx] = bb;
+        }
+    }
+}
+
+void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_m,
+                           const int32_t *keys_ckpt, const double *raw_tf, const double *raw_tb,
+                           double *const *tfc, double *const *tbc, cudaStream_t st) {
+    const int64_t n = (int64_t)n_keys * p.nb;
+    const int tpb = 128;
+    const unsigned blocks = (unsigned)((n + tpb - 1) / tpb);
+    if (p.monotone)
+        k_span_rows<true><<<blocks, tpb, 0, st>>>(p, n_keys, keys_m, keys_ckpt, raw_tf, raw_tb,
+                                                 tfc, tbc);
+    else
+        k_span_rows<false><<<blocks, tpb, 0, st>>>(p, n_keys, keys_m, keys_ckpt, raw_tf, raw_tb,
+                                                  tfc, tbc);
+}
+
+// ---------------------------------------------------------------- queries
+// CostModel.profile(BlockSet.span(lo, hi), m, ckpt) for arbitrary queries,
+// one thread each (stage records of a plan, BlockSet.costs, tests).
+__global__ void k_profile_queries(DevProblem p, int n, const int32_t *qlo, const int32_t *qhi,
+                                  const int64_t *qm, const int32_t *qckpt, double *otf,
+                                  double *otb, int64_t *omem) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int lo = qlo[i], hi = qhi[i];
+    const int64_t m = qm[i];
+    const double md = (double)m;
+    double tf = 0.0, tb = 0.0;
+    int t0 = 0, t1 = p.n_tasks;
+    if (p.monotone) { t0 = p.blk_off[lo]; t1 = p.blk_off[hi]; }
+    for (int t = t0; t < t1; ++t) {
+        const int b = p.task_block[t];
+        if (b < lo || b >= hi) continue;
+        const double x = __ddiv_rn(__dmul_rn(p.task_flops[t], md), p.flops);
+        const double y = __dmul_rn(p.beta, x);
+        tf = __dadd_rn(tf, x);
+        tb = __dadd_rn(tb, y);
+    }
+    int64_t run_fp = 0;
+    for (int blk = lo; blk < hi; ++blk)
+        for (int q = p.blk_off[blk]; q < p.blk_off[blk + 1]; ++q) {
+            const int t = p.blk_tasks[q];
+            int64_t fp = p.fp_fix[t] + m * p.fp_ps[t];
+            for (int d = p.dep_off[t]; d < p.dep_off[t + 1]; ++d)
+                if (p.dep_ob[d] >= lo) fp += p.dep_fix[d] + m * p.dep_ps[d];
+            run_fp = fp > run_fp ? fp : run_fp;
+        }
+    const int64_t idx = tri_idx(lo, hi, p.nb);
+    const int64_t param = p.pre_param[hi] - p.pre_param[lo];
+    const int64_t inb = p.in_tab_fix[idx] + m * p.in_tab_ps[idx];
+    const int64_t res = (p.pre_res_fix[hi] - p.pre_res_fix[lo]) +
+                        m * (p.pre_res_ps[hi] - p.pre_res_ps[lo]);
+    const int64_t act = inb + (qckpt[i] ? run_fp : res);
+    const double memd = __dadd_rn(__dmul_rn((double)param, p.factor), (double)act);
+    otf[i] = tf;
+    otb[i] = tb;
+    omem[i] = (int64_t)memd;
+}
+
+void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
+                            const int64_t *m, const int32_t *ckpt, double *tf, double *tb,
+                            int64_t *mem, cudaStream_t st) {
+    if (n <= 0) return;
+    k_profile_queries<<<(n + 127) / 128, 128, 0, st>>>(p, n, lo, hi, m, ckpt, tf, tb, mem);
+}
+
+}  // namespace pcb

@@ -1,0 +1,118 @@
+"""Drop-in `form_stage_dp` / `form_stage` backed by the B200 stage DP.
+
+Same signatures, argument meaning, results and exceptions as the reference
+(pkg/src/pipecut/stages.py:282-291 and 372-413): callers pass a reference
+`BlockSet` and `SearchOptions`, and get the reference's own `SearchResult`,
+`Plan`, `StagePlan` and `SearchStats` back; `InvalidArgs` and
+`SearchBudgetExceeded` are the reference's classes.  All search arithmetic
+runs on the GPU through libpipecut_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+from . import _lib, abi
+from ._host import pipecut as _pc
+from .flatten import flatten_blockset
+
+_stages = _pc.stages
+InvalidArgs = _stages.InvalidArgs
+SearchBudgetExceeded = _stages.SearchBudgetExceeded
+SearchOptions = _stages.SearchOptions
+SearchResult = _stages.SearchResult
+SearchStats = _stages.SearchStats
+StagePlan = _stages.StagePlan
+Plan = _stages.Plan
+
+
+def bind_problem(ctx: _lib.Context, blocks):
+    """Upload the flattened BlockSet once per BlockSet object."""
+    owner = ctx.problem_owner() if ctx.problem_owner is not None else None
+    if owner is blocks:
+        return ctx.problem_flat
+    flat = flatten_blockset(blocks)
+    st = abi.problem_struct(flat)
+    ctx.check(ctx.lib.pc_set_problem(ctx.h, C.byref(st)), "pc_set_problem")
+    ctx.problem_owner = weakref.ref(blocks)
+    ctx.problem_flat = flat
+    return flat
+
+
+def _check_args(blocks, S, D, batch_size, replica_factor, microbatches):
+    # same messages as stages.py:160-168
+    if S < 1 or D < 1 or batch_size < 1 or replica_factor < 1 or microbatches < 1:
+        raise InvalidArgs("stage count, devices, batch size, replicas and "
+                          "microbatches must all be at least 1")
+    if S > D:
+        raise InvalidArgs(f"cannot run {S} stages on {D} devices")
+    if S > len(blocks):
+        raise InvalidArgs(f"cannot cut {len(blocks)} blocks into {S} stages")
+
+
+def plan_from_buffers(buf: abi.PlanBuffers, batch_size: int) -> Plan:
+    s = buf.s
+    R = int(s.R)
+    stages = tuple(
+        StagePlan(blocks=(int(buf.lo[i]), int(buf.hi[i])), devices=int(buf.devices[i]),
+                  replicas=int(buf.devices[i]) * R, t_fwd=float(buf.t_fwd[i]),
+                  t_bwd=float(buf.t_bwd[i]), mem=int(buf.mem[i]))
+        for i in range(int(s.n_stages)))
+    return Plan(stages=stages, microbatches=int(s.MB), replica_factor=R,
+                objective=float(s.objective), batch_size=int(batch_size),
+                devices_total=int(s.D))
+
+
+def _budget(opts) -> int:
+    return -1 if opts.visit_budget is None else int(opts.visit_budget)
+
+
+def form_stage_dp(blocks, S: int, D: int, batch_size: int, replica_factor: int,
+                  microbatches: int, options=None):
+    """Optimal S-stage assignment of the block list onto D devices (GPU)."""
+    _check_args(blocks, S, D, batch_size, replica_factor, microbatches)
+    opts = options or SearchOptions()
+    ctx = _lib.context()
+    bind_problem(ctx, blocks)
+    buf = abi.PlanBuffers(S)
+    st = abi.PcStats()
+    rc = ctx.lib.pc_form_stage_dp(ctx.h, S, D, batch_size, replica_factor, microbatches,
+                                  int(bool(opts.disable_pruning)), _budget(opts),
+                                  C.byref(buf.s), C.byref(st))
+    ctx.check(rc, "form_stage_dp")
+    if rc == abi.PC_ERR_BUDGET:
+        raise SearchBudgetExceeded(int(st.visits), int(opts.visit_budget))
+    stats = SearchStats(visits=int(st.visits), dp_calls=int(st.dp_calls))
+    plan = plan_from_buffers(buf, batch_size) if rc == abi.PC_OK else None
+    return SearchResult(plan, stats)
+
+
+def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
+               options=None, *, speculative: bool = True, last_stats: dict | None = None):
+    """Search replica factor, stage count and microbatch count together (GPU).
+
+    ``speculative`` evaluates every widening level in one device batch and
+    then applies the reference's first-feasible-level rule; the result and
+    the stats are identical to the level-by-level order either way.
+    """
+    if num_nodes < 1 or devices_per_node < 1 or batch_size < 1:
+        raise InvalidArgs("node count, devices per node and batch size must be at least 1")
+    opts = options or SearchOptions()
+    ctx = _lib.context()
+    bind_problem(ctx, blocks)
+    buf = abi.PlanBuffers(max(1, len(blocks)))
+    st = abi.PcStats()
+    rc = ctx.lib.pc_form_stage(ctx.h, num_nodes, devices_per_node, batch_size,
+                               int(bool(opts.disable_pruning)), _budget(opts),
+                               int(bool(speculative)), C.byref(buf.s), C.byref(st))
+    ctx.check(rc, "form_stage")
+    if last_stats is not None:
+        last_stats.update(visits=int(st.visits), dp_calls=int(st.dp_calls),
+                          visits_unpruned=int(st.visits_unpruned), cells=int(st.cells),
+                          device_ms=float(st.device_ms), span_ms=float(st.span_ms))
+    if rc == abi.PC_ERR_BUDGET:
+        raise SearchBudgetExceeded(int(st.visits), int(opts.visit_budget))
+    stats = SearchStats(visits=int(st.visits), dp_calls=int(st.dp_calls))
+    plan = plan_from_buffers(buf, batch_size) if rc == abi.PC_OK else None
+    return SearchResult(plan, stats)
