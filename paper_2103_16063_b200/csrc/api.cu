@@ -474,7 +474,8 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     bool first_pass = true;
     for (;;) {
         // buffers for this frontier capacity
-        const size_t val_bytes = 2 * ((size_t)val_cells * (16 * (size_t)FL + 1) + 64);
+        const size_t val_half = (((size_t)val_cells * (16 * (size_t)FL + 1) + 64) + 255) & ~size_t(255);
+        const size_t val_bytes = 2 * val_half;
         const size_t hist_bytes = (size_t)hist_cells * (4 * (size_t)FL + 1) + 64;
         CUDA_TRY(ctx, ctx->val_d.ensure(val_bytes));
         CUDA_TRY(ctx, ctx->hist_d.ensure(hist_bytes));
@@ -493,7 +494,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.dpn = P.dpn;
         bt.val_cells = val_cells;
         for (int par = 0; par < 2; ++par) {
-            char *base = vb + par * (val_bytes / 2);
+            char *base = vb + par * val_half;
             bt.val_tf[par] = (double *)base;
             bt.val_tb[par] = (double *)(base + 8 * (size_t)FL * val_cells);
             bt.val_cnt[par] = (uint8_t *)(base + 16 * (size_t)FL * val_cells);
