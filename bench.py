@@ -1,0 +1,391 @@
+"""Benchmark: DP cells/s of RaNNC's partition search (form_stage) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, NCCL)
+
+Workload (config.workload): the C5 DP scaling sweep point of BASELINE.json
+configs[4] -- an enlarged-BERT layer chain (one BERT-1024 layer per block,
++-10% seeded FLOP jitter), nb blocks on D devices (D/8 nodes x 8), batch 8*D,
+every (n, S, MB) call of form_stage evaluated (full enumeration), the plan
+chosen by the reference's first-feasible-level rule.  A step is one complete
+search.  DP cells/s = the reference's unpruned SearchStats.visits unit
+ / step time.  Multi-GPU: the calls are sharded (LPT) over the
+ranks, one NCCL all-gather of fixed-size records per step: strong scaling.
+
+value: problem resident on the device, span/cut tables rebuilt every step.
+e2e:   the public API form_stage_sharded() per step, including host
+       flattening, host->device upload of the problem and device->host results.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_NB = 1024
+DEFAULT_D = 256
+JITTER_SEED = 0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nb", type=int, default=DEFAULT_NB)
+    ap.add_argument("--D", type=int, default=DEFAULT_D)
+    ap.add_argument("--cpu-sample-sec", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(nb, D, calls, unpruned):
+    nodes, dpn = max(1, D // 8), min(8, D)
+    return {
+        "workload": f"C5 enlarged-BERT layer chain: nb={nb} blocks, D={D} devices "
+                    f"({nodes}x{dpn}), batch {8 * D}, full (n,S,MB) enumeration of form_stage",
+        "nb": nb, "devices": D, "batch": 8 * D, "calls": len(calls),
+        "unpruned_visits_per_step": unpruned, "jitter_seed": JITTER_SEED,
+        "parallelism": "calls sharded over GPUs (LPT), one NCCL all-gather",
+        "l2": "span/cut tables rebuilt each step (> L2); 512 MiB L2 flush between steps",
+    }
+
+
+# --------------------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, index):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        self.index = index
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        try:
+            rows = [l.split(",") for l in open(self.path) if l.strip()]
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if len(r) > 4 + i and r[3 + i].strip() == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- CPU legs
+def _ref_worker_init(nb, D):
+    global _REF_BS
+    from paper_2103_16063_b200.workloads import c5_blockset
+    _REF_BS = c5_blockset(nb, D, jitter_seed=JITTER_SEED)
+
+
+def _ref_worker_call(args):
+    """The reference's own form_stage_dp on one call of the workload, bounded
+    by a visit budget (it raises SearchBudgetExceeded after `budget` visits)."""
+    import pipecut
+    (S, D, R, MB), bs_batch, budget = args
+    t0 = time.perf_counter()
+    try:
+        res = pipecut.form_stage_dp(_REF_BS, S, D, bs_batch, R, MB,
+                                    pipecut.SearchOptions(disable_pruning=True,
+                                                          visit_budget=budget))
+        visits = res.stats.visits
+    except pipecut.SearchBudgetExceeded as exc:
+        visits = exc.visits
+    return visits, time.perf_counter() - t0
+
+
+def sample_calls(calls, k):
+    step = max(1, len(calls) // k)
+    return [calls[(i * step) % len(calls)] for i in range(k)]
+
+
+def cpu_reference_rate(nb, D, calls, seconds, cores):
+    """Reference visits/s on `cores` host processes, one budget-bounded call
+    each (budget sized from a short calibration to take ~`seconds`)."""
+    import multiprocessing as mp
+    _ref_worker_init(nb, D)
+    probe = sample_calls(calls, 1)[0]
+    v, t = _ref_worker_call((probe, 8 * D, 200_000))
+    rate = v / max(t, 1e-6)
+    budget = max(10_000, int(rate * seconds))
+    work = [(c, 8 * D, budget) for c in sample_calls(calls, cores)]
+    if cores == 1:
+        t0 = time.perf_counter()
+        out = [_ref_worker_call(w) for w in work]
+        wall = time.perf_counter() - t0
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(cores, initializer=_ref_worker_init, initargs=(nb, D)) as pool:
+            pool.map(_ref_worker_call, [(probe, 8 * D, 1000)] * cores)  # warm workers
+            t0 = time.perf_counter()
+            out = pool.map(_ref_worker_call, work)
+            wall = time.perf_counter() - t0
+    visits = sum(o[0] for o in out)
+    return visits / wall, budget, work
+
+
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2103_16063_b200._host import pipecut  # noqa: F401  (baseline/_ref)
+    from paper_2103_16063_b200.search import enumerate_calls
+    from paper_2103_16063_b200.workloads import unpruned_visits
+    nodes, dpn = max(1, a.D // 8), min(8, a.D)
+    calls, _ = enumerate_calls(nodes, dpn, 8 * a.D, a.nb)
+    cores = os.cpu_count() or 1
+    per_step = max(2.0, min(a.cpu_sample_sec, 120.0 / max(1, a.steps + a.warmup)))
+    rates = []
+    budget = None
+    for i in range(a.warmup + a.steps):
+        r, budget, _ = cpu_reference_rate(a.nb, a.D, calls, per_step, cores)
+        if i >= a.warmup:
+            rates.append(r)
+    value = sorted(rates)[len(rates) // 2]
+    sample = (f"{cores} processes x one call of the workload each (calls spread over the "
+              f"enumeration), reference pipecut.form_stage_dp with disable_pruning and "
+              f"visit_budget={budget} (stops after exactly that many visits)")
+    line = {
+        "impl": "reference", "metric": "dp_cells_per_sec", "value": value,
+        "unit": "visits/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(a.nb, a.D, calls, unpruned_visits(a.nb, calls)),
+        "cpu_baseline": {"value": value, "unit": "visits/s", "cores": cores,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "visits/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    from paper_2103_16063_b200 import _lib
+    from paper_2103_16063_b200.search import (_pack, call_weight, decide, enumerate_calls,
+                                              exchange, form_stage_sharded, lpt_shard,
+                                              run_calls)
+    from paper_2103_16063_b200.stages import bind_problem
+    from paper_2103_16063_b200.workloads import c5_blockset, unpruned_visits
+    import ctypes as C
+
+    ctx = _lib.context(local)
+    nodes, dpn = max(1, a.D // 8), min(8, a.D)
+    BS = 8 * a.D
+    bs = c5_blockset(a.nb, a.D, jitter_seed=JITTER_SEED)
+    nb = len(bs)
+    calls, levels = enumerate_calls(nodes, dpn, BS, nb)
+    unpruned = unpruned_visits(nb, calls)
+    owner = lpt_shard(nb, calls, world)
+    local_idx = [i for i in range(len(calls)) if owner[i] == rank]
+    my_calls = [calls[i] for i in local_idx]
+    n_levels = max(levels) + 1
+    max_stages = max(c[0] for c in calls)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timer():
+        ctx.check(ctx.lib.pc_timer_start(ctx.h), "timer")
+
+    def stop():
+        ms = C.c_double()
+        ctx.check(ctx.lib.pc_timer_stop(ctx.h, C.byref(ms)), "timer")
+        return ms.value
+
+    # ---- device-resident step: span tables + DP + backtrack + simulate + exchange + select
+    bind_problem(ctx, bs)
+    last = {}
+
+    def step_resident():
+        ctx.check(ctx.lib.pc_reset_cache(ctx.h), "reset")
+        flush.zero_()
+        barrier()
+        timer()
+        batch = run_calls(ctx, my_calls, BS, False, True)
+        rec, plan_w = _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels, max_stages)
+        allrec = exchange(rec, None, dev)
+        out = decide(allrec, calls, levels, owner, plan_w, None, BS)
+        ms = stop()
+        last.update(stats=batch.stats, result=out[1])
+        return max_over_ranks(ms)
+
+    for _ in range(a.warmup):
+        step_resident()
+    times = []
+    pairs = cands = dp_ms = launches = dp_launches = 0
+    with Clocks(local) as clk:
+        for _ in range(a.steps):
+            times.append(step_resident())
+            st = last["stats"]
+            pairs += st.pairs
+            cands += st.candidates
+            dp_ms += st.device_ms
+            launches += st.kernel_launches
+            dp_launches += st.dp_launches
+    ms_per_step = sum(times) / len(times)
+    value = unpruned / (ms_per_step / 1e3)
+    result = last["result"]
+
+    # ---- e2e: public API from host objects every step
+    e2e_times = []
+    tim = {}
+    for i in range(a.warmup + a.steps):
+        ctx.problem_owner = None            # force flatten + H2D upload
+        ctx.check(ctx.lib.pc_reset_cache(ctx.h), "reset")
+        flush.zero_()
+        barrier()
+        timer()
+        res = form_stage_sharded(nodes, dpn, BS, bs, timings=tim)
+        ms = stop()
+        if i >= a.warmup:
+            e2e_times.append(max_over_ranks(ms))
+        assert res.plan == result.plan and res.stats == result.stats
+    e2e_ms = sum(e2e_times) / len(e2e_times)
+    plan_bytes = 0 if result.plan is None else 48 * len(result.plan.stages)
+
+    # ---- roofline of the dominant kernel (DP level kernel)
+    peak = C.c_double()
+    ctx.check(ctx.lib.pc_measure_fp64_peak(ctx.h, C.byref(peak)), "peak")
+    # algorithmic fp64 work: 2 comm adds per feasible (cell, pred) pair
+    # (stages.py:232-237) + per candidate 2 max (stages.py:239) + 2 compares (_pareto)
+    ops = 2.0 * pairs + 4.0 * cands
+    achieved = ops / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "dp_level_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    line = {
+        "metric": "dp_cells_per_sec", "value": value, "unit": "visits/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": workload_config(nb, a.D, calls, unpruned),
+        "e2e": {"value": unpruned / (e2e_ms / 1e3), "unit": "visits/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(tim.get("h2d_bytes", 0)),
+                "d2h_bytes_per_step": int(tim.get("d2h_bytes", 0)) + plan_bytes},
+        "gpu_launches": int(launches // max(1, a.steps)),
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
+                     "unit": "Gop/s", "frac": achieved / peak.value if peak.value else None,
+                     "traffic": traffic,
+                     "kernel": "k_dp_level", "avg_launch_ms": dp_ms / max(1, dp_launches),
+                     "ops_per_step": ops / a.steps,
+                     "peak_source": "measured on this GPU: pc_measure_fp64_peak "
+                                    "(DADD+DSETP.MAX+DSETP chains, full occupancy)"},
+        "plan": None if result.plan is None else {
+            "stages": len(result.plan.stages), "microbatches": result.plan.microbatches,
+            "replica_factor": result.plan.replica_factor, "objective": result.plan.objective,
+            "visits": result.stats.visits, "dp_calls": result.stats.dp_calls},
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not a.no_cpu_baseline:
+        rate, budget, work = cpu_reference_rate(nb, a.D, calls, a.cpu_sample_sec, 1)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": "visits/s", "cores": 1, "kind": "reference",
+            "sample": f"reference pipecut.form_stage_dp (baseline/_ref, unmodified) on one call "
+                      f"{work[0][0]} of the workload with disable_pruning and "
+                      f"visit_budget={budget}; single thread"}
+    if not a.no_latency and world == 1:
+        line["latency_ms"] = config_latencies(ctx)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def config_latencies(ctx):
+    """Reference-semantics form_stage latency on C1-C4 through the public API
+    (median of 5 warm runs + 1 cold), reported beside the headline."""
+    from paper_2103_16063_b200 import form_stage
+    from paper_2103_16063_b200._host import pipecut as pc
+    from paper_2103_16063_b200.workloads import config_partition
+    out = {}
+    for name in ("C1", "C2", "C3", "C4"):
+        part, model, k, batch, cl = config_partition(name)
+        bs = pc.partition_blocks(part, model, k)
+        ts = []
+        for i in range(6):
+            ctx.problem_owner = None
+            ctx.lib.pc_reset_cache(ctx.h)
+            t0 = time.perf_counter()
+            res = form_stage(cl.num_nodes, cl.devices_per_node, batch, bs)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        warm = sorted(ts[1:])
+        out[name] = {"cold_ms": ts[0], "warm_ms": warm[len(warm) // 2],
+                     "visits": res.stats.visits, "dp_calls": res.stats.dp_calls,
+                     "objective": None if res.plan is None else res.plan.objective}
+    return out
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)

@@ -112,8 +112,11 @@ typedef struct pc_stats {
     int64_t dp_calls;           /* SearchStats.dp_calls */
     int64_t visits_unpruned;    /* closed form: the throughput unit */
     int64_t cells;              /* (s, b, d) table cells computed on device */
-    int64_t entries;            /* Pareto frontier entries written on device */
-    double  device_ms;          /* device time of the DP kernels (CUDA events) */
+    int64_t pairs;              /* feasible (cell, predecessor) pairs evaluated */
+    int64_t candidates;         /* frontier candidates generated (stages.py:238-239) */
+    int64_t dp_launches;        /* DP level kernel launches */
+    int64_t kernel_launches;    /* all library kernel launches of the call */
+    double  device_ms;          /* device time of the DP level kernels (CUDA events) */
     double  span_ms;            /* device time of span/cut table kernels */
 } pc_stats;
 
@@ -162,6 +165,22 @@ int pc_run_calls(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_siz
 int pc_form_stage(pc_ctx *ctx, int32_t num_nodes, int32_t devices_per_node,
                   int64_t batch_size, int32_t disable_pruning, int64_t visit_budget,
                   int32_t speculative, pc_plan *plan, pc_stats *stats);
+
+/* Budget crossing inside call `index` of the last pc_run_calls batch given
+ * the visits accumulated before it (stages.py:214-216): -1 if not crossed. */
+int pc_last_crossing(pc_ctx *ctx, int32_t index, int64_t visits_before, int64_t budget,
+                     int64_t *visits_at_cross);
+
+/* Drop the cached span/cut tables (they are rebuilt on demand). */
+int pc_reset_cache(pc_ctx *ctx);
+
+/* CUDA events on the library stream bracketing host-visible work. */
+int pc_timer_start(pc_ctx *ctx);
+int pc_timer_stop(pc_ctx *ctx, double *ms);
+
+/* Measured fp64 add/max issue rate of this device (Gop/s), the roofline
+ * denominator of the DP kernel (no tensor-core roof: min/max/add recurrence). */
+int pc_measure_fp64_peak(pc_ctx *ctx, double *gops);
 
 #ifdef __cplusplus
 }

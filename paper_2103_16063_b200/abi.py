@@ -81,7 +81,10 @@ class PcStats(C.Structure):
         ("dp_calls", C.c_int64),
         ("visits_unpruned", C.c_int64),
         ("cells", C.c_int64),
-        ("entries", C.c_int64),
+        ("pairs", C.c_int64),
+        ("candidates", C.c_int64),
+        ("dp_launches", C.c_int64),
+        ("kernel_launches", C.c_int64),
         ("device_ms", C.c_double),
         ("span_ms", C.c_double),
     ]

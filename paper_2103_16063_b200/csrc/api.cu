@@ -88,6 +88,10 @@ struct pc_ctx {
     // timing of the last batch
     double last_dp_ms = 0, last_span_ms = 0;
     int64_t last_dp_launches = 0;
+    int64_t last_pairs = 0, last_cands = 0;
+    int64_t launches = 0;   // all kernel launches since the last reset
+    DBuf counters_d;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
 };
 
 #define CUDA_TRY(ctx, expr)                                                       \
@@ -158,6 +162,8 @@ extern "C" void pc_ctx_destroy(pc_ctx *ctx) {
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+    if (ctx->t0) cudaEventDestroy(ctx->t0);
+    if (ctx->t1) cudaEventDestroy(ctx->t1);
     if (ctx->st) cudaStreamDestroy(ctx->st);
     delete ctx;
 }
@@ -348,11 +354,13 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
         CUDA_TRY(ctx, ctx->raw_d.ensure(sizeof(double) * 2 * (size_t)nf * tri));
         double *r = ctx->raw_d.as<double>();
         launch_span_time_general(P, nf, d_km, r, r + (size_t)nf * tri, ctx->st);
+        ctx->launches++;
         if (int rc = check_launch(ctx, "span_time_general")) return rc;
         raw_tf = r;
         raw_tb = r + (size_t)nf * tri;
     }
     launch_span_dp_tables(P, nf, d_km, d_kc, raw_tf, raw_tb, d_pf, d_pb, ctx->st);
+    ctx->launches++;
     if (int rc = check_launch(ctx, "span_dp_tables")) return rc;
     for (int i = 0; i < nf; ++i) {
         CachedKey ck;
@@ -505,18 +513,26 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.hist_cells = hist_cells;
         bt.overflow = ctx->overflow_d.as<int>();
         CUDA_TRY(ctx, cudaMemsetAsync(bt.overflow, 0, sizeof(int), ctx->st));
+        CUDA_TRY(ctx, ctx->counters_d.ensure(2 * sizeof(unsigned long long)));
+        bt.counters = ctx->counters_d.as<unsigned long long>();
+        CUDA_TRY(ctx, cudaMemsetAsync(bt.counters, 0, 2 * sizeof(unsigned long long), ctx->st));
         int64_t launches = 0;
         for (int s = 1; s <= maxS; ++s) {
             int n_active = 0;
             while (n_active < n && cds[n_active].S >= s) ++n_active;
             launch_dp_level(bt, s, n_active, warp_prefix[n_active], FL, ctx->st);
+            ctx->launches++;
             ++launches;
         }
         if (int rc = check_launch(ctx, "dp_level")) return rc;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev2, ctx->st));
         int ovf = 0;
+        unsigned long long cnt[2] = {0, 0};
         CUDA_TRY(ctx, cudaMemcpyAsync(&ovf, bt.overflow, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(cnt, bt.counters, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        ctx->last_pairs += (int64_t)cnt[0];
+        ctx->last_cands += (int64_t)cnt[1];
         float ms = 0;
         cudaEventElapsedTime(&ms, ctx->ev1, ctx->ev2);
         dp_ms += ms;
@@ -526,7 +542,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             ctx->last_span_ms += sms;
             first_pass = false;
         }
-        ctx->last_dp_launches = launches;
+        ctx->last_dp_launches += launches;
         if (!ovf) break;
         if (FL == 4) FL = 16;
         else if (FL == 16) FL = 32;
@@ -549,6 +565,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->level_sums_d.p, 0, sizeof(int64_t) * level_off[n], ctx->st));
     launch_row_visits(bt, pruning, ctx->level_sums_d.as<int64_t>(), ctx->row_prefix_d.as<int64_t>(),
                       ctx->level_off_d.as<int64_t>(), row_prefix[n], ctx->st);
+    ctx->launches += 2;
     if (int rc = check_launch(ctx, "visits")) return rc;
 
     // ---- backtrack (plan offsets in sorted order, compact)
@@ -566,6 +583,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     int32_t *seg = ctx->seg_d.as<int32_t>();
     launch_backtrack(bt, FL, BS, ctx->plan_off_d.as<int32_t>(), seg, seg + seg_total, seg + 2 * seg_total,
                      ctx->objective_d.as<double>(), ctx->feasible_d.as<int32_t>(), ctx->st);
+    ctx->launches++;
     if (int rc = check_launch(ctx, "backtrack")) return rc;
     std::vector<int64_t> level_sums(level_off[n]);
     std::vector<int32_t> segs(3 * (size_t)seg_total), feas(calls.size(), 0);
@@ -631,6 +649,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         CUDA_TRY(ctx, cudaMemcpyAsync(d_R, pR.data(), 4 * (size_t)np, cudaMemcpyHostToDevice, ctx->st));
         CUDA_TRY(ctx, cudaMemcpyAsync(d_MB, pMB.data(), 4 * (size_t)np, cudaMemcpyHostToDevice, ctx->st));
         launch_profile_queries(P, nq, d_lo, d_hi, d_m, d_ck, o_tf, o_tb, o_mem, ctx->st);
+        ctx->launches++;
         if (int rc = check_launch(ctx, "profile_queries")) return rc;
         if (want_iter) {
             // seg_dev of the compact layout: rebuild from queries' m? use a device copy
@@ -644,6 +663,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             CUDA_TRY(ctx, cudaMemcpyAsync(ctx->sim_d.p, qdev.data(), 4 * (size_t)nq, cudaMemcpyHostToDevice, ctx->st));
             launch_simulate(P, np, d_poff, d_S, d_R, d_MB, BS, d_lo, d_hi, ctx->sim_d.as<int32_t>(),
                             o_tf, o_tb, o_it, ctx->st, maxS_f);
+            ctx->launches++;
             if (int rc = check_launch(ctx, "simulate")) return rc;
             CUDA_TRY(ctx, cudaMemcpyAsync(iters.data(), o_it, 8 * (size_t)np, cudaMemcpyDeviceToHost, ctx->st));
             CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
@@ -702,6 +722,10 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     outs.assign(calls.size(), CallOut());
     ctx->last_dp_ms = 0;
     ctx->last_span_ms = 0;
+    ctx->last_dp_launches = 0;
+    ctx->last_pairs = 0;
+    ctx->last_cands = 0;
+    ctx->launches = 0;
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const size_t cap = free_b / 2;
@@ -786,7 +810,10 @@ static void fill_stats(pc_ctx *ctx, pc_stats *stats, int64_t visits, int64_t cal
     stats->dp_calls = calls;
     stats->visits_unpruned = unpruned;
     stats->cells = cells;
-    stats->entries = 0;
+    stats->pairs = ctx->last_pairs;
+    stats->candidates = ctx->last_cands;
+    stats->dp_launches = ctx->last_dp_launches;
+    stats->kernel_launches = ctx->launches;
     stats->device_ms = ctx->last_dp_ms;
     stats->span_ms = ctx->last_span_ms;
 }
@@ -939,6 +966,7 @@ extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, in
     }
     running = calls_counted = unpruned = cells = 0;
     double dp_ms = 0, span_ms = 0;
+    int64_t pairs = 0, cands = 0, launches = 0;
     for (int lv = 0; lv < n_levels; ++lv) {
         std::vector<pc_call> sub;
         std::vector<int> map(calls.size(), -1);
@@ -952,8 +980,14 @@ extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, in
         if (int rc = run_calls_impl(ctx, sub, BS, !disable_pruning, 1, outs, &chunks)) return rc;
         dp_ms += ctx->last_dp_ms;
         span_ms += ctx->last_span_ms;
+        pairs += ctx->last_pairs;
+        cands += ctx->last_cands;
+        launches += ctx->last_dp_launches;
         ctx->last_dp_ms = dp_ms;
         ctx->last_span_ms = span_ms;
+        ctx->last_pairs = pairs;
+        ctx->last_cands = cands;
+        ctx->last_dp_launches = launches;
         if (int rc = process_level(lv, outs, map)) return rc;
         if (best >= 0) {
             fill_stats(ctx, stats, running, calls_counted, unpruned, cells);
@@ -996,5 +1030,39 @@ extern "C" int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const
     CUDA_TRY(ctx, cudaMemcpyAsync(t_bwd, o_tb, 8 * (size_t)n, cudaMemcpyDeviceToHost, ctx->st));
     CUDA_TRY(ctx, cudaMemcpyAsync(mem, o_mem, 8 * (size_t)n, cudaMemcpyDeviceToHost, ctx->st));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    return PC_OK;
+}
+
+extern "C" int pc_reset_cache(pc_ctx *ctx) {
+    cudaSetDevice(ctx->device);
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    free_keys(ctx);
+    return PC_OK;
+}
+
+extern "C" int pc_timer_start(pc_ctx *ctx) {
+    cudaSetDevice(ctx->device);
+    if (!ctx->t0) {
+        CUDA_TRY(ctx, cudaEventCreate(&ctx->t0));
+        CUDA_TRY(ctx, cudaEventCreate(&ctx->t1));
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->t0, ctx->st));
+    return PC_OK;
+}
+
+extern "C" int pc_timer_stop(pc_ctx *ctx, double *ms) {
+    cudaSetDevice(ctx->device);
+    CUDA_TRY(ctx, cudaEventRecord(ctx->t1, ctx->st));
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->t1));
+    float f = 0;
+    CUDA_TRY(ctx, cudaEventElapsedTime(&f, ctx->t0, ctx->t1));
+    *ms = f;
+    return PC_OK;
+}
+
+extern "C" int pc_measure_fp64_peak(pc_ctx *ctx, double *gops) {
+    cudaSetDevice(ctx->device);
+    *gops = measure_fp64_gops(ctx->st, ctx->sm_count);
+    if (*gops <= 0) return fail(ctx, PC_ERR_CUDA, "fp64 peak kernel failed");
     return PC_OK;
 }

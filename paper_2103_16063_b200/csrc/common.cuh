@@ -115,6 +115,7 @@ struct DPBatch {
     uint8_t *hist_cnt;
     int64_t hist_cells;
     int *overflow;                  // set when a frontier exceeded FL
+    unsigned long long *counters;   // [0] feasible (cell, pred) pairs, [1] candidates
 };
 
 // count byte: bits 0-5 entries, bit 6 overflow, bit 7 saw_zero_share
@@ -151,6 +152,8 @@ void launch_row_visits(const DPBatch &b, int pruning, int64_t *level_sums, int64
 void launch_backtrack(const DPBatch &b, int FL, int64_t batch_size, const int32_t *plan_off,
                       int32_t *seg_lo, int32_t *seg_hi, int32_t *seg_dev, double *objective,
                       int32_t *feasible, cudaStream_t st);
+// peak.cu
+double measure_fp64_gops(cudaStream_t st, int sm_count);
 // sim.cu
 void launch_simulate(const DevProblem &p, int n_plans, const int32_t *plan_off,
                      const int32_t *plan_S, const int32_t *plan_R, const int32_t *plan_MB,

@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(256) k_dp_level(DPBatch B, int s, int n_active
     Front<FL> F;
     F.init();
     bool zero = false;
+    uint32_t n_pairs = 0, n_cands = 0;
 
     if (s == 1) {
         // level 0 holds the single cell (0, 0) with entry (0.0, 0.0) (stages.py:201)
@@ -108,6 +109,8 @@ __global__ void __launch_bounds__(256) k_dp_level(DPBatch B, int s, int n_active
             if (!isnan(tfc)) {
                 const double tbc = B.key_tbc[kk][ti];
                 F.insert(dmax_ref(0.0, tfc), dmax_ref(0.0, tbc), pack_key(0, 0, 0));
+                n_pairs = 1;
+                n_cands = 1;
             }
         }
     } else {
@@ -134,6 +137,8 @@ __global__ void __launch_bounds__(256) k_dp_level(DPBatch B, int s, int n_active
                 if (isnan(tfc)) continue;          // mem > budget (stages.py:230)
                 const int inter_dp = inter_of(B.num_nodes, B.dpn, dp);
                 const double tbc = B.key_tbc[kk][inter_dp * tri + ti];
+                ++n_pairs;
+                n_cands += cnt;
                 for (int i = 0; i < cnt; ++i) {
                     const double a = ptf[i * vstride + pc];
                     const double bb = ptb[i * vstride + pc];
@@ -141,6 +146,16 @@ __global__ void __launch_bounds__(256) k_dp_level(DPBatch B, int s, int n_active
                 }
             }
         }
+    }
+    // algorithmic work counters (one atomic per warp)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        n_pairs += __shfl_xor_sync(0xffffffffu, n_pairs, o);
+        n_cands += __shfl_xor_sync(0xffffffffu, n_cands, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&B.counters[0], (unsigned long long)n_pairs);
+        atomicAdd(&B.counters[1], (unsigned long long)n_cands);
     }
     if (!active) return;
 

@@ -1,0 +1,304 @@
+"""form_stage's candidate enumeration, run as device batches and sharded
+across GPUs.
+
+The reference's form_stage (pkg/src/pipecut/stages.py:372-413) walks widening
+levels n = 1, 2, 4, ... (num_nodes % n == 0), and within a level every
+(S, MB) pair is an independent `_run_dp` call; the first level with a feasible
+plan wins and its candidates are ranked by (simulated iteration time,
+objective, microbatches), first in (S, MB) order on ties.
+
+Here the calls are independent device work units:
+  * `run_calls` evaluates any list of them in one level-synchronous batch;
+  * `form_stage_sharded` spreads them over the ranks of a torch.distributed
+    group (one process per GPU, NCCL over NVLink) by LPT on the closed-form
+    visit count and exchanges one fixed-size record per rank with a single
+    `all_gather_into_tensor`; every rank then applies the reference's
+    selection rule to the gathered records, so all ranks return the same
+    `SearchResult`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import heapq
+
+import numpy as np
+
+from . import _lib, abi
+from .stages import (InvalidArgs, Plan, SearchBudgetExceeded, SearchOptions, SearchResult,
+                     SearchStats, StagePlan, bind_problem)
+
+
+def enumerate_calls(num_nodes: int, dpn: int, batch_size: int, nb: int):
+    """(S, D, R, MB) calls and their widening-level index, in the reference's
+    order (stages.py:389-403)."""
+    calls, levels = [], []
+    n, lv = 1, 0
+    while n <= num_nodes:
+        if num_nodes % n == 0:
+            D, R = dpn * n, num_nodes // n
+            for S in range(dpn * (n - 1) + 1, D + 1):
+                if S > nb:
+                    continue
+                MB = 1
+                while MB * R <= batch_size:
+                    calls.append((S, D, R, MB))
+                    levels.append(lv)
+                    MB *= 2
+            lv += 1
+        n *= 2
+    return calls, levels
+
+
+def call_weight(nb: int, call) -> int:
+    S, D, _, _ = call
+    A, B = nb - S + 1, D - S + 1
+    return S * (A * (A + 1) // 2) * (B * (B + 1) // 2)
+
+
+def lpt_shard(nb: int, calls, world: int):
+    """Owner rank per call: longest-processing-time first, deterministic."""
+    order = sorted(range(len(calls)), key=lambda i: (-call_weight(nb, calls[i]), i))
+    heap = [(0, r) for r in range(world)]
+    owner = [0] * len(calls)
+    for i in order:
+        load, r = heapq.heappop(heap)
+        owner[i] = r
+        heapq.heappush(heap, (load + call_weight(nb, calls[i]) + 1, r))
+    return owner
+
+
+class BatchResult:
+    """Per-call records of one device batch (+ plan buffers)."""
+
+    def __init__(self, calls, results, bufs, stats):
+        self.calls = calls
+        self.results = results
+        self.bufs = bufs
+        self.stats = stats
+
+    def feasible(self, i):
+        return bool(self.results[i].feasible)
+
+    def plan(self, i, batch_size) -> Plan | None:
+        if not self.results[i].feasible:
+            return None
+        S, D, R, MB = self.calls[i]
+        buf = self.bufs[i]
+        stages = tuple(
+            StagePlan(blocks=(int(buf.lo[k]), int(buf.hi[k])), devices=int(buf.devices[k]),
+                      replicas=int(buf.devices[k]) * R, t_fwd=float(buf.t_fwd[k]),
+                      t_bwd=float(buf.t_bwd[k]), mem=int(buf.mem[k]))
+            for k in range(S))
+        return Plan(stages=stages, microbatches=MB, replica_factor=R,
+                    objective=float(self.results[i].objective), batch_size=batch_size,
+                    devices_total=D)
+
+
+def run_calls(ctx: _lib.Context, calls, batch_size: int, disable_pruning: bool = False,
+              want_iteration: bool = True) -> BatchResult:
+    n = len(calls)
+    arr = (abi.PcCall * max(n, 1))(*[abi.PcCall(*c) for c in calls])
+    res = (abi.PcCallResult * max(n, 1))()
+    bufs = [abi.PlanBuffers(c[0]) for c in calls]
+    plans = (abi.PcPlan * max(n, 1))(*[b.s for b in bufs])
+    st = abi.PcStats()
+    if n:
+        rc = ctx.lib.pc_run_calls(ctx.h, n, arr, batch_size, int(bool(disable_pruning)),
+                                  int(bool(want_iteration)), res, plans, C.byref(st))
+        ctx.check(rc, "pc_run_calls")
+        for i in range(n):
+            bufs[i].s.n_stages = plans[i].n_stages
+    return BatchResult(calls, res, bufs, st)
+
+
+def rank_key(iteration, objective, MB, index):
+    # min by (iteration_time, objective, microbatches), first wins (stages.py:407-411)
+    return (iteration, objective, MB, index)
+
+
+def select(levels, visits, feasible, keys, budget):
+    """Reference selection over per-call records in call order.
+
+    Returns (best index or -1, counted calls, visits, crossing call or -1,
+    visits before the crossing call)."""
+    running = 0
+    counted = 0
+    n = len(levels)
+    i = 0
+    while i < n:
+        lv = levels[i]
+        j = i
+        best = -1
+        while j < n and levels[j] == lv:
+            counted += 1
+            if budget is not None and running + visits[j] > budget:
+                return -1, counted, running, j, running
+            running += visits[j]
+            if feasible[j] and (best < 0 or keys[j] < keys[best]):
+                best = j
+            j += 1
+        if best >= 0:
+            return best, counted, running, -1, running
+        i = j
+    return -1, counted, running, -1, running
+
+
+# --------------------------------------------------------------------------- sharded
+_REC = 4  # per call: visits, feasible, iteration, objective
+
+
+def _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels, max_stages):
+    """This rank's record: per-call (visits, feasible, iteration, objective)
+    for the calls it owns (zeros elsewhere) + its best plan per level."""
+    n = len(calls)
+    plan_w = 4 + 6 * max_stages
+    rec = np.zeros(n * _REC + n_levels * plan_w, np.float64)
+    best = {}
+    for li, gi in enumerate(local_idx):
+        r = batch.results[li]
+        rec[gi * _REC + 0] = r.visits
+        rec[gi * _REC + 1] = r.feasible
+        rec[gi * _REC + 2] = r.iteration_time
+        rec[gi * _REC + 3] = r.objective
+        if r.feasible:
+            key = rank_key(r.iteration_time, r.objective, calls[gi][3], gi)
+            lv = levels[gi]
+            if lv not in best or key < best[lv][0]:
+                best[lv] = (key, li, gi)
+    base = n * _REC
+    for lv, (_, li, gi) in best.items():
+        o = base + lv * plan_w
+        buf = batch.bufs[li]
+        S = calls[gi][0]
+        rec[o] = 1
+        rec[o + 1] = gi
+        rec[o + 2] = S
+        rec[o + 3] = batch.results[li].objective
+        k = o + 4
+        rec[k:k + S] = buf.lo[:S]
+        rec[k + S:k + 2 * S] = buf.hi[:S]
+        rec[k + 2 * S:k + 3 * S] = buf.devices[:S]
+        rec[k + 3 * S:k + 4 * S] = buf.t_fwd[:S]
+        rec[k + 4 * S:k + 5 * S] = buf.t_bwd[:S]
+        rec[k + 5 * S:k + 6 * S] = buf.mem[:S]    # exact: mem < 2**53
+    return rec, plan_w
+
+
+def exchange(rec: np.ndarray, group=None, device=None) -> np.ndarray:
+    """all_gather_into_tensor of one fixed-size float64 record per rank
+    (NCCL on `device`, or gloo on CPU when device is None)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return rec.reshape(1, -1)
+    world = dist.get_world_size(group)
+    mine = torch.from_numpy(rec)
+    if device is not None:
+        mine = mine.to(device)
+    if mine.is_cuda:
+        out = torch.empty(world * rec.size, dtype=torch.float64, device=mine.device)
+        dist.all_gather_into_tensor(out, mine, group=group)
+        return out.view(world, rec.size).cpu().numpy()
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    return torch.stack(parts).numpy()
+
+
+def decide(allrec: np.ndarray, calls, levels, owner, plan_w: int, budget, batch_size: int):
+    """Apply the reference's selection to the gathered records.
+
+    Returns ("plan", SearchResult) or ("budget", crossing call, visits before)."""
+    n = len(calls)
+    world = allrec.shape[0]
+    per = allrec[:, :n * _REC].reshape(world, n, _REC)
+    own = np.asarray(owner, dtype=np.int64)
+    g = per[own, np.arange(n)] if n else np.zeros((0, _REC))
+    visits = [int(v) for v in g[:, 0]]
+    feasible = [bool(f) for f in g[:, 1]]
+    keys = [rank_key(float(g[i, 2]), float(g[i, 3]), calls[i][3], i) for i in range(n)]
+    best, counted, running, cross, before = select(levels, visits, feasible, keys, budget)
+    if cross >= 0:
+        return ("budget", cross, before)
+    stats = SearchStats(visits=running, dp_calls=counted)
+    if best < 0:
+        return ("plan", SearchResult(None, stats))
+    o = n * _REC + levels[best] * plan_w
+    row = allrec[owner[best]]
+    if row[o] != 1 or int(row[o + 1]) != best:
+        raise RuntimeError("inconsistent shard record")
+    S, D, R, MB = calls[best]
+    k = o + 4
+    stages = tuple(
+        StagePlan(blocks=(int(row[k + j]), int(row[k + S + j])), devices=int(row[k + 2 * S + j]),
+                  replicas=int(row[k + 2 * S + j]) * R, t_fwd=float(row[k + 3 * S + j]),
+                  t_bwd=float(row[k + 4 * S + j]), mem=int(row[k + 5 * S + j]))
+        for j in range(S))
+    plan = Plan(stages=stages, microbatches=MB, replica_factor=R, objective=float(row[o + 3]),
+                batch_size=batch_size, devices_total=D)
+    return ("plan", SearchResult(plan, stats))
+
+
+def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
+                       options=None, *, group=None, timings: dict | None = None):
+    """form_stage with its DP calls spread over every rank of a
+    torch.distributed group (one GPU per rank, NCCL); all ranks return the
+    reference's SearchResult."""
+    import torch
+    import torch.distributed as dist
+
+    if num_nodes < 1 or devices_per_node < 1 or batch_size < 1:
+        raise InvalidArgs("node count, devices per node and batch size must be at least 1")
+    opts = options or SearchOptions()
+    dist_on = dist.is_initialized()
+    world = dist.get_world_size(group) if dist_on else 1
+    rank = dist.get_rank(group) if dist_on else 0
+    ctx = _lib.context()
+    bind_problem(ctx, blocks)
+    nb = len(blocks)
+    calls, levels = enumerate_calls(num_nodes, devices_per_node, batch_size, nb)
+    n_levels = (max(levels) + 1) if levels else 0
+    owner = lpt_shard(nb, calls, world)
+    local_idx = [i for i in range(len(calls)) if owner[i] == rank]
+    batch = run_calls(ctx, [calls[i] for i in local_idx], batch_size,
+                      opts.disable_pruning, True)
+    max_stages = max((c[0] for c in calls), default=1)
+    rec, plan_w = _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels, max_stages)
+    dev = torch.device("cuda", ctx.device)
+    allrec = exchange(rec, group, dev)
+    if timings is not None:
+        timings.update(pairs=int(batch.stats.pairs), candidates=int(batch.stats.candidates),
+                       dp_ms=float(batch.stats.device_ms), span_ms=float(batch.stats.span_ms),
+                       dp_launches=int(batch.stats.dp_launches),
+                       kernel_launches=int(batch.stats.kernel_launches),
+                       local_unpruned=int(batch.stats.visits_unpruned),
+                       unpruned=sum(call_weight(nb, c) for c in calls),
+                       h2d_bytes=_flat_bytes(ctx.problem_flat), d2h_bytes=int(rec.nbytes))
+    out = decide(allrec, calls, levels, owner, plan_w, opts.visit_budget, batch_size)
+    if out[0] == "plan":
+        return out[1]
+    _, cross, before = out
+    v = np.zeros(1, np.float64)
+    if owner[cross] == rank:
+        li = local_idx.index(cross)
+        at = C.c_int64()
+        ctx.check(ctx.lib.pc_last_crossing(ctx.h, li, before, int(opts.visit_budget),
+                                           C.byref(at)), "pc_last_crossing")
+        if at.value < -1:   # flags of an earlier chunk are gone: recompute that call
+            run_calls(ctx, [calls[cross]], batch_size, opts.disable_pruning, False)
+            ctx.check(ctx.lib.pc_last_crossing(ctx.h, 0, before, int(opts.visit_budget),
+                                               C.byref(at)), "pc_last_crossing")
+        v[0] = at.value
+    if world > 1:
+        t = torch.from_numpy(v).to(dev)
+        dist.broadcast(t, src=owner[cross], group=group)
+        v = t.cpu().numpy()
+    raise SearchBudgetExceeded(int(v[0]), int(opts.visit_budget))
+
+
+def _flat_bytes(flat) -> int:
+    if flat is None:
+        return 0
+    return int(sum(getattr(flat, f).nbytes for f in flat.__dataclass_fields__
+                   if isinstance(getattr(flat, f), np.ndarray)))

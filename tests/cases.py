@@ -112,45 +112,5 @@ def search_instance(rng):
 
 
 # ---------------------------------------------------------------- configs
-CONFIGS = {
-    # name: (generator, args, (nodes, dpn, memory), k, batch)
-    "C1": ("bert", (1024, 24, 512, 30522), (1, 8, 2 ** 35), 32, 256),
-    "C2": ("bert", (2048, 96, 512, 30522), (4, 8, 32e9), 32, 256),
-    "C3": ("resnet", (152, 8), (1, 8, 180e9), 32, 128),
-    "C4": ("bert", (4096, 256, 512, 30522), (32, 8, 32e9), 32, 2048),
-}
-
-
-def config_partition(name):
-    """(partition, model, k, batch, cluster) for C1-C4."""
-    kind, args, (nodes, dpn, mem), k, batch = CONFIGS[name]
-    g = pc.gen_bert_like(*args) if kind == "bert" else pc.gen_resnet_like(*args)
-    cl = pc.ClusterSpec(nodes, dpn, int(mem), 50e9, 10e9)
-    part = pc.build_atomic_subcomponents(g)
-    model = pc.CostModel(part.graph, pc.CostModelConfig(), cl)
-    return part, model, k, batch, cl
-
-
-def bert_layer_chain(nb, hidden=1024, seq=512, jitter_seed=None):
-    """C5: one task per BERT layer, ids t%05d so sorted order is chain order."""
-    h, s = hidden, seq
-    heads = max(1, h // 64)
-    flops = 24.0 * s * h * h + 4.0 * s * s * h + 5.0 * s * s * heads + 52.0 * s * h
-    rng = random.Random(jitter_seed) if jitter_seed is not None else None
-    nodes, edges, prev = [_val("x", per_sample=s * 8)], [], "x"
-    for i in range(nb):
-        t, v, w = f"t{i:05d}", f"v{i:05d}", f"w{i:05d}"
-        f = flops if rng is None else flops * rng.uniform(0.9, 1.1)
-        nodes += [_task(t, f, op="layer"), _val(v, per_sample=s * h * 4),
-                  _val(w, fixed=(12 * h * h + 13 * h) * 4, param=True)]
-        edges += [(prev, t), (w, t), (t, v)]
-        prev = v
-    return TaskGraph(nodes, edges, ["x"], [prev])
-
-
-def c5_blockset(nb, D, jitter_seed=None):
-    g = bert_layer_chain(nb, jitter_seed=jitter_seed)
-    cl = pc.ClusterSpec(max(1, D // 8), min(8, D), int(32e9), 50e9, 10e9)
-    part = pc.build_atomic_subcomponents(g)
-    model = pc.CostModel(part.graph, pc.CostModelConfig(), cl)
-    return pc.partition_blocks(part, model, k=10 ** 6)
+from paper_2103_16063_b200.workloads import (  # noqa: E402,F401
+    CONFIGS, bert_layer_chain, c5_blockset, config_partition)
