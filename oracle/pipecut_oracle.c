@@ -89,6 +89,13 @@ double orc_cut_time(const pc_problem *p, int cut, int64_t m, int64_t cum)
 typedef struct { double tf, tb; int bp, dp, idx; int ord; } orc_entry;
 typedef struct { int n; orc_entry *e; } orc_cell;
 
+/* frontier-size histogram of the cells computed (diagnostics) */
+static int64_t g_fhist[65];
+void orc_frontier_hist(int64_t *out)
+{
+    for (int i = 0; i < 65; ++i) { out[i] = g_fhist[i]; g_fhist[i] = 0; }
+}
+
 static int cmp_entry(const void *a, const void *b)
 {
     const orc_entry *x = (const orc_entry *)a, *y = (const orc_entry *)b;
@@ -281,6 +288,7 @@ int orc_run_dp(const pc_problem *p, orc_prof *pf, int S, int D, int64_t BS, int 
                             best = cands[i].tb;
                         }
                     }
+                    g_fhist[cc->n < 64 ? cc->n : 64]++;
                 } else if (!disable_pruning && !saw_zero) {   /* :242-249 */
                     if (s == 1) d_min = d + 1;
                     break;

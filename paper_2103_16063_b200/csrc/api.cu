@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -48,8 +49,9 @@ struct DBuf {
 struct CachedKey {
     int64_t m;
     int ckpt;
-    double *tfc = nullptr;
-    double *tbc = nullptr;
+    double *tf = nullptr;    // [tri] hi-major, NaN = infeasible
+    double *tb = nullptr;    // [tri] or null when derived as beta * tf
+    double *cut = nullptr;   // [2][nb+1]
 };
 
 }  // namespace
@@ -70,14 +72,16 @@ struct pc_ctx {
     // key cache
     std::vector<CachedKey> keys;
     std::map<std::pair<int64_t, int>, int> key_map;
-    DBuf key_ptrs;   // [2][n_keys] device pointers
+    DBuf key_ptrs;   // [3][n_keys] device pointers (tf, tb, cut)
     size_t key_bytes = 0;
+    bool derived = false;    // t_bwd derived as beta * t_fwd (beta a power of two)
+    DBuf mismatch_d;
     // batch scratch
     DBuf calls_d, warp_prefix_d, keyidx_d, val_d, hist_d, overflow_d;
     DBuf level_off_d, level_sums_d, row_prefix_d;
     DBuf plan_off_d, seg_d, objective_d, feasible_d;
     DBuf q_d, q_out_d, sim_d;
-    DBuf raw_d, keys_m_d, keys_ckpt_d;
+    DBuf raw_d, keys_m_d, keys_ckpt_d, colb_d;
     // last batch (for budget crossing queries)
     std::vector<CallDesc> last_calls;   // sorted order
     std::vector<int> last_pos;          // orig -> sorted position
@@ -88,7 +92,7 @@ struct pc_ctx {
     // timing of the last batch
     double last_dp_ms = 0, last_span_ms = 0;
     int64_t last_dp_launches = 0;
-    int64_t last_pairs = 0, last_cands = 0;
+    int64_t last_pairs = 0, last_cands = 0, last_inserts = 0;
     int64_t launches = 0;   // all kernel launches since the last reset
     DBuf counters_d;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -146,8 +150,9 @@ extern "C" int pc_ctx_create(int device, pc_ctx **out) {
 
 static void free_keys(pc_ctx *ctx) {
     for (auto &k : ctx->keys) {
-        if (k.tfc) cudaFree(k.tfc);
-        if (k.tbc) cudaFree(k.tbc);
+        if (k.tf) cudaFree(k.tf);
+        if (k.tb) cudaFree(k.tb);
+        if (k.cut) cudaFree(k.cut);
     }
     ctx->keys.clear();
     ctx->key_map.clear();
@@ -293,6 +298,11 @@ extern "C" int pc_set_problem(pc_ctx *ctx, const pc_problem *p) {
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
     ctx->pre_param = pre_param;
     ctx->nb = nb;
+    {
+        int ex = 0;
+        const double fr = frexp(p->bwd_fwd_ratio, &ex);
+        ctx->derived = p->bwd_fwd_ratio > 0 && fr == 0.5;
+    }
     ctx->has_problem = true;
     return PC_OK;
 }
@@ -301,87 +311,117 @@ extern "C" int pc_set_problem(pc_ctx *ctx, const pc_problem *p) {
 static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &want) {
     const DevProblem &P = ctx->P;
     const int64_t tri = tri_size(P.nb);
-    const size_t per_key = sizeof(double) * 2 * (size_t)P.n_inter * (size_t)tri;
     std::vector<std::pair<int64_t, int>> fresh;
     for (auto &k : want)
         if (!ctx->key_map.count(k)) fresh.push_back(k);
     if (fresh.empty()) return PC_OK;
-    // bounded cache: drop keys the current batch does not need when the cache
-    // would outgrow a third of free device memory
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    if (ctx->key_bytes + fresh.size() * per_key > (ctx->key_bytes + free_b) / 3) {
-        std::map<std::pair<int64_t, int>, int> need;
-        for (auto &k : want) need[k] = 1;
-        std::vector<CachedKey> kept;
-        for (auto &k : ctx->keys) {
-            if (need.count({k.m, k.ckpt})) {
-                kept.push_back(k);
-            } else {
-                cudaFree(k.tfc);
-                cudaFree(k.tbc);
-                ctx->key_bytes -= per_key;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const size_t per_key = sizeof(double) * ((ctx->derived ? 1 : 2) * (size_t)tri + 2 * (size_t)(P.nb + 1)) + sizeof(int32_t) * (size_t)(P.nb + 1);
+        // bounded cache: drop keys the current batch does not need when the cache
+        // would outgrow a third of free device memory
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        if (ctx->key_bytes + fresh.size() * per_key > (ctx->key_bytes + free_b) / 3) {
+            std::map<std::pair<int64_t, int>, int> need;
+            for (auto &k : want) need[k] = 1;
+            std::vector<CachedKey> kept;
+            for (auto &k : ctx->keys) {
+                if (need.count({k.m, k.ckpt})) {
+                    kept.push_back(k);
+                } else {
+                    cudaFree(k.tf);
+                    if (k.tb) cudaFree(k.tb);
+                    cudaFree(k.cut);
+                    ctx->key_bytes -= per_key;
+                }
             }
+            ctx->keys = kept;
+            ctx->key_map.clear();
+            for (size_t i = 0; i < ctx->keys.size(); ++i)
+                ctx->key_map[{ctx->keys[i].m, ctx->keys[i].ckpt}] = (int)i;
         }
-        ctx->keys = kept;
-        ctx->key_map.clear();
-        for (size_t i = 0; i < ctx->keys.size(); ++i)
-            ctx->key_map[{ctx->keys[i].m, ctx->keys[i].ckpt}] = (int)i;
-    }
-    const int nf = (int)fresh.size();
-    std::vector<int64_t> km(nf);
-    std::vector<int32_t> kc(nf);
-    std::vector<double *> pf(nf), pb(nf);
-    for (int i = 0; i < nf; ++i) {
-        km[i] = fresh[i].first;
-        kc[i] = fresh[i].second;
-        CUDA_TRY(ctx, cudaMalloc(&pf[i], per_key / 2));
-        CUDA_TRY(ctx, cudaMalloc(&pb[i], per_key / 2));
-        ctx->key_bytes += per_key;
-    }
-    CUDA_TRY(ctx, ctx->keys_m_d.ensure(sizeof(int64_t) * nf + sizeof(int32_t) * nf + sizeof(double *) * 2 * nf + 64));
-    char *kb = ctx->keys_m_d.as<char>();
-    int64_t *d_km = (int64_t *)kb;
-    int32_t *d_kc = (int32_t *)(kb + sizeof(int64_t) * nf);
-    double **d_pf = (double **)(kb + ((sizeof(int64_t) * nf + sizeof(int32_t) * nf + 15) & ~size_t(15)));
-    double **d_pb = d_pf + nf;
-    CUDA_TRY(ctx, cudaMemcpyAsync(d_km, km.data(), sizeof(int64_t) * nf, cudaMemcpyHostToDevice, ctx->st));
-    CUDA_TRY(ctx, cudaMemcpyAsync(d_kc, kc.data(), sizeof(int32_t) * nf, cudaMemcpyHostToDevice, ctx->st));
-    CUDA_TRY(ctx, cudaMemcpyAsync(d_pf, pf.data(), sizeof(double *) * nf, cudaMemcpyHostToDevice, ctx->st));
-    CUDA_TRY(ctx, cudaMemcpyAsync(d_pb, pb.data(), sizeof(double *) * nf, cudaMemcpyHostToDevice, ctx->st));
-    const double *raw_tf = nullptr, *raw_tb = nullptr;
-    if (!P.monotone) {
-        CUDA_TRY(ctx, ctx->raw_d.ensure(sizeof(double) * 2 * (size_t)nf * tri));
-        double *r = ctx->raw_d.as<double>();
-        launch_span_time_general(P, nf, d_km, r, r + (size_t)nf * tri, ctx->st);
+        const int nf = (int)fresh.size();
+        std::vector<int64_t> km(nf);
+        std::vector<int32_t> kc(nf);
+        std::vector<double *> pf(nf), pb(nf, nullptr), pcut(nf);
+        for (int i = 0; i < nf; ++i) {
+            km[i] = fresh[i].first;
+            kc[i] = fresh[i].second;
+            CUDA_TRY(ctx, cudaMalloc(&pf[i], sizeof(double) * (size_t)tri));
+            if (!ctx->derived) CUDA_TRY(ctx, cudaMalloc(&pb[i], sizeof(double) * (size_t)tri));
+            CUDA_TRY(ctx, cudaMalloc(&pcut[i], sizeof(double) * 2 * (size_t)(P.nb + 1) + sizeof(int32_t) * (size_t)(P.nb + 1)));
+            ctx->key_bytes += per_key;
+        }
+        const size_t hdr = (sizeof(int64_t) * nf + sizeof(int32_t) * nf + 15) & ~size_t(15);
+        CUDA_TRY(ctx, ctx->keys_m_d.ensure(hdr + sizeof(double *) * 4 * nf + 64));
+        char *kb = ctx->keys_m_d.as<char>();
+        int64_t *d_km = (int64_t *)kb;
+        int32_t *d_kc = (int32_t *)(kb + sizeof(int64_t) * nf);
+        double **d_pf = (double **)(kb + hdr);
+        double **d_pb = d_pf + nf;
+        double **d_pc = d_pb + nf;
+        int32_t **d_pff = (int32_t **)(d_pc + nf);
+        std::vector<int32_t *> pff(nf);
+        for (int i = 0; i < nf; ++i) pff[i] = (int32_t *)(pcut[i] + 2 * (size_t)(P.nb + 1));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_km, km.data(), sizeof(int64_t) * nf, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_kc, kc.data(), sizeof(int32_t) * nf, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_pf, pf.data(), sizeof(double *) * nf, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_pb, pb.data(), sizeof(double *) * nf, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_pc, pcut.data(), sizeof(double *) * nf, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(d_pff, pff.data(), sizeof(int32_t *) * nf, cudaMemcpyHostToDevice, ctx->st));
+        const double *raw_tf = nullptr, *raw_tb = nullptr;
+        if (!P.monotone) {
+            CUDA_TRY(ctx, ctx->raw_d.ensure(sizeof(double) * 2 * (size_t)nf * tri));
+            double *r = ctx->raw_d.as<double>();
+            launch_span_time_general(P, nf, d_km, r, r + (size_t)nf * tri, ctx->st);
+            ctx->launches++;
+            if (int rc = check_launch(ctx, "span_time_general")) return rc;
+            raw_tf = r;
+            raw_tb = r + (size_t)nf * tri;
+        }
+        CUDA_TRY(ctx, ctx->mismatch_d.ensure(sizeof(int)));
+        CUDA_TRY(ctx, cudaMemsetAsync(ctx->mismatch_d.p, 0, sizeof(int), ctx->st));
+        launch_span_dp_tables(P, nf, d_km, d_kc, raw_tf, raw_tb, d_pf, d_pb, d_pc, ctx->derived ? 1 : 0,
+                              ctx->mismatch_d.as<int>(), ctx->st);
         ctx->launches++;
-        if (int rc = check_launch(ctx, "span_time_general")) return rc;
-        raw_tf = r;
-        raw_tb = r + (size_t)nf * tri;
-    }
-    launch_span_dp_tables(P, nf, d_km, d_kc, raw_tf, raw_tb, d_pf, d_pb, ctx->st);
-    ctx->launches++;
-    if (int rc = check_launch(ctx, "span_dp_tables")) return rc;
-    for (int i = 0; i < nf; ++i) {
-        CachedKey ck;
-        ck.m = km[i];
-        ck.ckpt = kc[i];
-        ck.tfc = pf[i];
-        ck.tbc = pb[i];
-        ctx->key_map[{km[i], kc[i]}] = (int)ctx->keys.size();
-        ctx->keys.push_back(ck);
+        if (int rc = check_launch(ctx, "span_dp_tables")) return rc;
+        launch_first_feasible(P.nb, nf, d_pf, d_pff, ctx->st);
+        ctx->launches++;
+        if (int rc = check_launch(ctx, "first_feasible")) return rc;
+        int mism = 0;
+        CUDA_TRY(ctx, cudaMemcpyAsync(&mism, ctx->mismatch_d.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        for (int i = 0; i < nf; ++i) {
+            CachedKey ck;
+            ck.m = km[i];
+            ck.ckpt = kc[i];
+            ck.tf = pf[i];
+            ck.tb = pb[i];
+            ck.cut = pcut[i];
+            ctx->key_map[{km[i], kc[i]}] = (int)ctx->keys.size();
+            ctx->keys.push_back(ck);
+        }
+        if (mism && ctx->derived) {
+            // t_bwd is not exactly beta * t_fwd here: store it explicitly
+            free_keys(ctx);
+            ctx->derived = false;
+            fresh = want;
+            continue;
+        }
+        break;
     }
     // device pointer arrays for the DP kernels
     const size_t nk = ctx->keys.size();
-    std::vector<const double *> ptrs(2 * nk);
+    std::vector<const void *> ptrs(4 * nk);
     for (size_t i = 0; i < nk; ++i) {
-        ptrs[i] = ctx->keys[i].tfc;
-        ptrs[nk + i] = ctx->keys[i].tbc;
+        ptrs[i] = ctx->keys[i].tf;
+        ptrs[nk + i] = ctx->keys[i].tb;
+        ptrs[2 * nk + i] = ctx->keys[i].cut;
+        ptrs[3 * nk + i] = ctx->keys[i].cut + 2 * (size_t)(P.nb + 1);
     }
-    CUDA_TRY(ctx, ctx->key_ptrs.ensure(sizeof(double *) * 2 * nk));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->key_ptrs.p, ptrs.data(), sizeof(double *) * 2 * nk,
+    CUDA_TRY(ctx, ctx->key_ptrs.ensure(sizeof(void *) * 4 * nk));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->key_ptrs.p, ptrs.data(), sizeof(void *) * 4 * nk,
                                   cudaMemcpyHostToDevice, ctx->st));
-    // keep staging vectors alive until the copies complete
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
     return PC_OK;
 }
@@ -442,7 +482,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     // call descriptors
     std::vector<CallDesc> cds(n);
     std::vector<int16_t> keyidx;
-    std::vector<int64_t> warp_prefix(n + 1, 0);
+    std::vector<int64_t> cta_prefix(n + 1, 0);
     int64_t val_cells = 0, hist_cells = 0;
     int maxS = 0;
     for (int i = 0; i < n; ++i) {
@@ -465,74 +505,123 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         const int64_t cells = (int64_t)cd.A * cd.B;
         val_cells += cells;
         hist_cells += cells * cd.S;
-        warp_prefix[i + 1] = warp_prefix[i] + (int64_t)((cd.A + 31) / 32) * cd.B;
+        cta_prefix[i + 1] = cta_prefix[i] + ((int64_t)cd.A * cd.B + DP_WARPS - 1) / DP_WARPS;
         maxS = std::max(maxS, cd.S);
     }
     CUDA_TRY(ctx, ctx->calls_d.ensure(sizeof(CallDesc) * n));
     CUDA_TRY(ctx, ctx->warp_prefix_d.ensure(sizeof(int64_t) * (n + 1)));
     CUDA_TRY(ctx, ctx->keyidx_d.ensure(sizeof(int16_t) * keyidx.size() + 16));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->calls_d.p, cds.data(), sizeof(CallDesc) * n, cudaMemcpyHostToDevice, ctx->st));
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->warp_prefix_d.p, warp_prefix.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->warp_prefix_d.p, cta_prefix.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->st));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->keyidx_d.p, keyidx.data(), sizeof(int16_t) * keyidx.size(), cudaMemcpyHostToDevice, ctx->st));
 
     const size_t nk = ctx->keys.size();
-    int FL = 4;
     DPBatch bt{};
     float dp_ms = 0;
     bool first_pass = true;
+    int vcap = 4, hcap = 4;     // pool entries reserved per cell (grown on overflow)
     for (;;) {
-        // buffers for this frontier capacity
-        const size_t val_half = (((size_t)val_cells * (16 * (size_t)FL + 1) + 64) + 255) & ~size_t(255);
-        const size_t val_bytes = 2 * val_half;
-        const size_t hist_bytes = (size_t)hist_cells * (4 * (size_t)FL + 1) + 64;
-        CUDA_TRY(ctx, ctx->val_d.ensure(val_bytes));
-        CUDA_TRY(ctx, ctx->hist_d.ensure(hist_bytes));
-        CUDA_TRY(ctx, ctx->overflow_d.ensure(sizeof(int)));
+        int64_t vpool_total = 0, hpool_total = 0, col_total = 0;
+        std::vector<int64_t> col_prefix(n + 1, 0);
+        for (int i = 0; i < n; ++i) {
+            cds[i].col_off = col_total;
+            col_total += cds[i].B;
+            col_prefix[i + 1] = col_total;
+            const int64_t cells = (int64_t)cds[i].A * cds[i].B;
+            cds[i].vpool_base = vpool_total;
+            cds[i].vpool_cap = cells * vcap + 64;
+            vpool_total += cds[i].vpool_cap;
+            cds[i].hpool_base = hpool_total;
+            cds[i].hpool_cap = cells * cds[i].S * hcap + 64;
+            hpool_total += cds[i].hpool_cap;
+        }
+        CUDA_TRY(ctx, cudaMemcpyAsync(ctx->calls_d.p, cds.data(), sizeof(CallDesc) * n, cudaMemcpyHostToDevice, ctx->st));
+        const size_t a256 = 255;
+        const size_t vmeta = ((size_t)val_cells * 5 + a256) & ~a256;      // cnt u8 + off u32
+        const size_t vpool = ((size_t)vpool_total * 16 + a256) & ~a256;   // tf + tb
+        const size_t hmeta = ((size_t)hist_cells * 5 + a256) & ~a256;
+        const int64_t vspill = std::max<int64_t>(1 << 20, val_cells) * vcap / 4;
+        const int64_t hspill = std::max<int64_t>(1 << 22, hist_cells / 2) * hcap / 4;
+        const size_t vsp = ((size_t)vspill * 16 + a256) & ~a256;
+        CUDA_TRY(ctx, ctx->val_d.ensure(2 * (vmeta + vpool + vsp) + 256));
+        CUDA_TRY(ctx, ctx->hist_d.ensure(hmeta + 4 * (size_t)(hpool_total + hspill) + 512));
+        CUDA_TRY(ctx, ctx->overflow_d.ensure(64 + 3 * sizeof(unsigned long long) * (size_t)n + 64));
+        CUDA_TRY(ctx, ctx->colb_d.ensure(4 * sizeof(int32_t) * (size_t)col_total + 64));
+        for (int par = 0; par < 2; ++par) {
+            bt.col_min[par] = ctx->colb_d.as<int32_t>() + (size_t)(2 * par) * col_total;
+            bt.col_max[par] = ctx->colb_d.as<int32_t>() + (size_t)(2 * par + 1) * col_total;
+        }
         char *vb = ctx->val_d.as<char>();
         bt.nb = nb;
         bt.n_calls = n;
         bt.calls = ctx->calls_d.as<CallDesc>();
-        bt.warp_prefix = ctx->warp_prefix_d.as<int64_t>();
+        bt.cta_prefix = ctx->warp_prefix_d.as<int64_t>();
         bt.keyidx = ctx->keyidx_d.as<int16_t>();
-        bt.key_tfc = (const double *const *)ctx->key_ptrs.p;
-        bt.key_tbc = ((const double *const *)ctx->key_ptrs.p) + nk;
-        bt.tri = tri_size(nb);
-        bt.n_inter = P.n_inter;
+        bt.key_tf = (const double *const *)ctx->key_ptrs.p;
+        bt.key_tb = ((const double *const *)ctx->key_ptrs.p) + nk;
+        bt.key_cut = ((const double *const *)ctx->key_ptrs.p) + 2 * nk;
+        bt.key_ffb = ((const int32_t *const *)ctx->key_ptrs.p) + 3 * nk;
+        bt.beta = P.beta;
         bt.num_nodes = P.num_nodes;
         bt.dpn = P.dpn;
         bt.val_cells = val_cells;
+        char *ob = ctx->overflow_d.as<char>();
+        bt.overflow = (int *)ob;
+        unsigned long long *used = (unsigned long long *)(ob + 64);
         for (int par = 0; par < 2; ++par) {
-            char *base = vb + par * val_half;
-            bt.val_tf[par] = (double *)base;
-            bt.val_tb[par] = (double *)(base + 8 * (size_t)FL * val_cells);
-            bt.val_cnt[par] = (uint8_t *)(base + 16 * (size_t)FL * val_cells);
+            char *base = vb + par * (vmeta + vpool + vsp);
+            bt.val_off[par] = (uint32_t *)base;
+            bt.val_cnt[par] = (uint8_t *)(base + 4 * (size_t)val_cells);
+            bt.pool_tf[par] = (double *)(base + vmeta);
+            bt.pool_tb[par] = (double *)(base + vmeta + 8 * (size_t)vpool_total);
+            bt.spill_tf[par] = (double *)(base + vmeta + vpool);
+            bt.spill_tb[par] = (double *)(base + vmeta + vpool + 8 * (size_t)vspill);
+            bt.vpool_used[par] = used + (size_t)par * n;
         }
+        bt.vspill_cap = vspill;
         char *hb = ctx->hist_d.as<char>();
-        bt.hist_key = (uint32_t *)hb;
-        bt.hist_cnt = (uint8_t *)(hb + 4 * (size_t)FL * hist_cells);
+        bt.hist_off = (uint32_t *)hb;
+        bt.hist_cnt = (uint8_t *)(hb + 4 * (size_t)hist_cells);
+        bt.hpool = (uint32_t *)(hb + hmeta);
+        bt.hspill = bt.hpool + hpool_total;
+        bt.hspill_cap = hspill;
+        bt.hpool_used = used + 2 * (size_t)n;
+        bt.vspill_used = used + 3 * (size_t)n;
+        bt.hspill_used = used + 3 * (size_t)n + 2;
         bt.hist_cells = hist_cells;
-        bt.overflow = ctx->overflow_d.as<int>();
-        CUDA_TRY(ctx, cudaMemsetAsync(bt.overflow, 0, sizeof(int), ctx->st));
-        CUDA_TRY(ctx, ctx->counters_d.ensure(2 * sizeof(unsigned long long)));
+        CUDA_TRY(ctx, cudaMemsetAsync(ob, 0, 64 + 3 * sizeof(unsigned long long) * (size_t)n + 64, ctx->st));
+        CUDA_TRY(ctx, ctx->counters_d.ensure((4 + FMAX) * sizeof(unsigned long long)));
         bt.counters = ctx->counters_d.as<unsigned long long>();
-        CUDA_TRY(ctx, cudaMemsetAsync(bt.counters, 0, 2 * sizeof(unsigned long long), ctx->st));
+        CUDA_TRY(ctx, cudaMemsetAsync(bt.counters, 0, (4 + FMAX) * sizeof(unsigned long long), ctx->st));
         int64_t launches = 0;
         for (int s = 1; s <= maxS; ++s) {
             int n_active = 0;
             while (n_active < n && cds[n_active].S >= s) ++n_active;
-            launch_dp_level(bt, s, n_active, warp_prefix[n_active], FL, ctx->st);
-            ctx->launches++;
+            CUDA_TRY(ctx, cudaMemsetAsync(bt.vpool_used[s & 1], 0, sizeof(unsigned long long) * n_active, ctx->st));
+            CUDA_TRY(ctx, cudaMemsetAsync(bt.vspill_used + (s & 1), 0, sizeof(unsigned long long), ctx->st));
+            CUDA_TRY(ctx, cudaMemsetAsync(bt.col_min[s & 1], 0x7f, sizeof(int32_t) * col_prefix[n_active], ctx->st));
+            CUDA_TRY(ctx, cudaMemsetAsync(bt.col_max[s & 1], 0xff, sizeof(int32_t) * col_prefix[n_active], ctx->st));
+            launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, ctx->st);
             ++launches;
+            ctx->launches++;
         }
         if (int rc = check_launch(ctx, "dp_level")) return rc;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev2, ctx->st));
         int ovf = 0;
-        unsigned long long cnt[2] = {0, 0};
+        unsigned long long cnt[4 + FMAX] = {0};
         CUDA_TRY(ctx, cudaMemcpyAsync(&ovf, bt.overflow, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaMemcpyAsync(cnt, bt.counters, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
         ctx->last_pairs += (int64_t)cnt[0];
         ctx->last_cands += (int64_t)cnt[1];
+        ctx->last_inserts += (int64_t)cnt[2];
+        if (getenv("PIPECUT_B200_DEBUG")) {
+            fprintf(stderr, "[pipecut_b200] batch: %d calls, pairs %llu cands %llu inserts %llu ovf %d vcap %d hcap %d\n  frontier sizes:",
+                    n, cnt[0], cnt[1], cnt[2], ovf, vcap, hcap);
+            for (int q = 0; q <= FMAX; ++q)
+                if (cnt[3 + q]) fprintf(stderr, " %d:%llu", q, cnt[3 + q]);
+            fprintf(stderr, "\n");
+        }
         float ms = 0;
         cudaEventElapsedTime(&ms, ctx->ev1, ctx->ev2);
         dp_ms += ms;
@@ -543,10 +632,11 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             first_pass = false;
         }
         ctx->last_dp_launches += launches;
+        if (ovf & 1) return fail(ctx, PC_ERR_CAPACITY, "a Pareto frontier exceeded 64 entries");
         if (!ovf) break;
-        if (FL == 4) FL = 16;
-        else if (FL == 16) FL = 32;
-        else return fail(ctx, PC_ERR_CAPACITY, "a Pareto frontier exceeded 32 entries");
+        // a pool region ran out: grow and rerun the batch
+        vcap *= 2;
+        hcap *= 2;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->st));
     }
     ctx->last_dp_ms += dp_ms;
@@ -581,7 +671,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     CUDA_TRY(ctx, ctx->feasible_d.ensure(sizeof(int32_t) * calls.size()));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->plan_off_d.p, plan_off_orig.data(), sizeof(int32_t) * calls.size(), cudaMemcpyHostToDevice, ctx->st));
     int32_t *seg = ctx->seg_d.as<int32_t>();
-    launch_backtrack(bt, FL, BS, ctx->plan_off_d.as<int32_t>(), seg, seg + seg_total, seg + 2 * seg_total,
+    launch_backtrack(bt, BS, ctx->plan_off_d.as<int32_t>(), seg, seg + seg_total, seg + 2 * seg_total,
                      ctx->objective_d.as<double>(), ctx->feasible_d.as<int32_t>(), ctx->st);
     ctx->launches++;
     if (int rc = check_launch(ctx, "backtrack")) return rc;
@@ -705,7 +795,6 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     ctx->last_calls = cds;
     ctx->last_batch = bt;
     ctx->last_pruning = pruning;
-    ctx->last_FL = FL;
     ctx->last_pos.assign(calls.size(), -1);
     for (int i = 0; i < n; ++i) ctx->last_pos[cds[i].orig] = i;
     return PC_OK;
@@ -725,6 +814,7 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     ctx->last_dp_launches = 0;
     ctx->last_pairs = 0;
     ctx->last_cands = 0;
+    ctx->last_inserts = 0;
     ctx->launches = 0;
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
@@ -735,7 +825,7 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     for (size_t i = 0; i < calls.size(); ++i) {
         const pc_call &c = calls[i];
         const int64_t A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
-        const size_t bytes = (size_t)A * B * (2 * (16 * 4 + 1) + (size_t)c.S * (4 * 4 + 1));
+        const size_t bytes = (size_t)A * B * (2 * (5 + 16 * 4) + (size_t)c.S * (5 + 4 * 4));
         if (!cur.empty() && cur_bytes + bytes > cap) {
             if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
             ++*n_chunks;

@@ -55,6 +55,9 @@ __host__ __device__ inline int64_t tri_idx(int64_t lo, int64_t hi, int64_t nb) {
     return tri_row(lo, nb) + (hi - lo - 1);
 }
 __host__ __device__ inline int64_t tri_size(int64_t nb) { return nb * (nb + 1) / 2; }
+// hi-major triangular index (row hi holds lo = 0 .. hi-1): the DP reads a
+// cell's predecessors lo = b' contiguously.
+__host__ __device__ inline int64_t hm_idx(int64_t lo, int64_t hi) { return hi * (hi - 1) / 2 + lo; }
 
 // _Profiler.cut_time (stages.py:147-157) given the inter-node flag.
 __device__ inline double cut_time_dev(const DevProblem &p, int cut, int64_t m, int inter) {
@@ -69,16 +72,10 @@ __host__ __device__ inline int inter_of(int num_nodes, int dpn, int64_t cum) {
 }
 
 // ------------------------------------------------------------------ key tables
-// One (microbatch share m, checkpointing) key: DP-ready span tables with the
-// boundary transfer already charged (stages.py:232-237):
-//   tfc[inter][tri(lo,hi)] = t_fwd + (hi<nb ? cut_time(hi, m, inter) : 0), NaN if mem > budget
-//   tbc[inter][tri(lo,hi)] = t_bwd + (lo>0  ? cut_time(lo, m, inter) : 0)
-struct KeyTable {
-    int64_t m = 0;
-    int ckpt = 0;
-    double *tfc = nullptr;
-    double *tbc = nullptr;
-};
+// One (microbatch share m, checkpointing) key:
+//   tf[hm_idx(lo,hi)]  t_fwd of span [lo,hi) at m, NaN if mem > budget
+//   tb[hm_idx(lo,hi)]  t_bwd (absent when it is derived as beta * t_fwd)
+//   cut[inter][c]      cut_time(c, m, inter) for c in [0, nb]
 
 // ------------------------------------------------------------------ DP batch
 // One DP call in a level-synchronous batch.  Calls are ordered by S
@@ -88,49 +85,75 @@ struct CallDesc {
     int32_t A, B;              // b-range and d-range sizes: nb-S+1, D-S+1
     int32_t ckpt;
     int32_t key_off;           // keyidx[key_off + dev], dev in [1, B]
-    int64_t val_off;           // cell offset of this call in the ping-pong value buffers
-    int64_t hist_off;          // cell offset of level 1 in the history buffers
+    int64_t val_off;           // cell offset of this call in the ping-pong value arrays
+    int64_t hist_off;          // cell offset of level 1 in the history arrays
+    int64_t vpool_base;        // entry offset of this call in each value pool
+    int64_t vpool_cap;
+    int64_t hpool_base;        // entry offset of this call in the history pool
+    int64_t hpool_cap;
+    int64_t col_off;           // offset of this call's d columns in the column-bound arrays
     int32_t orig;              // index in the caller's call list
     int32_t pad;
 };
+
+constexpr int DP_WARPS = 8;    // warps (d cells) per CTA of the level kernel
+constexpr int FMAX = 64;       // Pareto frontier capacity per cell (two slots per lane)
 
 struct DPBatch {
     int nb;
     int n_calls;
     const CallDesc *calls;
-    const int64_t *warp_prefix;     // [n_calls+1] warps per call (chunks of 32 b x B)
+    const int64_t *cta_prefix;      // [n_calls+1] CTAs per call: ceil(A * B / DP_WARPS)
     const int16_t *keyidx;          // -1 = zero share
-    const double *const *key_tfc;   // device array of per-key table pointers
-    const double *const *key_tbc;
-    int64_t tri;                    // tri_size(nb)
-    int n_inter;
+    const double *const *key_tf;    // per-key table pointers (device arrays)
+    const double *const *key_tb;
+    const double *const *key_cut;
+    const int32_t *const *key_ffb;  // per key: first feasible lo for each hi
+    double beta;
     int num_nodes, dpn;
-    // ping-pong values: [2][FL][val_cells] doubles, counts [2][val_cells]
-    double *val_tf[2];
-    double *val_tb[2];
+    // per level, per (call, d column): smallest / largest b of a non-empty cell
+    int32_t *col_min[2];
+    int32_t *col_max[2];
+    // ping-pong level values: per cell count + offset into the call's pool
+    // region (exact-size allocation by one atomic per cell)
     uint8_t *val_cnt[2];
+    uint32_t *val_off[2];
+    double *pool_tf[2];
+    double *pool_tb[2];
+    unsigned long long *vpool_used[2];  // [n_calls] per parity
+    double *spill_tf[2];                // shared spill pool when a call region is full
+    double *spill_tb[2];
+    unsigned long long *vspill_used;    // [2]
+    int64_t vspill_cap;
     int64_t val_cells;
-    // history: keys [FL][hist_cells] (per level/cell slot), counts [hist_cells]
-    uint32_t *hist_key;
+    // back-pointer history of every level, same scheme
     uint8_t *hist_cnt;
+    uint32_t *hist_off;
+    uint32_t *hpool;
+    unsigned long long *hpool_used;     // [n_calls]
+    uint32_t *hspill;
+    unsigned long long *hspill_used;
+    int64_t hspill_cap;
     int64_t hist_cells;
-    int *overflow;                  // set when a frontier exceeded FL
-    unsigned long long *counters;   // [0] feasible (cell, pred) pairs, [1] candidates
+    int *overflow;                  // 1: frontier > FMAX, 2: a pool region ran out
+    unsigned long long *counters;   // [0] pairs, [1] candidates, [2] inserts, [3..] sizes
 };
 
-// count byte: bits 0-5 entries, bit 6 overflow, bit 7 saw_zero_share
-constexpr uint8_t CNT_MASK = 0x3f;
-constexpr uint8_t CNT_OVF = 0x40;
+// pool offsets: bit 31 set = entry offset into the shared spill pool
+constexpr uint32_t SPILL_BIT = 0x80000000u;
+
+// count byte: bits 0-6 entries, bit 7 saw_zero_share
+constexpr uint8_t CNT_MASK = 0x7f;
 constexpr uint8_t CNT_ZERO = 0x80;
 
 // packed back-pointer (bp, dp, idx): lexicographic order == integer order
 __host__ __device__ inline uint32_t pack_key(uint32_t bp, uint32_t dp, uint32_t idx) {
-    return (bp << 17) | (dp << 5) | idx;
+    return (bp << 18) | (dp << 6) | idx;
 }
-__host__ __device__ inline int key_bp(uint32_t k) { return (int)(k >> 17); }
-__host__ __device__ inline int key_dp(uint32_t k) { return (int)((k >> 5) & 0xfff); }
-__host__ __device__ inline int key_idx(uint32_t k) { return (int)(k & 31); }
-constexpr int MAX_NB_KEY = (1 << 15) - 1;
+__host__ __device__ inline int key_bp(uint32_t k) { return (int)(k >> 18); }
+__host__ __device__ inline int key_dp(uint32_t k) { return (int)((k >> 6) & 0xfff); }
+__host__ __device__ inline int key_idx(uint32_t k) { return (int)(k & 63); }
+constexpr int MAX_NB_KEY = (1 << 14) - 1;
 constexpr int MAX_D_KEY = (1 << 12) - 1;
 
 // ------------------------------------------------------------------ launchers
@@ -140,16 +163,19 @@ void launch_span_time_general(const DevProblem &p, int n_keys, const int64_t *ke
                               double *raw_tf, double *raw_tb, cudaStream_t st);
 void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_m,
                            const int32_t *keys_ckpt, const double *raw_tf, const double *raw_tb,
-                           double *const *tfc, double *const *tbc, cudaStream_t st);
+                           double *const *tf, double *const *tb, double *const *cut,
+                           int derived, int *mismatch, cudaStream_t st);
+void launch_first_feasible(int nb, int n_keys, const double *const *tf, int32_t *const *ffb,
+                           cudaStream_t st);
 void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
                             const int64_t *m, const int32_t *ckpt, double *tf, double *tb,
                             int64_t *mem, cudaStream_t st);
 // dp.cu
-void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_warps, int FL,
+void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool derived,
                      cudaStream_t st);
 void launch_row_visits(const DPBatch &b, int pruning, int64_t *level_sums, int64_t *row_sums,
                        const int64_t *level_row_off, int64_t n_rows_total, cudaStream_t st);
-void launch_backtrack(const DPBatch &b, int FL, int64_t batch_size, const int32_t *plan_off,
+void launch_backtrack(const DPBatch &b, int64_t batch_size, const int32_t *plan_off,
                       int32_t *seg_lo, int32_t *seg_hi, int32_t *seg_dev, double *objective,
                       int32_t *feasible, cudaStream_t st);
 // peak.cu

@@ -5,147 +5,278 @@
 //
 // Within a level s every cell (b, d) depends only on level s-1
 // (stages.py:204-251), so one launch per level covers every active DP call of
-// a batch.  Thread = one cell (b, d); a warp holds 32 consecutive b of one d,
-// so
-//   * the predecessor cells (b', d') of level s-1 are warp-uniform
-//     (broadcast loads, every lane walks the same b' and d'),
-//   * the span records (lo=b', hi=b) are contiguous across lanes
-//     (hi-contiguous triangular tables: coalesced 256 B loads),
-//   * each thread visits its candidates in ascending (b', d', idx) order, the
-//     reference's insertion order, so its private Pareto frontier is exactly
-//     _pareto's output without any cross-thread merge.
-// The frontier lives in registers (capacity FL); a cell that would exceed FL
-// sets a flag and the host reruns the batch with a larger FL -- entries are
-// never dropped silently.
+// a batch.  One warp owns one cell (b, d); a CTA holds the cells of one b for
+// up to DP_WARPS consecutive d, which share the span row of b and the
+// predecessor cells in L1.  Lanes stride over the predecessor blocks b', so
+// every global load is coalesced and independent of the previous one:
+//   * predecessor counts / frontier values of level s-1 ([d'][b'] layout),
+//   * the span row t_fwd(b', b) (hi-major tables, b' contiguous),
+//   * cut times cut(b', m, inter(d')) (per-key [inter][c] tables).
+//
+// Exact _pareto (stages.py:176-185) without ordering constraints: an entry e
+// dominates a candidate c iff e precedes c in the (tf, tb, key) order and
+// e.tb <= c.tb.  That relation is a strict partial order, so the frontier is
+// the set of its maximal elements whatever the insertion order.  The cell's
+// frontier lives in shared memory sorted by tf (capacity FMAX = 32); lanes
+// build candidates in parallel and test them against it by binary search,
+// and only the few survivors are inserted, one warp-cooperative step each.
 #include <math.h>
 
 #include "common.cuh"
 
 namespace pcb {
 
-// Pareto frontier of (max fwd, max bwd) pairs for candidates that arrive in
-// strictly increasing key order.  With keys increasing, the reference's
-// (tf, tb, index) lexicographic filter (stages.py:176-185) reduces to weak
-// dominance: a newcomer is dropped iff some entry has x <= cx and y <= cy,
-// and it removes every entry with cx <= x and cy <= y.
-template <int FL>
-struct Front {
-    double x[FL], y[FL];
-    uint32_t k[FL];
-    uint32_t valid;
-    bool ovf;
-
-    __device__ __forceinline__ void init() {
-        valid = 0;
-        ovf = false;
-    }
-
-    __device__ __forceinline__ void insert(double cx, double cy, uint32_t ck) {
-#pragma unroll
-        for (int j = 0; j < FL; ++j)
-            if (((valid >> j) & 1u) && x[j] <= cx && y[j] <= cy) return;
-#pragma unroll
-        for (int j = 0; j < FL; ++j)
-            if (((valid >> j) & 1u) && cx <= x[j] && cy <= y[j]) valid &= ~(1u << j);
-        bool placed = false;
-#pragma unroll
-        for (int j = 0; j < FL; ++j) {
-            if (!placed && !((valid >> j) & 1u)) {
-                x[j] = cx;
-                y[j] = cy;
-                k[j] = ck;
-                valid |= 1u << j;
-                placed = true;
-            }
-        }
-        if (!placed) ovf = true;
-    }
-};
-
 __device__ __forceinline__ double dmax_ref(double a, double b) {
     // Python max(a, b): b if b > a else a (stages.py:239)
     return b > a ? b : a;
 }
 
-template <int FL>
-__global__ void __launch_bounds__(256) k_dp_level(DPBatch B, int s, int n_active) {
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (gw >= B.warp_prefix[n_active]) return;
+// e dominates c: e before c in (x, y, key) order and e.y <= c.y
+__device__ __forceinline__ bool dominates(double ex, double ey, uint32_t ek, double cx, double cy,
+                                          uint32_t ck) {
+    return ey <= cy && (ex < cx || (ex == cx && (ey < cy || ek < ck)));
+}
+
+struct WarpFront {
+    double *x, *y;     // shared [FMAX], sorted by x ascending (y strictly descending)
+    uint32_t *k;
+};
+
+__device__ __forceinline__ int log2_steps(int n) {
+    // number of binary-search halvings covering n entries (n >= 1)
+    return 32 - __clz(n);
+}
+
+// Is c dominated by the sorted frontier (n entries)?  Binary search for
+// p = #entries before c in (x, y, key) order; dominated iff p > 0 and
+// y[p-1] <= cy (y strictly decreases along the frontier).
+__device__ __forceinline__ bool front_dominated(const WarpFront &f, int n, double cx, double cy,
+                                                uint32_t ck) {
+    int pos = 0;
+    for (int st = 1 << (log2_steps(n) - 1); st > 0; st >>= 1)
+        if (pos + st <= n && f.x[pos + st - 1] < cx) pos += st;
+    if (pos < n && f.x[pos] == cx && (f.y[pos] < cy || (f.y[pos] == cy && f.k[pos] < ck))) ++pos;
+    return pos > 0 && f.y[pos - 1] <= cy;
+}
+
+// Is the corner (tx, ty) strictly dominated: some entry with x <= tx,
+// y <= ty and (x, y) != (tx, ty)?  Every candidate of a predecessor pair is
+// componentwise >= its corner (max(ptf, tfc), max(ptb, tbc)), so a strictly
+// dominated corner settles the whole pair without per-candidate tests.
+__device__ __forceinline__ bool corner_dominated(const WarpFront &f, int n, double tx, double ty) {
+    int pos = 0;   // #entries with x <= tx
+    for (int st = 1 << (log2_steps(n) - 1); st > 0; st >>= 1)
+        if (pos + st <= n && f.x[pos + st - 1] <= tx) pos += st;
+    if (pos == 0) return false;
+    const double ex = f.x[pos - 1], ey = f.y[pos - 1];
+    return ey <= ty && (ex < tx || ey < ty);
+}
+
+// Warp-cooperative exact insert of c (same c in every lane); lane l owns
+// slots l and l + 32.  Returns the new size, or -1 beyond FMAX.
+__device__ __forceinline__ int front_insert(WarpFront &f, int n, int lane, double cx, double cy,
+                                            uint32_t ck) {
+    const bool h0 = lane < n, h1 = lane + 32 < n;
+    double x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+    uint32_t k0 = 0, k1 = 0;
+    if (h0) { x0 = f.x[lane]; y0 = f.y[lane]; k0 = f.k[lane]; }
+    if (h1) { x1 = f.x[lane + 32]; y1 = f.y[lane + 32]; k1 = f.k[lane + 32]; }
+    if (__any_sync(0xffffffffu, (h0 && dominates(x0, y0, k0, cx, cy, ck)) ||
+                                    (h1 && dominates(x1, y1, k1, cx, cy, ck))))
+        return n;
+    const bool keep0 = h0 && !dominates(cx, cy, ck, x0, y0, k0);
+    const bool keep1 = h1 && !dominates(cx, cy, ck, x1, y1, k1);
+    const uint32_t m0 = __ballot_sync(0xffffffffu, keep0);
+    const uint32_t m1 = __ballot_sync(0xffffffffu, keep1);
+    const bool lt0 = keep0 && x0 < cx, lt1 = keep1 && x1 < cx;
+    const int pos_c = __popc(__ballot_sync(0xffffffffu, lt0)) + __popc(__ballot_sync(0xffffffffu, lt1));
+    const int nn = __popc(m0) + __popc(m1) + 1;
+    if (nn > FMAX) return -1;
+    const uint32_t below = (1u << lane) - 1u;
+    const int p0 = __popc(m0 & below) + (lt0 ? 0 : 1);
+    const int p1 = __popc(m0) + __popc(m1 & below) + (lt1 ? 0 : 1);
+    __syncwarp();
+    if (keep0) { f.x[p0] = x0; f.y[p0] = y0; f.k[p0] = k0; }
+    if (keep1) { f.x[p1] = x1; f.y[p1] = y1; f.k[p1] = k1; }
+    if (lane == 0) { f.x[pos_c] = cx; f.y[pos_c] = cy; f.k[pos_c] = ck; }
+    __syncwarp();
+    return nn;
+}
+
+// Lane of the lexicographically smallest (x, y, key) among lanes with
+// `live`.  x, y >= 0, so their IEEE bit patterns order like the values: a
+// cascade of 32-bit warp min-reductions (x high/low word, y high/low word,
+// key) settles it, stopping as soon as one lane is left.
+__device__ __forceinline__ bool lex_stage(bool &live, uint32_t &m, unsigned part) {
+    const unsigned v = live ? part : 0xffffffffu;
+    const unsigned mn = __reduce_min_sync(0xffffffffu, v);
+    live = live && v == mn;
+    m = __ballot_sync(0xffffffffu, live);
+    return __popc(m) <= 1;
+}
+
+__device__ __forceinline__ int lex_min_lane(bool live, double x, double y, uint32_t k) {
+    const unsigned long long xb = (unsigned long long)__double_as_longlong(x);
+    const unsigned long long yb = (unsigned long long)__double_as_longlong(y);
+    uint32_t m = __ballot_sync(0xffffffffu, live);
+    if (__popc(m) > 1 && !lex_stage(live, m, (unsigned)(xb >> 32)) &&
+        !lex_stage(live, m, (unsigned)xb) && !lex_stage(live, m, (unsigned)(yb >> 32)) &&
+        !lex_stage(live, m, (unsigned)yb))
+        lex_stage(live, m, k);
+    return __ffs(m) - 1;
+}
+
+template <bool DERIVED>
+__global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s, int n_active) {
+    __shared__ double sx[DP_WARPS][FMAX], sy[DP_WARPS][FMAX];
+    __shared__ uint32_t sk[DP_WARPS][FMAX];
+    const int64_t cta = blockIdx.x;
+    if (cta >= B.cta_prefix[n_active]) return;
     int lo = 0, hi = n_active;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (B.warp_prefix[mid] <= gw) lo = mid; else hi = mid;
+        if (B.cta_prefix[mid] <= cta) lo = mid; else hi = mid;
     }
     const int c = lo;
     const CallDesc cd = B.calls[c];
-    const int64_t wl = gw - B.warp_prefix[c];
-    const int di = (int)(wl % cd.B);
-    const int bchunk = (int)(wl / cd.B);
-    const int d = s + di;
-    const int bi = bchunk * 32 + lane;
+    // warps take consecutive cells of the call in (b, d) order, so every warp
+    // of the CTA has a cell whatever B is
+    const int w = threadIdx.x >> 5;
+    const int64_t idx = (cta - B.cta_prefix[c]) * DP_WARPS + w;
+    if (idx >= (int64_t)cd.A * cd.B) return;          // whole warp
+    const int bi = (int)(idx / cd.B);
+    const int di = (int)(idx % cd.B);
+    const int lane = threadIdx.x & 31;
     const int b = s + bi;
-    const bool active = bi < cd.A;
+    const int d = s + di;
     const int nb = B.nb;
-    const int64_t tri = B.tri;
     const int64_t cells = (int64_t)cd.A * cd.B;
     const int cur = s & 1, prv = (s - 1) & 1;
     const int16_t *keyidx = B.keyidx + cd.key_off;
     const int inter_d = inter_of(B.num_nodes, B.dpn, d);
-
-    Front<FL> F;
-    F.init();
+    const int64_t row = (int64_t)b * (b - 1) / 2;       // hm_idx(0, b)
+    const double beta = B.beta;
+    WarpFront F{sx[w], sy[w], sk[w]};
+    int n = 0;
+    bool ovf = false;
     bool zero = false;
-    uint32_t n_pairs = 0, n_cands = 0;
+    uint32_t n_pairs = 0, n_cands = 0, n_ins = 0;
 
     if (s == 1) {
         // level 0 holds the single cell (0, 0) with entry (0.0, 0.0) (stages.py:201)
         const int kk = keyidx[d];
         if (kk < 0) {
             zero = true;
-        } else if (active) {
-            const int64_t ti = tri_idx(0, b, nb);
-            const double tfc = B.key_tfc[kk][inter_d * tri + ti];
-            if (!isnan(tfc)) {
-                const double tbc = B.key_tbc[kk][ti];
-                F.insert(dmax_ref(0.0, tfc), dmax_ref(0.0, tbc), pack_key(0, 0, 0));
-                n_pairs = 1;
-                n_cands = 1;
+        } else {
+            const double tf = B.key_tf[kk][row];
+            if (!isnan(tf)) {
+                double tfc = tf;
+                if (b < nb) tfc = __dadd_rn(tf, B.key_cut[kk][inter_d * (nb + 1) + b]);
+                const double tbc = DERIVED ? __dmul_rn(beta, tf) : B.key_tb[kk][row];
+                if (lane == 0) {
+                    F.x[0] = dmax_ref(0.0, tfc);
+                    F.y[0] = dmax_ref(0.0, tbc);
+                    F.k[0] = pack_key(0, 0, 0);
+                }
+                __syncwarp();
+                n = 1;
+                n_pairs = lane == 0;
+                n_cands = lane == 0;
             }
         }
     } else {
+        // Predecessor columns d' in order; within a column only b' from
+        // max(first non-empty b' of the column, first feasible lo of the key)
+        // to min(last non-empty b', b - 1) can yield a candidate.  The frontier
+        // is order-independent (see top), so this order is as good as the
+        // reference's.
         const int base = s - 1;
-        const int bmax = s + min(bchunk * 32 + 31, cd.A - 1);
-        const double *ptf = B.val_tf[prv] + cd.val_off;
-        const double *ptb = B.val_tb[prv] + cd.val_off;
         const uint8_t *pcnt = B.val_cnt[prv] + cd.val_off;
-        const int64_t vstride = B.val_cells;
-        for (int bp = base; bp < bmax; ++bp) {
-            const bool lane_ok = active && bp < b;
-            const int64_t ti = lane_ok ? tri_idx(bp, b, nb) : 0;
-            for (int dp = base; dp < d; ++dp) {
-                const int64_t pc = (int64_t)(dp - base) * cd.A + (bp - base);
-                const int cnt = pcnt[pc] & CNT_MASK;
-                if (cnt == 0) continue;
-                const int kk = keyidx[d - dp];
-                if (kk < 0) {                      // m == 0 (stages.py:224-228)
-                    zero |= lane_ok;
-                    continue;
+        const uint32_t *poff = B.val_off[prv] + cd.val_off;
+        const double *qtf = B.pool_tf[prv] + cd.vpool_base;
+        const double *qtb = B.pool_tb[prv] + cd.vpool_base;
+        const double *stf = B.spill_tf[prv];
+        const double *stb = B.spill_tb[prv];
+        const int32_t *cmin = B.col_min[prv] + cd.col_off;
+        const int32_t *cmax = B.col_max[prv] + cd.col_off;
+        const double *tfrow_base = nullptr;
+        for (int dp = base; dp < d; ++dp) {
+            const int lo_col = cmin[dp - base];
+            const int hi_col = cmax[dp - base];
+            if (lo_col > hi_col || lo_col >= b) continue;           // no predecessor cell
+            const int kk = keyidx[d - dp];                          // warp-uniform
+            if (kk < 0) {                                           // m == 0 (stages.py:224-228)
+                zero = true;
+                continue;
+            }
+            const int bp_lo = max(lo_col, B.key_ffb[kk][b]);
+            const int bp_hi = min(hi_col, b - 1);
+            if (bp_lo > bp_hi) continue;                            // all spans infeasible
+            const double *tfrow = B.key_tf[kk] + row;
+            const double *tbrow = DERIVED ? nullptr : B.key_tb[kk] + row;
+            const double cutf = b < nb ? B.key_cut[kk][inter_d * (nb + 1) + b] : 0.0;
+            const double *cutb = B.key_cut[kk] + inter_of(B.num_nodes, B.dpn, dp) * (nb + 1);
+            const uint8_t *ccol = pcnt + (int64_t)(dp - base) * cd.A - base;
+            const uint32_t *ocol = poff + (int64_t)(dp - base) * cd.A - base;
+            for (int bp0 = bp_lo; bp0 <= bp_hi; bp0 += 32) {
+                const int bp = bp0 + lane;
+                int cnt = bp <= bp_hi ? (ccol[bp] & CNT_MASK) : 0;
+                double tfc = 0.0, tbc = 0.0;
+                int wlo = 0, whi = -1;
+                const double *etf = qtf, *etb = qtb;
+                int64_t pbase = 0;
+                if (cnt > 0) {
+                    const double tf = tfrow[bp];
+                    if (!isnan(tf)) {                               // mem <= budget (stages.py:230)
+                        tfc = b < nb ? __dadd_rn(tf, cutf) : tf;
+                        tbc = DERIVED ? __dmul_rn(beta, tf) : tbrow[bp];
+                        if (bp > 0) tbc = __dadd_rn(tbc, cutb[bp]);
+                        ++n_pairs;
+                        n_cands += cnt;
+                        if (n == 0 || !corner_dominated(F, n, tfc, tbc)) {
+                            const uint32_t praw = ocol[bp];
+                            pbase = (int64_t)(praw & ~SPILL_BIT);
+                            if (praw & SPILL_BIT) { etf = stf; etb = stb; }
+                            // exact window: entries with ptf <= tfc collapse onto the
+                            // last of them, entries with ptb <= tbc onto the first
+                            int i0 = -1, i1 = cnt;
+                            for (int i = 0; i < cnt; ++i) {
+                                if (etf[pbase + i] <= tfc) i0 = i;
+                                if (i1 == cnt && etb[pbase + i] <= tbc) i1 = i;
+                            }
+                            if (i1 <= i0) { wlo = i1; whi = i1; }
+                            else { wlo = i0 < 0 ? 0 : i0; whi = i1 < cnt ? i1 : cnt - 1; }
+                        }
+                    }
                 }
-                if (!lane_ok) continue;
-                const double tfc = B.key_tfc[kk][inter_d * tri + ti];
-                if (isnan(tfc)) continue;          // mem > budget (stages.py:230)
-                const int inter_dp = inter_of(B.num_nodes, B.dpn, dp);
-                const double tbc = B.key_tbc[kk][inter_dp * tri + ti];
-                ++n_pairs;
-                n_cands += cnt;
-                for (int i = 0; i < cnt; ++i) {
-                    const double a = ptf[i * vstride + pc];
-                    const double bb = ptb[i * vstride + pc];
-                    F.insert(dmax_ref(a, tfc), dmax_ref(bb, tbc), pack_key(bp, dp, i));
+                const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)(whi - wlo + 1));
+                for (int r = 0; r < rounds; ++r) {
+                    const int i = wlo + r;
+                    double cx = 0.0, cy = 0.0;
+                    uint32_t ck = 0;
+                    bool surv = false;
+                    if (i <= whi) {
+                        cx = dmax_ref(etf[pbase + i], tfc);
+                        cy = dmax_ref(etb[pbase + i], tbc);
+                        ck = pack_key(bp, dp, i);
+                        surv = n == 0 || !front_dominated(F, n, cx, cy, ck);
+                    }
+                    while (__any_sync(0xffffffffu, surv)) {
+                        // insert the lexicographically smallest survivor first: nothing
+                        // among the survivors can dominate it, and it removes the most
+                        const int t = lex_min_lane(surv, cx, cy, ck);
+                        const double tx = __shfl_sync(0xffffffffu, cx, t);
+                        const double ty = __shfl_sync(0xffffffffu, cy, t);
+                        const uint32_t tk = __shfl_sync(0xffffffffu, ck, t);
+                        ++n_ins;
+                        const int nn = front_insert(F, n, lane, tx, ty, tk);
+                        if (nn < 0) ovf = true; else n = nn;
+                        surv = surv && lane != t && !dominates(tx, ty, tk, cx, cy, ck);
+                    }
                 }
             }
         }
+        (void)tfrow_base;
     }
     // algorithmic work counters (one atomic per warp)
 #pragma unroll
@@ -156,40 +287,68 @@ __global__ void __launch_bounds__(256) k_dp_level(DPBatch B, int s, int n_active
     if (lane == 0) {
         atomicAdd(&B.counters[0], (unsigned long long)n_pairs);
         atomicAdd(&B.counters[1], (unsigned long long)n_cands);
+        atomicAdd(&B.counters[2], (unsigned long long)n_ins);
+        atomicAdd(&B.counters[3 + min(n, FMAX)], 1ull);     // frontier-size histogram
     }
-    if (!active) return;
+    const bool any_zero = __any_sync(0xffffffffu, zero);
 
-    // emit in tf-ascending order (entries have distinct tf)
+    // emit the frontier (sorted by tf) into exact-size pool slots
     const int64_t cell = (int64_t)di * cd.A + bi;
-    int n = 0;
-    uint8_t byte = 0;
-#pragma unroll
-    for (int j = 0; j < FL; ++j) {
-        if (!((F.valid >> j) & 1u)) continue;
-        int rank = 0;
-#pragma unroll
-        for (int i = 0; i < FL; ++i)
-            if (((F.valid >> i) & 1u) && F.x[i] < F.x[j]) ++rank;
-        B.val_tf[cur][rank * B.val_cells + cd.val_off + cell] = F.x[j];
-        B.val_tb[cur][rank * B.val_cells + cd.val_off + cell] = F.y[j];
-        B.hist_key[rank * B.hist_cells + cd.hist_off + (int64_t)(s - 1) * cells + cell] = F.k[j];
-        ++n;
+    const int64_t hcell = cd.hist_off + (int64_t)(s - 1) * cells + cell;
+    const int64_t vcell = cd.val_off + cell;
+    if (ovf) n = 0;
+    if (n > 0) {
+        // exact-size slots in the call's region, or the shared spill pool
+        unsigned long long vo = 0, ho = 0;
+        if (lane == 0) {
+            vo = atomicAdd(&B.vpool_used[cur][c], (unsigned long long)n);
+            if ((int64_t)(vo + n) > cd.vpool_cap)
+                vo = SPILL_BIT | atomicAdd(&B.vspill_used[cur], (unsigned long long)n);
+            ho = atomicAdd(&B.hpool_used[c], (unsigned long long)n);
+            if ((int64_t)(ho + n) > cd.hpool_cap)
+                ho = SPILL_BIT | atomicAdd(B.hspill_used, (unsigned long long)n);
+        }
+        vo = __shfl_sync(0xffffffffu, vo, 0);
+        ho = __shfl_sync(0xffffffffu, ho, 0);
+        const bool vs = (vo & SPILL_BIT) != 0, hs = (ho & SPILL_BIT) != 0;
+        const int64_t vi = (int64_t)(vo & ~(unsigned long long)SPILL_BIT);
+        const int64_t hi2 = (int64_t)(ho & ~(unsigned long long)SPILL_BIT);
+        if ((vs && vi + n > B.vspill_cap) || (hs && hi2 + n > B.hspill_cap)) {
+            if (lane == 0) atomicOr(B.overflow, 2);
+            n = 0;
+        } else {
+            double *otf = vs ? B.spill_tf[cur] + vi : B.pool_tf[cur] + cd.vpool_base + vi;
+            double *otb = vs ? B.spill_tb[cur] + vi : B.pool_tb[cur] + cd.vpool_base + vi;
+            uint32_t *okk = hs ? B.hspill + hi2 : B.hpool + cd.hpool_base + hi2;
+            for (int j = lane; j < n; j += 32) {
+                otf[j] = F.x[j];
+                otb[j] = F.y[j];
+                okk[j] = F.k[j];
+            }
+            if (lane == 0) {
+                B.val_off[cur][vcell] = (uint32_t)vi | (vs ? SPILL_BIT : 0u);
+                B.hist_off[hcell] = (uint32_t)hi2 | (hs ? SPILL_BIT : 0u);
+                atomicMin(&B.col_min[cur][cd.col_off + di], b);
+                atomicMax(&B.col_max[cur][cd.col_off + di], b);
+            }
+        }
     }
-    byte = (uint8_t)n | (zero ? CNT_ZERO : 0) | (F.ovf ? CNT_OVF : 0);
-    B.val_cnt[cur][cd.val_off + cell] = byte;
-    B.hist_cnt[cd.hist_off + (int64_t)(s - 1) * cells + cell] = byte;
-    if (F.ovf) atomicOr(B.overflow, 1);
+    if (lane == 0) {
+        const uint8_t byte = (uint8_t)n | (any_zero ? CNT_ZERO : 0);
+        B.val_cnt[cur][vcell] = byte;
+        B.hist_cnt[hcell] = byte;
+        if (ovf) atomicOr(B.overflow, 1);
+    }
 }
 
-void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_warps, int FL,
+void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool derived,
                      cudaStream_t st) {
-    const int tpb = 256;
-    const int64_t blocks = (n_warps * 32 + tpb - 1) / tpb;
-    switch (FL) {
-        case 4: k_dp_level<4><<<(unsigned)blocks, tpb, 0, st>>>(b, s, n_active); break;
-        case 16: k_dp_level<16><<<(unsigned)blocks, tpb, 0, st>>>(b, s, n_active); break;
-        default: k_dp_level<32><<<(unsigned)blocks, tpb, 0, st>>>(b, s, n_active); break;
-    }
+    const int tpb = DP_WARPS * 32;
+    const unsigned blocks = (unsigned)n_ctas;
+    if (derived)
+        k_dp_level<true><<<blocks, tpb, 0, st>>>(b, s, n_active);
+    else
+        k_dp_level<false><<<blocks, tpb, 0, st>>>(b, s, n_active);
 }
 
 // ---------------------------------------------------------------- visits (K7)
@@ -280,23 +439,24 @@ __global__ void k_backtrack(DPBatch Bt, int64_t batch_size, const int32_t *plan_
     const int64_t cells = (int64_t)cd.A * cd.B;
     const int64_t fcell = (int64_t)(cd.B - 1) * cd.A + (cd.A - 1);   // (nb, D)
     const int par = S & 1;
-    const uint8_t byte = Bt.val_cnt[par][cd.val_off + fcell];
-    const int n = byte & CNT_MASK;
+    const int64_t vcell = cd.val_off + fcell;
+    const int n = Bt.val_cnt[par][vcell] & CNT_MASK;
     const int o = cd.orig;
     if (n == 0) {
         feasible[o] = 0;
         return;
     }
+    const uint32_t vo = Bt.val_off[par][vcell];
+    const int64_t vi = vo & ~SPILL_BIT;
+    const double *vx = (vo & SPILL_BIT) ? Bt.spill_tf[par] + vi : Bt.pool_tf[par] + cd.vpool_base + vi;
+    const double *vy = (vo & SPILL_BIT) ? Bt.spill_tb[par] + vi : Bt.pool_tb[par] + cd.vpool_base + vi;
     int best = 0;
-    double bx = Bt.val_tf[par][cd.val_off + fcell];
-    double by = Bt.val_tb[par][cd.val_off + fcell];
+    double bx = vx[0], by = vy[0];
     for (int j = 1; j < n; ++j) {
-        const double x = Bt.val_tf[par][j * Bt.val_cells + cd.val_off + fcell];
-        const double y = Bt.val_tb[par][j * Bt.val_cells + cd.val_off + fcell];
-        if (__dadd_rn(x, y) < __dadd_rn(bx, by)) {
+        if (__dadd_rn(vx[j], vy[j]) < __dadd_rn(bx, by)) {
             best = j;
-            bx = x;
-            by = y;
+            bx = vx[j];
+            by = vy[j];
         }
     }
     feasible[o] = 1;
@@ -305,8 +465,10 @@ __global__ void k_backtrack(DPBatch Bt, int64_t batch_size, const int32_t *plan_
     int64_t cell = fcell;
     const int32_t off = plan_off[o];
     while (s > 0) {
-        const uint32_t key =
-            Bt.hist_key[(int64_t)j * Bt.hist_cells + cd.hist_off + (int64_t)(s - 1) * cells + cell];
+        const int64_t hcell = cd.hist_off + (int64_t)(s - 1) * cells + cell;
+        const uint32_t ho = Bt.hist_off[hcell];
+        const uint32_t key = (ho & SPILL_BIT) ? Bt.hspill[(ho & ~SPILL_BIT) + j]
+                                              : Bt.hpool[cd.hpool_base + ho + j];
         const int bp = key_bp(key), dp = key_dp(key);
         seg_lo[off + s - 1] = bp;
         seg_hi[off + s - 1] = b;
@@ -319,10 +481,9 @@ __global__ void k_backtrack(DPBatch Bt, int64_t batch_size, const int32_t *plan_
     }
 }
 
-void launch_backtrack(const DPBatch &b, int FL, int64_t batch_size, const int32_t *plan_off,
+void launch_backtrack(const DPBatch &b, int64_t batch_size, const int32_t *plan_off,
                       int32_t *seg_lo, int32_t *seg_hi, int32_t *seg_dev, double *objective,
                       int32_t *feasible, cudaStream_t st) {
-    (void)FL;
     k_backtrack<<<(b.n_calls + 127) / 128, 128, 0, st>>>(b, batch_size, plan_off, seg_lo, seg_hi,
                                                          seg_dev, objective, feasible);
 }

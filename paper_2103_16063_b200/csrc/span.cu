@@ -106,11 +106,18 @@ void launch_span_time_general(const DevProblem &p, int n_keys, const int64_t *ke
 //     footprint counting only predecessors owned in blocks >= lo;
 //   * in the monotone case the time fold itself (blocks in sorted-id order,
 //     so extending hi continues the reference's fold exactly);
-//   * memory (costs.py:157-159) and the DP-ready tables with cut times.
+//   * memory (costs.py:157-159) -> feasibility (stages.py:230) folded into the
+//     table as NaN;
+//   * its row of the per-key cut-time table (stages.py:147-157).
+// Output layout is hi-major (lo contiguous), the DP's predecessor order.
+// With beta a power of two, t_bwd == beta * t_fwd exactly (scaling by 2^k
+// commutes with every rounding of the fold); the DP then derives it and only
+// t_fwd is stored -- verified here for every span, flag set on any mismatch.
 template <bool MONO>
 __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
                             const int32_t *keys_ckpt, const double *raw_tf,
-                            const double *raw_tb, double *const *tfc, double *const *tbc) {
+                            const double *raw_tb, double *const *tf_out, double *const *tb_out,
+                            double *const *cut_out, int derived, int *mismatch) {
     const int nb = p.nb;
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (int64_t)n_keys * nb) return;
@@ -120,13 +127,16 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
     const double md = (double)m;
     const int ckpt = keys_ckpt[k];
     const int64_t tri = tri_size(nb);
-    double *out_f = tfc[k];
-    double *out_b = tbc[k];
+    double *out_f = tf_out[k];
+    double *out_b = derived ? nullptr : tb_out[k];
+    double *cut = cut_out[k];
+    for (int i = 0; i < 2; ++i) {
+        cut[(int64_t)i * (nb + 1) + lo] = cut_time_dev(p, lo, m, i);
+        if (lo == nb - 1) cut[(int64_t)i * (nb + 1) + nb] = cut_time_dev(p, nb, m, i);
+    }
     double tf = 0.0, tb = 0.0;
     int64_t run_fp = 0;
-    double cutb[2] = {0.0, 0.0};
-    if (lo > 0)
-        for (int i = 0; i < p.n_inter; ++i) cutb[i] = cut_time_dev(p, lo, m, i);
+    bool bad = false;
     const int64_t row = tri_row(lo, nb);
     for (int hi = lo + 1; hi <= nb; ++hi) {
         const int blk = hi - 1;
@@ -157,29 +167,49 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
         const double memd = __dadd_rn(__dmul_rn((double)param, p.factor), (double)act);
         const int64_t mem = (int64_t)memd;
         const bool ok = mem <= p.mem_budget;                   // stages.py:230
-        for (int i = 0; i < p.n_inter; ++i) {
-            double ff = f;
-            if (hi < nb) ff = __dadd_rn(f, cut_time_dev(p, hi, m, i));
-            double bb = b;
-            if (lo > 0) bb = __dadd_rn(b, cutb[i]);
-            out_f[(int64_t)i * tri + idx] = ok ? ff : __longlong_as_double(0x7ff8000000000000LL);
-            out_b[(int64_t)i * tri + idx] = bb;
+        const int64_t o = hm_idx(lo, hi);
+        out_f[o] = ok ? f : __longlong_as_double(0x7ff8000000000000LL);
+        if (derived) {
+            bad |= ok && __dmul_rn(p.beta, f) != b;
+        } else {
+            out_b[o] = b;
         }
     }
+    if (bad) atomicOr(mismatch, 1);
 }
 
 void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_m,
                            const int32_t *keys_ckpt, const double *raw_tf, const double *raw_tb,
-                           double *const *tfc, double *const *tbc, cudaStream_t st) {
+                           double *const *tf, double *const *tb, double *const *cut,
+                           int derived, int *mismatch, cudaStream_t st) {
     const int64_t n = (int64_t)n_keys * p.nb;
     const int tpb = 128;
     const unsigned blocks = (unsigned)((n + tpb - 1) / tpb);
     if (p.monotone)
         k_span_rows<true><<<blocks, tpb, 0, st>>>(p, n_keys, keys_m, keys_ckpt, raw_tf, raw_tb,
-                                                 tfc, tbc);
+                                                 tf, tb, cut, derived, mismatch);
     else
         k_span_rows<false><<<blocks, tpb, 0, st>>>(p, n_keys, keys_m, keys_ckpt, raw_tf, raw_tb,
-                                                  tfc, tbc);
+                                                  tf, tb, cut, derived, mismatch);
+}
+
+// First feasible lo of every hi (per key): the DP skips b' below it, which
+// are all infeasible by construction (no monotonicity assumed).
+__global__ void k_first_feasible(int nb, int n_keys, const double *const *tf, int32_t *const *ffb) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (int64_t)n_keys * (nb + 1)) return;
+    const int k = (int)(gid / (nb + 1));
+    const int hi = (int)(gid % (nb + 1));
+    const double *row = tf[k] + hm_idx(0, hi);
+    int lo = 0;
+    while (lo < hi && isnan(row[lo])) ++lo;
+    ffb[k][hi] = lo;
+}
+
+void launch_first_feasible(int nb, int n_keys, const double *const *tf, int32_t *const *ffb,
+                           cudaStream_t st) {
+    const int64_t n = (int64_t)n_keys * (nb + 1);
+    k_first_feasible<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(nb, n_keys, tf, ffb);
 }
 
 // ---------------------------------------------------------------- queries
