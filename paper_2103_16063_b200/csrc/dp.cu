@@ -37,9 +37,18 @@ __device__ __forceinline__ bool dominates(double ex, double ey, uint32_t ek, dou
     return ey <= cy && (ex < cx || (ex == cx && (ey < cy || ek < ck)));
 }
 
+// Per-warp Pareto frontiers in shared memory, each sorted by x ascending
+// (y strictly descending).  Namespace scope so every access compiles to
+// LDS/STS rather than generic loads.
+__shared__ double g_fx[DP_WARPS][FMAX];
+__shared__ double g_fy[DP_WARPS][FMAX];
+__shared__ uint32_t g_fk[DP_WARPS][FMAX];
+
 struct WarpFront {
-    double *x, *y;     // shared [FMAX], sorted by x ascending (y strictly descending)
-    uint32_t *k;
+    int w;
+    __device__ __forceinline__ double &x(int j) const { return g_fx[w][j]; }
+    __device__ __forceinline__ double &y(int j) const { return g_fy[w][j]; }
+    __device__ __forceinline__ uint32_t &k(int j) const { return g_fk[w][j]; }
 };
 
 __device__ __forceinline__ int log2_steps(int n) {
@@ -54,9 +63,9 @@ __device__ __forceinline__ bool front_dominated(const WarpFront &f, int n, doubl
                                                 uint32_t ck) {
     int pos = 0;
     for (int st = 1 << (log2_steps(n) - 1); st > 0; st >>= 1)
-        if (pos + st <= n && f.x[pos + st - 1] < cx) pos += st;
-    if (pos < n && f.x[pos] == cx && (f.y[pos] < cy || (f.y[pos] == cy && f.k[pos] < ck))) ++pos;
-    return pos > 0 && f.y[pos - 1] <= cy;
+        if (pos + st <= n && f.x(pos + st - 1) < cx) pos += st;
+    if (pos < n && f.x(pos) == cx && (f.y(pos) < cy || (f.y(pos) == cy && f.k(pos) < ck))) ++pos;
+    return pos > 0 && f.y(pos - 1) <= cy;
 }
 
 // Is the corner (tx, ty) strictly dominated: some entry with x <= tx,
@@ -66,9 +75,9 @@ __device__ __forceinline__ bool front_dominated(const WarpFront &f, int n, doubl
 __device__ __forceinline__ bool corner_dominated(const WarpFront &f, int n, double tx, double ty) {
     int pos = 0;   // #entries with x <= tx
     for (int st = 1 << (log2_steps(n) - 1); st > 0; st >>= 1)
-        if (pos + st <= n && f.x[pos + st - 1] <= tx) pos += st;
+        if (pos + st <= n && f.x(pos + st - 1) <= tx) pos += st;
     if (pos == 0) return false;
-    const double ex = f.x[pos - 1], ey = f.y[pos - 1];
+    const double ex = f.x(pos - 1), ey = f.y(pos - 1);
     return ey <= ty && (ex < tx || ey < ty);
 }
 
@@ -79,8 +88,8 @@ __device__ __forceinline__ int front_insert(WarpFront &f, int n, int lane, doubl
     const bool h0 = lane < n, h1 = lane + 32 < n;
     double x0 = 0, y0 = 0, x1 = 0, y1 = 0;
     uint32_t k0 = 0, k1 = 0;
-    if (h0) { x0 = f.x[lane]; y0 = f.y[lane]; k0 = f.k[lane]; }
-    if (h1) { x1 = f.x[lane + 32]; y1 = f.y[lane + 32]; k1 = f.k[lane + 32]; }
+    if (h0) { x0 = f.x(lane); y0 = f.y(lane); k0 = f.k(lane); }
+    if (h1) { x1 = f.x(lane + 32); y1 = f.y(lane + 32); k1 = f.k(lane + 32); }
     if (__any_sync(0xffffffffu, (h0 && dominates(x0, y0, k0, cx, cy, ck)) ||
                                     (h1 && dominates(x1, y1, k1, cx, cy, ck))))
         return n;
@@ -96,9 +105,9 @@ __device__ __forceinline__ int front_insert(WarpFront &f, int n, int lane, doubl
     const int p0 = __popc(m0 & below) + (lt0 ? 0 : 1);
     const int p1 = __popc(m0) + __popc(m1 & below) + (lt1 ? 0 : 1);
     __syncwarp();
-    if (keep0) { f.x[p0] = x0; f.y[p0] = y0; f.k[p0] = k0; }
-    if (keep1) { f.x[p1] = x1; f.y[p1] = y1; f.k[p1] = k1; }
-    if (lane == 0) { f.x[pos_c] = cx; f.y[pos_c] = cy; f.k[pos_c] = ck; }
+    if (keep0) { f.x(p0) = x0; f.y(p0) = y0; f.k(p0) = k0; }
+    if (keep1) { f.x(p1) = x1; f.y(p1) = y1; f.k(p1) = k1; }
+    if (lane == 0) { f.x(pos_c) = cx; f.y(pos_c) = cy; f.k(pos_c) = ck; }
     __syncwarp();
     return nn;
 }
@@ -128,8 +137,6 @@ __device__ __forceinline__ int lex_min_lane(bool live, double x, double y, uint3
 
 template <bool DERIVED>
 __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s, int n_active) {
-    __shared__ double sx[DP_WARPS][FMAX], sy[DP_WARPS][FMAX];
-    __shared__ uint32_t sk[DP_WARPS][FMAX];
     const int64_t cta = blockIdx.x;
     if (cta >= B.cta_prefix[n_active]) return;
     int lo = 0, hi = n_active;
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
     const int inter_d = inter_of(B.num_nodes, B.dpn, d);
     const int64_t row = (int64_t)b * (b - 1) / 2;       // hm_idx(0, b)
     const double beta = B.beta;
-    WarpFront F{sx[w], sy[w], sk[w]};
+    WarpFront F{w};
     int n = 0;
     bool ovf = false;
     bool zero = false;
@@ -174,9 +181,9 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
                 if (b < nb) tfc = __dadd_rn(tf, B.key_cut[kk][inter_d * (nb + 1) + b]);
                 const double tbc = DERIVED ? __dmul_rn(beta, tf) : B.key_tb[kk][row];
                 if (lane == 0) {
-                    F.x[0] = dmax_ref(0.0, tfc);
-                    F.y[0] = dmax_ref(0.0, tbc);
-                    F.k[0] = pack_key(0, 0, 0);
+                    F.x(0) = dmax_ref(0.0, tfc);
+                    F.y(0) = dmax_ref(0.0, tbc);
+                    F.k(0) = pack_key(0, 0, 0);
                 }
                 __syncwarp();
                 n = 1;
@@ -321,9 +328,9 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
             double *otb = vs ? B.spill_tb[cur] + vi : B.pool_tb[cur] + cd.vpool_base + vi;
             uint32_t *okk = hs ? B.hspill + hi2 : B.hpool + cd.hpool_base + hi2;
             for (int j = lane; j < n; j += 32) {
-                otf[j] = F.x[j];
-                otb[j] = F.y[j];
-                okk[j] = F.k[j];
+                otf[j] = F.x(j);
+                otb[j] = F.y(j);
+                okk[j] = F.k(j);
             }
             if (lane == 0) {
                 B.val_off[cur][vcell] = (uint32_t)vi | (vs ? SPILL_BIT : 0u);
