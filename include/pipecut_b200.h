@@ -88,6 +88,39 @@ typedef struct pc_problem {
     double latency;
 } pc_problem;
 
+/*
+ * Flattened atomic partition for partition_blocks (blocks.py:73-124): what the
+ * memory of any atom set at microbatch 1 with checkpointing, convexity and
+ * cut traffic need (paper_2103_16063_b200/flatten.py: flatten_atoms).
+ */
+typedef struct pc_atoms {
+    int32_t n;                  /* atoms (topological order) */
+    int32_t n_tasks;
+    int32_t n_in;               /* values listed in some atom's input_values */
+    int32_t n_traffic;          /* value traffic entries (blocks.py:96-102) */
+    const int64_t *atom_param;  /* [n] parameter bytes owned by each atom */
+    const int32_t *task_atom;   /* [n_tasks] sorted node-id order */
+    const double  *task_flops;  /* [n_tasks] */
+    const int64_t *task_fp1;    /* [n_tasks] produced + always-counted preds at m=1 */
+    const int32_t *dep_off;     /* [n_tasks+1] anchor inputs owned by atom dep_owner */
+    const int32_t *dep_owner;
+    const int64_t *dep_size;
+    const int32_t *atom_task_off, *atom_tasks;   /* tasks of each atom, ascending */
+    const int32_t *atom_in_off, *atom_in;        /* input values of each atom */
+    const int32_t *in_owner;    /* [n_in] owner atom, -1 model input / unowned */
+    const int64_t *in_size;     /* [n_in] size at m=1 */
+    const int32_t *in_atoms_off, *in_atoms;      /* atoms listing each input, ascending */
+    const int32_t *succ_off, *succ;              /* partition.dependencies() */
+    const int32_t *pred_off, *pred;
+    const int32_t *nbr_off, *nbr;                /* sorted(succ | pred) */
+    const int32_t *tr_owner;    /* [n_traffic] */
+    const int64_t *tr_size;
+    const int32_t *tr_cons_off, *tr_cons;        /* foreign consumer atoms */
+    const int32_t *atom_tr_off, *atom_tr;        /* traffic entries touching each atom */
+    int64_t budget;             /* ClusterSpec.device_memory_bytes */
+    double flops_per_sec, bwd_fwd_ratio, grad_factor, opt_factor;
+} pc_atoms;
+
 /* One DP call of _run_dp (stages.py:188): S stages on D devices. */
 typedef struct pc_call {
     int32_t S, D, R, MB;        /* stage count, devices, replica factor, microbatches */
@@ -170,6 +203,17 @@ int pc_form_stage(pc_ctx *ctx, int32_t num_nodes, int32_t devices_per_node,
  * the visits accumulated before it (stages.py:214-216): -1 if not crossed. */
 int pc_last_crossing(pc_ctx *ctx, int32_t index, int64_t visits_before, int64_t budget,
                      int64_t *visits_at_cross);
+
+/* partition_blocks (blocks.py:361-397): at most k convex, memory-feasible
+ * blocks in dependency order.  Outputs (caller capacity n atoms): n_blocks,
+ * block_off[n_blocks+1], block_atoms[n] (ascending within a block), and per
+ * block t_fwd, t_bwd, mem = CostModel.profile(block, 1, ckpt=True)
+ * (blocks.py:390).  PC_ERR_ATOM: err[0] = atom index, err[1] = its memory
+ * (InfeasibleAtom); PC_ERR_STUCK: err[0] = groups left (CompactionStuck);
+ * PC_ERR_INVALID: k < 1. */
+int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *atoms, int32_t k, int32_t *n_blocks,
+                        int32_t *block_off, int32_t *block_atoms, double *t_fwd,
+                        double *t_bwd, int64_t *mem, int64_t *err);
 
 /* Drop the cached span/cut tables (they are rebuilt on demand). */
 int pc_reset_cache(pc_ctx *ctx);

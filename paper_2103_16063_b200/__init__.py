@@ -2,8 +2,10 @@
 
 Drop-in replacements for the reference package `pipecut`'s hot path:
 
-    form_stage_dp   (pkg/src/pipecut/stages.py:282-291)
-    form_stage      (pkg/src/pipecut/stages.py:372-413)
+    partition_blocks (pkg/src/pipecut/blocks.py:361-397)
+    form_stage_dp    (pkg/src/pipecut/stages.py:282-291)
+    form_stage       (pkg/src/pipecut/stages.py:372-413)
+    form_stage_sharded  -- form_stage over the GPUs of a torch.distributed group
 
 They take and return the reference's own host objects (BlockSet,
 SearchOptions, SearchResult, Plan) and run the span-cost tables, the Pareto
@@ -13,19 +15,22 @@ CLI and library users pick the GPU path up unchanged.
 """
 
 from ._host import pipecut as _pc  # noqa: F401  (host API package)
+from .blocks import partition_blocks
+from .search import form_stage_sharded
 from .stages import form_stage, form_stage_dp
 
-__all__ = ["form_stage", "form_stage_dp", "install"]
+__all__ = ["form_stage", "form_stage_dp", "form_stage_sharded", "install", "partition_blocks"]
 
 
 def install():
     """Point the reference's modules at the GPU entry points."""
     import pipecut
+    import pipecut.blocks
     import pipecut.cli
     import pipecut.stages
 
-    for mod in (pipecut, pipecut.stages, pipecut.cli):
-        if hasattr(mod, "form_stage"):
-            mod.form_stage = form_stage
-        if hasattr(mod, "form_stage_dp"):
-            mod.form_stage_dp = form_stage_dp
+    for mod in (pipecut, pipecut.stages, pipecut.blocks, pipecut.cli):
+        for name, fn in (("form_stage", form_stage), ("form_stage_dp", form_stage_dp),
+                         ("partition_blocks", partition_blocks)):
+            if hasattr(mod, name):
+                setattr(mod, name, fn)

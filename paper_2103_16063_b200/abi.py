@@ -58,6 +58,45 @@ class PcProblem(C.Structure):
     ]
 
 
+class PcAtoms(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32), ("n_tasks", C.c_int32), ("n_in", C.c_int32), ("n_traffic", C.c_int32),
+        ("atom_param", _i64p),
+        ("task_atom", _i32p), ("task_flops", _f64p), ("task_fp1", _i64p),
+        ("dep_off", _i32p), ("dep_owner", _i32p), ("dep_size", _i64p),
+        ("atom_task_off", _i32p), ("atom_tasks", _i32p),
+        ("atom_in_off", _i32p), ("atom_in", _i32p),
+        ("in_owner", _i32p), ("in_size", _i64p), ("in_atoms_off", _i32p), ("in_atoms", _i32p),
+        ("succ_off", _i32p), ("succ", _i32p), ("pred_off", _i32p), ("pred", _i32p),
+        ("nbr_off", _i32p), ("nbr", _i32p),
+        ("tr_owner", _i32p), ("tr_size", _i64p), ("tr_cons_off", _i32p), ("tr_cons", _i32p),
+        ("atom_tr_off", _i32p), ("atom_tr", _i32p),
+        ("budget", C.c_int64),
+        ("flops_per_sec", C.c_double), ("bwd_fwd_ratio", C.c_double),
+        ("grad_factor", C.c_double), ("opt_factor", C.c_double),
+    ]
+
+
+def atoms_struct(fa) -> PcAtoms:
+    s = PcAtoms()
+    s.n = fa.n
+    s.n_tasks = int(fa.task_atom.shape[0])
+    s.n_in = int(fa.in_owner.shape[0])
+    s.n_traffic = int(fa.tr_owner.shape[0])
+    ctypes_of = {np.dtype(np.int32): C.c_int32, np.dtype(np.int64): C.c_int64,
+                 np.dtype(np.float64): C.c_double}
+    for name, _ in PcAtoms._fields_:
+        v = getattr(fa, name, None)
+        if isinstance(v, np.ndarray):
+            setattr(s, name, _ptr(v, ctypes_of[v.dtype]))
+    s.budget = fa.budget
+    s.flops_per_sec = fa.flops_per_sec
+    s.bwd_fwd_ratio = fa.bwd_fwd_ratio
+    s.grad_factor = fa.factor_g
+    s.opt_factor = fa.factor_o
+    return s
+
+
 class PcCall(C.Structure):
     _fields_ = [("S", C.c_int32), ("D", C.c_int32), ("R", C.c_int32), ("MB", C.c_int32)]
 

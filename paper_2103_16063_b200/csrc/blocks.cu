@@ -1,0 +1,786 @@
+// K6: block coarsening -- partition_blocks (pkg/src/pipecut/blocks.py:361-397).
+//
+// The reference is a sequential greedy multilevel algorithm whose decisions
+// must be reproduced exactly (SURVEY.md finding 7).  Its cost is in the
+// predicates it evaluates: the memory of merged atom sets (a full
+// CostModel.profile each, blocks.py:107-116), convexity (blocks.py:45-70),
+// group compute times (blocks.py:104-105) and cut traffic (blocks.py:118-124).
+// Every candidate of a pass -- all adjacent group pairs of a coarsening level,
+// all (pair, mover, target) moves of an uncoarsening round across all coarser
+// levels -- is independent of the greedy state it is tested in, so the device
+// evaluates the whole pass in one batch; the host then replays the greedy
+// order over the device's answers.  Uncoarsening changes state after an
+// accepted move, so it runs in speculative rounds: evaluate every remaining
+// pair against the current state, accept the first pair with a move, re-run
+// from the next pair (accepted moves are rare: 62 on BERT, 0 on ResNet).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <queue>
+#include <set>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace pcb {
+
+struct DevAtoms {
+    int n, T, V, E;
+    int64_t budget;
+    double factor, flops, beta;
+    const int64_t *atom_param;
+    const int32_t *task_atom;
+    const double *task_flops;
+    const int64_t *task_fp1;
+    const int32_t *dep_off, *dep_owner;
+    const int64_t *dep_size;
+    const int32_t *atom_task_off, *atom_tasks;
+    const int32_t *atom_in_off, *atom_in;
+    const int32_t *in_owner;
+    const int64_t *in_size;
+    const int32_t *in_atoms_off, *in_atoms;
+    const int32_t *pred_off, *pred;
+    const int32_t *tr_owner;
+    const int64_t *tr_size;
+    const int32_t *tr_cons_off, *tr_cons;
+    const int32_t *atom_tr_off, *atom_tr;
+};
+
+// Group memberships of the coarsening levels: grp[l*n + x] = group of atom x
+// at level l; CSR goff[l*(n+1) + g] / gat[l*n + j] lists each group's atoms
+// ascending (groups ordered by first atom, as the reference keeps them).
+struct DevLevels {
+    const int32_t *grp, *goff, *gat;
+    int n;
+};
+
+// mode 0: group (la, ga) union group (lb, gb) (gb < 0: just (la, ga));
+// mode 1: group (la, ga) minus group (lb, gb)
+struct SetDesc {
+    int32_t la, ga, lb, gb, mode;
+};
+
+struct MoveDesc {
+    int32_t li, mover, dest, top;
+};
+
+__device__ __forceinline__ bool in_set(const DevLevels &L, const SetDesc &s, int x) {
+    const bool a = L.grp[(int64_t)s.la * L.n + x] == s.ga;
+    if (s.mode == 0) return a || (s.gb >= 0 && L.grp[(int64_t)s.lb * L.n + x] == s.gb);
+    return a && L.grp[(int64_t)s.lb * L.n + x] != s.gb;
+}
+
+template <class F>
+__device__ __forceinline__ void for_each_member(const DevLevels &L, const SetDesc &s, F f) {
+    const int32_t *off = L.goff + (int64_t)s.la * (L.n + 1);
+    const int32_t *at = L.gat + (int64_t)s.la * L.n;
+    for (int j = off[s.ga]; j < off[s.ga + 1]; ++j) {
+        const int x = at[j];
+        if (s.mode == 1 && L.grp[(int64_t)s.lb * L.n + x] == s.gb) continue;
+        f(x);
+    }
+    if (s.mode == 0 && s.gb >= 0) {
+        const int32_t *offb = L.goff + (int64_t)s.lb * (L.n + 1);
+        const int32_t *atb = L.gat + (int64_t)s.lb * L.n;
+        for (int j = offb[s.gb]; j < offb[s.gb + 1]; ++j) {
+            const int x = atb[j];
+            if (L.grp[(int64_t)s.la * L.n + x] == s.ga) continue;
+            f(x);
+        }
+    }
+}
+
+// CostModel.profile(merged(G), 1, checkpointing=True).mem_bytes (costs.py:97-160)
+__device__ int64_t set_mem(const DevAtoms &A, const DevLevels &L, const SetDesc &s) {
+    int64_t param = 0, inb = 0, mfp = 0;
+    for_each_member(L, s, [&](int x) {
+        param += A.atom_param[x];
+        for (int q = A.atom_in_off[x]; q < A.atom_in_off[x + 1]; ++q) {
+            const int iv = A.atom_in[q];
+            const int own = A.in_owner[iv];
+            if (own >= 0 && in_set(L, s, own)) continue;          // owned inside: not an input
+            for (int r = A.in_atoms_off[iv]; r < A.in_atoms_off[iv + 1]; ++r) {
+                const int y = A.in_atoms[r];
+                if (in_set(L, s, y)) {                              // count at the first lister
+                    if (y == x) inb += A.in_size[iv];
+                    break;
+                }
+            }
+        }
+        for (int q = A.atom_task_off[x]; q < A.atom_task_off[x + 1]; ++q) {
+            const int t = A.atom_tasks[q];
+            int64_t fp = A.task_fp1[t];
+            for (int d = A.dep_off[t]; d < A.dep_off[t + 1]; ++d)
+                if (in_set(L, s, A.dep_owner[d])) fp += A.dep_size[d];
+            mfp = fp > mfp ? fp : mfp;
+        }
+    });
+    const double memd = __dadd_rn(__dmul_rn((double)param, A.factor), (double)(inb + mfp));
+    return (int64_t)memd;
+}
+
+// is_convex (blocks.py:45-70) as one sweep in index order: atom indices are
+// a topological order, so "reached" (the reference's DFS set) is
+// x in (lo, hi), not a member, with a member or reached predecessor; the set
+// is non-convex iff a member has a reached predecessor.
+__device__ bool set_convex(const DevAtoms &A, const DevLevels &L, const SetDesc &s, int lo, int hi,
+                           int count, uint32_t *bits) {
+    if (hi - lo + 1 == count) return true;
+    const int span = hi - lo + 1;
+    for (int w = 0; w < (span + 31) / 32; ++w) bits[w] = 0u;
+    for (int x = lo + 1; x <= hi; ++x) {
+        if (in_set(L, s, x)) {
+            for (int q = A.pred_off[x]; q < A.pred_off[x + 1]; ++q) {
+                const int p = A.pred[q];
+                if (p > lo && p < hi && ((bits[(p - lo) >> 5] >> ((p - lo) & 31)) & 1u)) return false;
+            }
+        } else if (x < hi) {
+            for (int q = A.pred_off[x]; q < A.pred_off[x + 1]; ++q) {
+                const int p = A.pred[q];
+                if (p < lo) continue;
+                const bool pm = in_set(L, s, p);
+                const bool pr = p > lo && ((bits[(p - lo) >> 5] >> ((p - lo) & 31)) & 1u);
+                if (pm || pr) {
+                    bits[(x - lo) >> 5] |= 1u << ((x - lo) & 31);
+                    break;
+                }
+            }
+        }
+    }
+    return true;
+}
+
+__global__ void k_eval_sets(DevAtoms A, DevLevels L, const SetDesc *sets, int nsets, uint32_t *scratch,
+                            int words, int64_t *out_mem, int32_t *out_count, uint8_t *out_convex) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nsets) return;
+    const SetDesc s = sets[i];
+    int lo = 0x7fffffff, hi = -1, count = 0;
+    for_each_member(L, s, [&](int x) {
+        lo = x < lo ? x : lo;
+        hi = x > hi ? x : hi;
+        ++count;
+    });
+    out_count[i] = count;
+    if (count == 0) {
+        out_mem[i] = 0;
+        out_convex[i] = 1;
+        return;
+    }
+    out_mem[i] = set_mem(A, L, s);
+    out_convex[i] = set_convex(A, L, s, lo, hi, count, scratch + (int64_t)i * words) ? 1 : 0;
+}
+
+// sum(atom_comp[i] for i in group) with CPython 3.12's float sum: the first
+// term enters as 0 + x0, the rest by Neumaier compensation (bltinmodule.c).
+__global__ void k_group_comps(DevLevels L, int level, int ngroups, const double *atom_comp,
+                              double *out) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
+    const int32_t *off = L.goff + (int64_t)level * (L.n + 1);
+    const int32_t *at = L.gat + (int64_t)level * L.n;
+    double f = __dadd_rn(0.0, atom_comp[at[off[g]]]);
+    double c = 0.0;
+    for (int j = off[g] + 1; j < off[g + 1]; ++j) {
+        const double x = atom_comp[at[j]];
+        const double t = __dadd_rn(f, x);
+        if (fabs(f) >= fabs(x))
+            c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+        else
+            c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+        f = t;
+    }
+    if (c != 0.0 && isfinite(c)) f = __dadd_rn(f, c);
+    out[g] = f;
+}
+
+// CostModel.profile(group, 1, checkpointing=True) for every group of a level:
+// time folds over the group's tasks in global sorted node-id order.
+__global__ void k_group_profiles(DevAtoms A, DevLevels L, int level, int ngroups, int single_atoms,
+                                 double *out_tf, double *out_tb, double *out_comp, int64_t *out_mem) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ngroups) return;
+    double tf = 0.0, tb = 0.0;
+    if (single_atoms) {
+        const int x = L.gat[(int64_t)level * L.n + L.goff[(int64_t)level * (L.n + 1) + g]];
+        for (int q = A.atom_task_off[x]; q < A.atom_task_off[x + 1]; ++q) {
+            const int t = A.atom_tasks[q];
+            const double v = __ddiv_rn(__dmul_rn(A.task_flops[t], 1.0), A.flops);
+            tf = __dadd_rn(tf, v);
+            tb = __dadd_rn(tb, __dmul_rn(A.beta, v));
+        }
+    } else {
+        const int32_t *grp = L.grp + (int64_t)level * L.n;
+        for (int t = 0; t < A.T; ++t) {
+            if (grp[A.task_atom[t]] != g) continue;
+            const double v = __ddiv_rn(__dmul_rn(A.task_flops[t], 1.0), A.flops);
+            tf = __dadd_rn(tf, v);
+            tb = __dadd_rn(tb, __dmul_rn(A.beta, v));
+        }
+    }
+    out_tf[g] = tf;
+    out_tb[g] = tb;
+    out_comp[g] = __dadd_rn(tf, tb);                      // blocks.py:93
+    const SetDesc s{level, g, level, -1, 0};
+    out_mem[g] = set_mem(A, L, s);
+}
+
+// Traffic saving of moving level-li group `mover` into top-level block `dest`
+// (blocks.py:193-201): base_traffic - traffic(moved), summed exactly over the
+// value entries the mover touches (each entry once, at its smallest mover atom).
+__global__ void k_move_savings(DevAtoms A, DevLevels L, const MoveDesc *mv, int nm, int64_t *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nm) return;
+    const MoveDesc m = mv[i];
+    const int32_t *gl = L.grp + (int64_t)m.li * L.n;
+    const int32_t *gt = L.grp + (int64_t)m.top * L.n;
+    const int32_t *off = L.goff + (int64_t)m.li * (L.n + 1);
+    const int32_t *at = L.gat + (int64_t)m.li * L.n;
+    int64_t saving = 0;
+    for (int j = off[m.mover]; j < off[m.mover + 1]; ++j) {
+        const int x = at[j];
+        for (int q = A.atom_tr_off[x]; q < A.atom_tr_off[x + 1]; ++q) {
+            const int e = A.atom_tr[q];
+            const int owner = A.tr_owner[e];
+            int first = gl[owner] == m.mover ? owner : 0x7fffffff;
+            for (int r = A.tr_cons_off[e]; r < A.tr_cons_off[e + 1]; ++r) {
+                const int c = A.tr_cons[r];
+                if (gl[c] == m.mover && c < first) first = c;
+            }
+            if (first != x) continue;
+            const int home0 = gt[owner];
+            const int home1 = gl[owner] == m.mover ? m.dest : home0;
+            int before = 0, after = 0;
+            const int c0 = A.tr_cons_off[e], c1 = A.tr_cons_off[e + 1];
+            for (int r = c0; r < c1; ++r) {
+                const int c = A.tr_cons[r];
+                const int b0 = gt[c];
+                const int b1 = gl[c] == m.mover ? m.dest : b0;
+                bool seen0 = b0 == home0, seen1 = b1 == home1;
+                for (int u = c0; u < r && !(seen0 && seen1); ++u) {
+                    const int cu = A.tr_cons[u];
+                    if (gt[cu] == b0) seen0 = true;
+                    if ((gl[cu] == m.mover ? m.dest : gt[cu]) == b1) seen1 = true;
+                }
+                before += !seen0;
+                after += !seen1;
+            }
+            saving += A.tr_size[e] * (int64_t)(before - after);
+        }
+    }
+    out[i] = saving;
+}
+
+// ====================================================================== host side
+namespace {
+
+struct Coarsener {
+    pc_ctx *ctx;
+    const pc_atoms *H;
+    DevAtoms A{};
+    int n;
+    DBuf atoms_d, lev_grp, lev_off, lev_at, sets_d, scratch_d, out_d, comp_d, mv_d;
+    int lev_cap = 0;
+    std::vector<std::vector<std::vector<int>>> levels;
+    std::vector<double> atom_comp;
+
+    int upload_atoms() {
+        struct Part { const void *src; size_t bytes; size_t off; };
+        std::vector<Part> parts;
+        size_t total = 0;
+        auto add = [&](const void *src, size_t bytes) {
+            size_t off = (total + 15) & ~size_t(15);
+            parts.push_back({src, bytes, off});
+            total = off + bytes;
+            return parts.size() - 1;
+        };
+        const size_t T = H->n_tasks, V = H->n_in, E = H->n_traffic, N = H->n;
+        const size_t nd = H->dep_off[T], nin = H->atom_in_off[N], nia = H->in_atoms_off[V];
+        const size_t np = H->pred_off[N], nc = H->tr_cons_off[E], ntr = H->atom_tr_off[N];
+        size_t i0 = add(H->atom_param, 8 * N), i1 = add(H->task_atom, 4 * T), i2 = add(H->task_flops, 8 * T);
+        size_t i3 = add(H->task_fp1, 8 * T), i4 = add(H->dep_off, 4 * (T + 1)), i5 = add(H->dep_owner, 4 * nd);
+        size_t i6 = add(H->dep_size, 8 * nd), i7 = add(H->atom_task_off, 4 * (N + 1)), i8 = add(H->atom_tasks, 4 * T);
+        size_t i9 = add(H->atom_in_off, 4 * (N + 1)), i10 = add(H->atom_in, 4 * nin), i11 = add(H->in_owner, 4 * V);
+        size_t i12 = add(H->in_size, 8 * V), i13 = add(H->in_atoms_off, 4 * (V + 1)), i14 = add(H->in_atoms, 4 * nia);
+        size_t i15 = add(H->pred_off, 4 * (N + 1)), i16 = add(H->pred, 4 * np), i17 = add(H->tr_owner, 4 * E);
+        size_t i18 = add(H->tr_size, 8 * E), i19 = add(H->tr_cons_off, 4 * (E + 1)), i20 = add(H->tr_cons, 4 * nc);
+        size_t i21 = add(H->atom_tr_off, 4 * (N + 1)), i22 = add(H->atom_tr, 4 * ntr);
+        CUDA_TRY(ctx, atoms_d.ensure(total + 64));
+        std::vector<char> staging(total + 64, 0);
+        for (auto &p : parts)
+            if (p.bytes) memcpy(staging.data() + p.off, p.src, p.bytes);
+        CUDA_TRY(ctx, cudaMemcpy(atoms_d.p, staging.data(), total, cudaMemcpyHostToDevice));
+        char *b = atoms_d.as<char>();
+        auto at = [&](size_t i) { return (void *)(b + parts[i].off); };
+        A.n = (int)N;
+        A.T = (int)T;
+        A.V = (int)V;
+        A.E = (int)E;
+        A.budget = H->budget;
+        A.factor = (1.0 + H->grad_factor) + H->opt_factor;
+        A.flops = H->flops_per_sec;
+        A.beta = H->bwd_fwd_ratio;
+        A.atom_param = (const int64_t *)at(i0);
+        A.task_atom = (const int32_t *)at(i1);
+        A.task_flops = (const double *)at(i2);
+        A.task_fp1 = (const int64_t *)at(i3);
+        A.dep_off = (const int32_t *)at(i4);
+        A.dep_owner = (const int32_t *)at(i5);
+        A.dep_size = (const int64_t *)at(i6);
+        A.atom_task_off = (const int32_t *)at(i7);
+        A.atom_tasks = (const int32_t *)at(i8);
+        A.atom_in_off = (const int32_t *)at(i9);
+        A.atom_in = (const int32_t *)at(i10);
+        A.in_owner = (const int32_t *)at(i11);
+        A.in_size = (const int64_t *)at(i12);
+        A.in_atoms_off = (const int32_t *)at(i13);
+        A.in_atoms = (const int32_t *)at(i14);
+        A.pred_off = (const int32_t *)at(i15);
+        A.pred = (const int32_t *)at(i16);
+        A.tr_owner = (const int32_t *)at(i17);
+        A.tr_size = (const int64_t *)at(i18);
+        A.tr_cons_off = (const int32_t *)at(i19);
+        A.tr_cons = (const int32_t *)at(i20);
+        A.atom_tr_off = (const int32_t *)at(i21);
+        A.atom_tr = (const int32_t *)at(i22);
+        return PC_OK;
+    }
+
+    DevLevels dev_levels() const {
+        return DevLevels{lev_grp.as<int32_t>(), lev_off.as<int32_t>(), lev_at.as<int32_t>(), n};
+    }
+
+    // copy level `l` (list of ascending atom groups) into device slot l
+    int upload_level(int l, const std::vector<std::vector<int>> &groups) {
+        if (l >= lev_cap) {
+            int cap = std::max(16, 2 * (l + 1));
+            DBuf g2, o2, a2;
+            CUDA_TRY(ctx, g2.ensure(sizeof(int32_t) * (size_t)cap * n));
+            CUDA_TRY(ctx, o2.ensure(sizeof(int32_t) * (size_t)cap * (n + 1)));
+            CUDA_TRY(ctx, a2.ensure(sizeof(int32_t) * (size_t)cap * n));
+            if (lev_cap) {
+                CUDA_TRY(ctx, cudaMemcpy(g2.p, lev_grp.p, sizeof(int32_t) * (size_t)lev_cap * n, cudaMemcpyDeviceToDevice));
+                CUDA_TRY(ctx, cudaMemcpy(o2.p, lev_off.p, sizeof(int32_t) * (size_t)lev_cap * (n + 1), cudaMemcpyDeviceToDevice));
+                CUDA_TRY(ctx, cudaMemcpy(a2.p, lev_at.p, sizeof(int32_t) * (size_t)lev_cap * n, cudaMemcpyDeviceToDevice));
+            }
+            std::swap(lev_grp.p, g2.p); std::swap(lev_grp.n, g2.n);
+            std::swap(lev_off.p, o2.p); std::swap(lev_off.n, o2.n);
+            std::swap(lev_at.p, a2.p); std::swap(lev_at.n, a2.n);
+            lev_cap = cap;
+        }
+        std::vector<int32_t> grp(n, -1), off(n + 1, 0), at;
+        at.reserve(n);
+        for (size_t g = 0; g < groups.size(); ++g) {
+            for (int x : groups[g]) {
+                grp[x] = (int32_t)g;
+                at.push_back(x);
+            }
+            off[g + 1] = (int32_t)at.size();
+        }
+        for (size_t g = groups.size(); g < (size_t)n; ++g) off[g + 1] = off[groups.size()];
+        at.resize(n, 0);
+        CUDA_TRY(ctx, cudaMemcpy(lev_grp.as<int32_t>() + (size_t)l * n, grp.data(), 4 * (size_t)n, cudaMemcpyHostToDevice));
+        CUDA_TRY(ctx, cudaMemcpy(lev_off.as<int32_t>() + (size_t)l * (n + 1), off.data(), 4 * (size_t)(n + 1), cudaMemcpyHostToDevice));
+        CUDA_TRY(ctx, cudaMemcpy(lev_at.as<int32_t>() + (size_t)l * n, at.data(), 4 * (size_t)n, cudaMemcpyHostToDevice));
+        return PC_OK;
+    }
+
+    int comps(int l, int ngroups, std::vector<double> &out) {
+        CUDA_TRY(ctx, out_d.ensure(sizeof(double) * ngroups + 64));
+        k_group_comps<<<(ngroups + 127) / 128, 128, 0, ctx->st>>>(dev_levels(), l, ngroups, comp_d.as<double>(),
+                                                                 out_d.as<double>());
+        ctx->launches++;
+        if (int rc = check_launch(ctx, "group_comps")) return rc;
+        out.resize(ngroups);
+        CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), out_d.p, sizeof(double) * ngroups, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        return PC_OK;
+    }
+
+    int eval(const std::vector<SetDesc> &sets, std::vector<int64_t> &mem, std::vector<int32_t> &count,
+             std::vector<uint8_t> &convex) {
+        const int ns = (int)sets.size();
+        mem.assign(ns, 0);
+        count.assign(ns, 0);
+        convex.assign(ns, 0);
+        if (!ns) return PC_OK;
+        const int words = (n + 31) / 32 + 1;
+        CUDA_TRY(ctx, sets_d.ensure(sizeof(SetDesc) * ns));
+        CUDA_TRY(ctx, scratch_d.ensure(sizeof(uint32_t) * (size_t)ns * words));
+        CUDA_TRY(ctx, out_d.ensure((8 + 4 + 1) * (size_t)ns + 64));
+        CUDA_TRY(ctx, cudaMemcpyAsync(sets_d.p, sets.data(), sizeof(SetDesc) * ns, cudaMemcpyHostToDevice, ctx->st));
+        int64_t *om = out_d.as<int64_t>();
+        int32_t *oc = (int32_t *)(om + ns);
+        uint8_t *ov = (uint8_t *)(oc + ns);
+        k_eval_sets<<<(ns + 127) / 128, 128, 0, ctx->st>>>(A, dev_levels(), sets_d.as<SetDesc>(), ns,
+                                                           scratch_d.as<uint32_t>(), words, om, oc, ov);
+        ctx->launches++;
+        if (int rc = check_launch(ctx, "eval_sets")) return rc;
+        CUDA_TRY(ctx, cudaMemcpyAsync(mem.data(), om, 8 * (size_t)ns, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(count.data(), oc, 4 * (size_t)ns, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(convex.data(), ov, (size_t)ns, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        return PC_OK;
+    }
+
+    int savings(const std::vector<MoveDesc> &mv, std::vector<int64_t> &out) {
+        const int nm = (int)mv.size();
+        out.assign(nm, 0);
+        if (!nm) return PC_OK;
+        CUDA_TRY(ctx, mv_d.ensure(sizeof(MoveDesc) * nm + 8 * (size_t)nm + 64));
+        MoveDesc *dm = mv_d.as<MoveDesc>();
+        int64_t *ds = (int64_t *)(((uintptr_t)(dm + nm) + 15) & ~uintptr_t(15));
+        CUDA_TRY(ctx, cudaMemcpyAsync(dm, mv.data(), sizeof(MoveDesc) * nm, cudaMemcpyHostToDevice, ctx->st));
+        k_move_savings<<<(nm + 127) / 128, 128, 0, ctx->st>>>(A, dev_levels(), dm, nm, ds);
+        ctx->launches++;
+        if (int rc = check_launch(ctx, "move_savings")) return rc;
+        CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), ds, 8 * (size_t)nm, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        return PC_OK;
+    }
+
+    int profiles(int l, int ngroups, bool single, std::vector<double> &tf, std::vector<double> &tb,
+                 std::vector<double> &comp, std::vector<int64_t> &mem) {
+        CUDA_TRY(ctx, out_d.ensure(32 * (size_t)ngroups + 64));
+        double *a = out_d.as<double>();
+        k_group_profiles<<<(ngroups + 127) / 128, 128, 0, ctx->st>>>(A, dev_levels(), l, ngroups, single ? 1 : 0,
+                                                                    a, a + ngroups, a + 2 * ngroups,
+                                                                    (int64_t *)(a + 3 * ngroups));
+        ctx->launches++;
+        if (int rc = check_launch(ctx, "group_profiles")) return rc;
+        tf.resize(ngroups);
+        tb.resize(ngroups);
+        comp.resize(ngroups);
+        mem.resize(ngroups);
+        CUDA_TRY(ctx, cudaMemcpyAsync(tf.data(), a, 8 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(tb.data(), a + ngroups, 8 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(comp.data(), a + 2 * ngroups, 8 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(mem.data(), a + 3 * ngroups, 8 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        return PC_OK;
+    }
+};
+
+std::vector<int> member_map(int n, const std::vector<std::vector<int>> &level) {
+    std::vector<int> m(n, -1);
+    for (size_t g = 0; g < level.size(); ++g)
+        for (int x : level[g]) m[x] = (int)g;
+    return m;
+}
+
+void sort_by_first(std::vector<std::vector<int>> &level) {
+    std::sort(level.begin(), level.end(),
+              [](const std::vector<int> &a, const std::vector<int> &b) { return a[0] < b[0]; });
+}
+
+}  // namespace
+}  // namespace pcb
+
+using namespace pcb;
+
+extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, int32_t *n_blocks,
+                                   int32_t *block_off, int32_t *block_atoms, double *out_tf,
+                                   double *out_tb, int64_t *out_mem, int64_t *err) {
+    if (k < 1) return fail(ctx, PC_ERR_INVALID, "k must be at least 1");
+    if (H->n < 1) return fail(ctx, PC_ERR_INVALID, "no atoms");
+    cudaSetDevice(ctx->device);
+    Coarsener co;
+    co.ctx = ctx;
+    co.H = H;
+    co.n = H->n;
+    const int n = H->n;
+    const int64_t budget = H->budget;
+    if (int rc = co.upload_atoms()) return rc;
+
+    // ---- level 0 and the atoms' own profiles (blocks.py:89-94, 366-369)
+    std::vector<std::vector<int>> l0(n);
+    for (int i = 0; i < n; ++i) l0[i] = {i};
+    co.levels.push_back(l0);
+    if (int rc = co.upload_level(0, l0)) return rc;
+    std::vector<double> tf, tb, comp;
+    std::vector<int64_t> mem;
+    if (int rc = co.profiles(0, n, true, tf, tb, comp, mem)) return rc;
+    co.atom_comp = comp;
+    CUDA_TRY(ctx, co.comp_d.ensure(sizeof(double) * n));
+    CUDA_TRY(ctx, cudaMemcpy(co.comp_d.p, comp.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    for (int i = 0; i < n; ++i) {
+        if (mem[i] >= budget) {                                 // InfeasibleAtom
+            err[0] = i;
+            err[1] = mem[i];
+            return fail(ctx, PC_ERR_ATOM, "atom exceeds device memory");
+        }
+    }
+    const int32_t *nbr_off = H->nbr_off, *nbr = H->nbr;
+
+    // ---- coarsening passes (blocks.py:127-166, 371-378)
+    std::vector<std::vector<std::pair<std::vector<int>, std::vector<int>>>> transitions;
+    while ((int)co.levels.back().size() > k) {
+        const int L = (int)co.levels.size() - 1;
+        const std::vector<std::vector<int>> &G = co.levels[L];
+        const int m = (int)G.size();
+        std::vector<double> gc;
+        if (int rc = co.comps(L, m, gc)) return rc;
+        const std::vector<int> gmap = member_map(n, G);
+        auto key_less = [&](int a, int b) {
+            if (gc[a] != gc[b]) return gc[a] < gc[b];
+            return G[a][0] < G[b][0];
+        };
+        std::vector<int> order(m);
+        for (int i = 0; i < m; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), key_less);
+        // every adjacent pair, evaluated once on the device
+        std::vector<std::vector<int>> adj(m);
+        for (int gi = 0; gi < m; ++gi) {
+            std::vector<int> &c = adj[gi];
+            for (int a : G[gi])
+                for (int q = nbr_off[a]; q < nbr_off[a + 1]; ++q) {
+                    const int gj = gmap[nbr[q]];
+                    if (gj != gi) c.push_back(gj);
+                }
+            std::sort(c.begin(), c.end());
+            c.erase(std::unique(c.begin(), c.end()), c.end());
+        }
+        std::vector<SetDesc> sets;
+        std::map<std::pair<int, int>, int> pair_idx;
+        for (int gi = 0; gi < m; ++gi)
+            for (int gj : adj[gi])
+                if (gi < gj) {
+                    pair_idx[{gi, gj}] = (int)sets.size();
+                    sets.push_back(SetDesc{L, gi, L, gj, 0});
+                }
+        std::vector<int64_t> smem;
+        std::vector<int32_t> scount;
+        std::vector<uint8_t> sconv;
+        if (int rc = co.eval(sets, smem, scount, sconv)) return rc;
+        // the greedy pass over the device's answers
+        std::vector<char> used(m, 0);
+        std::vector<int> partner(m, -1);
+        int count = m;
+        for (int gi : order) {
+            if (count <= k) break;
+            if (used[gi]) continue;
+            std::vector<int> cands;
+            for (int gj : adj[gi])
+                if (!used[gj]) cands.push_back(gj);
+            std::sort(cands.begin(), cands.end(), key_less);
+            for (int gj : cands) {
+                const int si = pair_idx[{std::min(gi, gj), std::max(gi, gj)}];
+                if (sconv[si] && smem[si] < budget) {           // is_convex and fits (blocks.py:115-116)
+                    partner[gi] = gj;
+                    used[gi] = used[gj] = 1;
+                    --count;
+                    break;
+                }
+            }
+        }
+        std::vector<char> absorbed(m, 0);
+        for (int gi = 0; gi < m; ++gi)
+            if (partner[gi] >= 0) absorbed[partner[gi]] = 1;
+        std::vector<std::vector<int>> next;
+        std::vector<std::pair<std::vector<int>, std::vector<int>>> merges;
+        for (int gi = 0; gi < m; ++gi) {
+            if (absorbed[gi]) continue;
+            if (partner[gi] < 0) {
+                next.push_back(G[gi]);
+            } else {
+                std::vector<int> u = G[gi];
+                u.insert(u.end(), G[partner[gi]].begin(), G[partner[gi]].end());
+                std::sort(u.begin(), u.end());
+                next.push_back(u);
+                merges.push_back({G[gi], G[partner[gi]]});
+            }
+        }
+        if (merges.empty()) break;
+        sort_by_first(next);
+        co.levels.push_back(next);
+        transitions.push_back(merges);
+        if (int rc = co.upload_level(L + 1, co.levels.back())) return rc;
+    }
+
+    // ---- refinement: speculative rounds over the recorded merges (blocks.py:173-232)
+    const int top = (int)co.levels.size() - 1;
+    for (int li = (int)transitions.size() - 1; li >= 0; --li) {
+        const auto &pairs = transitions[li];
+        size_t p = 0;
+        while (p < pairs.size()) {
+            for (int l = li; l <= top; ++l)
+                if (int rc = co.upload_level(l, co.levels[l])) return rc;
+            std::vector<std::vector<int>> maps(top + 1);
+            for (int l = li; l <= top; ++l) maps[l] = member_map(n, co.levels[l]);
+            struct Tri { int q, mi, ti, mv; int64_t set0; };
+            std::vector<Tri> tris;
+            std::vector<SetDesc> sets;
+            std::vector<MoveDesc> moves;
+            for (size_t q = p; q < pairs.size(); ++q) {
+                for (int mi = 0; mi < 2; ++mi) {
+                    const std::vector<int> &mover = mi == 0 ? pairs[q].first : pairs[q].second;
+                    const int here = maps[top][mover[0]];
+                    const int mv = maps[li][mover[0]];
+                    std::vector<int> targets;
+                    for (int a : mover)
+                        for (int r = nbr_off[a]; r < nbr_off[a + 1]; ++r) targets.push_back(maps[li][nbr[r]]);
+                    std::sort(targets.begin(), targets.end());
+                    targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
+                    for (int ti : targets) {
+                        const std::vector<int> &target = co.levels[li][ti];
+                        if (maps[top][target[0]] == here || ti == mv) continue;
+                        tris.push_back(Tri{(int)q, mi, ti, mv, (int64_t)sets.size()});
+                        for (int ell = li + 1; ell <= top; ++ell) {
+                            const int src = maps[ell][mover[0]], dst = maps[ell][target[0]];
+                            sets.push_back(SetDesc{ell, src, li, mv, 1});   // shrunk
+                            sets.push_back(SetDesc{ell, dst, li, mv, 0});   // grown
+                        }
+                        moves.push_back(MoveDesc{li, mv, maps[top][target[0]], top});
+                    }
+                }
+            }
+            std::vector<int64_t> smem, sav;
+            std::vector<int32_t> scount;
+            std::vector<uint8_t> sconv;
+            if (int rc = co.eval(sets, smem, scount, sconv)) return rc;
+            if (int rc = co.savings(moves, sav)) return rc;
+            const int nlev = top - li;
+            bool applied = false;
+            size_t ti_ptr = 0;
+            for (size_t q = p; q < pairs.size() && !applied; ++q) {
+                int64_t best_saving = 0;
+                int best = -1;
+                for (; ti_ptr < tris.size() && tris[ti_ptr].q == (int)q; ++ti_ptr) {
+                    const Tri &t = tris[ti_ptr];
+                    bool fits = true;                           // _move_fits (blocks.py:206-221)
+                    for (int e = 0; e < nlev && fits; ++e) {
+                        const int64_t sh = t.set0 + 2 * e, gr = sh + 1;
+                        if (scount[sh] == 0) fits = false;
+                        else if (!(sconv[gr] && sconv[sh])) fits = false;
+                        else if (!(smem[gr] < budget && smem[sh] < budget)) fits = false;
+                    }
+                    if (!fits) continue;
+                    const int64_t s = sav[ti_ptr];
+                    if (s > 0 && (best < 0 || s > best_saving)) {
+                        best_saving = s;
+                        best = (int)ti_ptr;
+                    }
+                }
+                if (best >= 0) {
+                    // _apply_move (blocks.py:224-232)
+                    const Tri &t = tris[best];
+                    const std::vector<int> mover = t.mi == 0 ? pairs[q].first : pairs[q].second;
+                    const std::vector<int> target = co.levels[li][t.ti];
+                    std::vector<char> in_mover(n, 0);
+                    for (int a : mover) in_mover[a] = 1;
+                    for (int ell = li + 1; ell <= top; ++ell) {
+                        auto &lev = co.levels[ell];
+                        const std::vector<int> mm = member_map(n, lev);
+                        const int si = mm[mover[0]], di = mm[target[0]];
+                        std::vector<int> shr;
+                        for (int a : lev[si])
+                            if (!in_mover[a]) shr.push_back(a);
+                        lev[si] = shr;
+                        std::vector<int> gr = lev[di];
+                        gr.insert(gr.end(), mover.begin(), mover.end());
+                        std::sort(gr.begin(), gr.end());
+                        lev[di] = gr;
+                        sort_by_first(lev);
+                    }
+                    applied = true;
+                    p = q + 1;
+                }
+            }
+            if (!applied) break;
+        }
+    }
+
+    // ---- dependency order (blocks.py:235-255) and compaction (267-292)
+    auto topo = [&](const std::vector<std::vector<int>> &groups) {
+        const int m = (int)groups.size();
+        const std::vector<int> gm = member_map(n, groups);
+        std::vector<std::set<int>> out(m);
+        std::vector<int> indeg(m, 0);
+        for (int a = 0; a < n; ++a)
+            for (int q = H->succ_off[a]; q < H->succ_off[a + 1]; ++q) {
+                const int ga = gm[a], gb = gm[H->succ[q]];
+                if (ga != gb && out[ga].insert(gb).second) indeg[gb]++;
+            }
+        std::priority_queue<std::pair<int, int>, std::vector<std::pair<int, int>>, std::greater<>> heap;
+        for (int g = 0; g < m; ++g)
+            if (indeg[g] == 0) heap.push({groups[g][0], g});
+        std::vector<std::vector<int>> order;
+        while (!heap.empty()) {
+            const int g = heap.top().second;
+            heap.pop();
+            order.push_back(groups[g]);
+            for (int nbg : out[g])
+                if (--indeg[nbg] == 0) heap.push({groups[nbg][0], nbg});
+        }
+        return order;
+    };
+    std::vector<std::vector<int>> glist = topo(co.levels[top]);
+    if ((int)glist.size() != (int)co.levels[top].size())
+        return fail(ctx, PC_ERR_INVALID, "group contraction must stay acyclic");
+    if ((int)glist.size() > k) {
+        const int scratch = (int)co.levels.size();
+        while ((int)glist.size() > k) {
+            if (int rc = co.upload_level(scratch, glist)) return rc;
+            const int m = (int)glist.size();
+            std::vector<double> gc;
+            if (int rc = co.comps(scratch, m, gc)) return rc;
+            // groups of glist are disjoint, so level `scratch` indexes them by position
+            std::vector<int> order(m);
+            for (int i = 0; i < m; ++i) order[i] = i;
+            auto key_less = [&](int a, int b) {
+                if (gc[a] != gc[b]) return gc[a] < gc[b];
+                return glist[a][0] < glist[b][0];
+            };
+            std::sort(order.begin(), order.end(), key_less);
+            std::vector<SetDesc> sets;
+            for (int pos = 0; pos + 1 < m; ++pos) sets.push_back(SetDesc{scratch, pos, scratch, pos + 1, 0});
+            std::vector<int64_t> smem;
+            std::vector<int32_t> scount;
+            std::vector<uint8_t> sconv;
+            if (int rc = co.eval(sets, smem, scount, sconv)) return rc;
+            int merged_at = -1;
+            for (int pos : order) {
+                std::vector<int> sides;
+                if (pos - 1 >= 0) sides.push_back(pos - 1);
+                if (pos + 1 < m) sides.push_back(pos + 1);
+                std::sort(sides.begin(), sides.end(), key_less);
+                for (int side : sides) {
+                    const int lo = std::min(pos, side);
+                    if (smem[lo] < budget) {                    // fits(union)
+                        std::vector<int> u = glist[lo];
+                        u.insert(u.end(), glist[lo + 1].begin(), glist[lo + 1].end());
+                        std::sort(u.begin(), u.end());
+                        glist[lo] = u;
+                        glist.erase(glist.begin() + lo + 1);
+                        merged_at = lo;
+                        break;
+                    }
+                }
+                if (merged_at >= 0) break;
+            }
+            if (merged_at < 0) {
+                err[0] = (int64_t)glist.size();
+                return fail(ctx, PC_ERR_STUCK, "compaction stuck");
+            }
+        }
+        glist = topo(glist);
+    }
+
+    // ---- outputs: blocks and their profiles (blocks.py:387-397)
+    const int nbk = (int)glist.size();
+    const int fin = (int)co.levels.size();
+    if (int rc = co.upload_level(fin, glist)) return rc;
+    if (int rc = co.profiles(fin, nbk, false, tf, tb, comp, mem)) return rc;
+    *n_blocks = nbk;
+    int pos = 0;
+    block_off[0] = 0;
+    for (int b = 0; b < nbk; ++b) {
+        for (int a : glist[b]) block_atoms[pos++] = a;
+        block_off[b + 1] = pos;
+        out_tf[b] = tf[b];
+        out_tb[b] = tb[b];
+        out_mem[b] = mem[b];
+    }
+    return PC_OK;
+}

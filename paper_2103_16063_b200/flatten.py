@@ -263,3 +263,175 @@ def flatten_blockset(bs) -> FlatProblem:
         latency=float(cl.link_latency_sec),
         monotone=monotone,
     )
+
+
+# --------------------------------------------------------------------------- atoms
+@dataclass
+class FlatAtoms:
+    """Atom-level arrays for partition_blocks (blocks.py:73-124): memory of an
+    arbitrary atom set G at microbatch 1 with checkpointing, convexity and
+    cut traffic.
+
+    mem(G) = int(param(G) * factor + (in(G) + maxfp(G)))  (costs.py:157-159)
+      in(G):    values listed in some member atom's input_values that are
+                model inputs / unowned or owned outside G (atoms.py:136-138),
+                each once;
+      maxfp(G): max over member tasks of produced + non-param preds that are
+                not inputs of G: an anchor's listed input counts iff its owner
+                atom is in G, any other pred always counts (costs.py:150-155).
+    """
+    n: int
+    atom_param: np.ndarray      # int64 [n]
+    task_atom: np.ndarray       # int32 [T] sorted node-id order
+    task_flops: np.ndarray      # float64 [T]
+    task_fp1: np.ndarray        # int64 [T] produced + always-counted preds, at m=1
+    dep_off: np.ndarray         # int32 [T+1]
+    dep_owner: np.ndarray       # int32 owner atom of an anchor input pred
+    dep_size: np.ndarray        # int64 size at m=1
+    atom_task_off: np.ndarray   # int32 [n+1]
+    atom_tasks: np.ndarray      # int32 task indices, ascending
+    atom_in_off: np.ndarray     # int32 [n+1]
+    atom_in: np.ndarray         # int32 input-value indices
+    in_owner: np.ndarray        # int32 [V] owner atom, -1 model input / unowned
+    in_size: np.ndarray         # int64 [V] size at m=1
+    in_atoms_off: np.ndarray    # int32 [V+1]
+    in_atoms: np.ndarray        # int32 atoms listing the value, ascending
+    succ_off: np.ndarray        # int32 [n+1] partition.dependencies() (atoms.py:115-125)
+    succ: np.ndarray
+    pred_off: np.ndarray
+    pred: np.ndarray
+    nbr_off: np.ndarray         # int32 [n+1] sorted(succ | pred) (blocks.py:87-88)
+    nbr: np.ndarray
+    tr_owner: np.ndarray        # int32 [E] value traffic entries (blocks.py:96-102)
+    tr_size: np.ndarray         # int64 [E]
+    tr_cons_off: np.ndarray     # int32 [E+1]
+    tr_cons: np.ndarray         # int32 foreign consumer atoms, ascending
+    atom_tr_off: np.ndarray     # int32 [n+1] entries touching each atom
+    atom_tr: np.ndarray
+    budget: int
+    flops_per_sec: float
+    bwd_fwd_ratio: float
+    factor_g: float
+    factor_o: float
+
+
+def _csr(lists):
+    off = np.zeros(len(lists) + 1, np.int64)
+    for i, l in enumerate(lists):
+        off[i + 1] = off[i] + len(l)
+    flat = [x for l in lists for x in l]
+    return _i32(off), _i32(flat)
+
+
+def flatten_atoms(partition, model) -> FlatAtoms:
+    cfg = model.config
+    if cfg.cost_table is not None:
+        raise UnsupportedGraph("measured cost tables are not supported by the "
+                               "device span-cost kernel yet (SURVEY.md §8f)")
+    g = model.graph
+    pg = partition.graph
+    n = len(partition.atoms)
+    atom_of = atom_node_tables(partition)
+    graph_inputs = g.inputs
+
+    def size1(info, what):
+        return _as_int(info.fixed_bytes, what) + _as_int(info.bytes_per_sample, what)
+
+    inputs_of_atom = [frozenset(a.input_values) for a in partition.atoms]
+    in_ids = sorted({v for ins in inputs_of_atom for v in ins})
+    in_index = {v: i for i, v in enumerate(in_ids)}
+    in_owner, in_size, in_atoms = [], [], []
+    listing = {v: [] for v in in_ids}
+    for a, ins in enumerate(inputs_of_atom):
+        for v in ins:
+            listing[v].append(a)
+    for v in in_ids:
+        node = g.nodes[v]
+        if not node.is_value:
+            raise UnsupportedGraph(f"atom input {v!r} is not a value")
+        own = atom_of.get(v)
+        in_owner.append(-1 if (v in graph_inputs or own is None) else own)
+        in_size.append(size1(node.value, v))
+        in_atoms.append(sorted(listing[v]))
+
+    atom_param = [0] * n
+    task_atom, task_flops, task_fp1, deps = [], [], [], []
+    atom_tasks = [[] for _ in range(n)]
+    for nid, node in g.nodes.items():           # sorted id order (graph.py:90-93)
+        a = atom_of.get(nid)
+        if a is None:
+            continue
+        if node.is_value:
+            if node.value.is_param:
+                atom_param[a] += _as_int(node.value.fixed_bytes, nid)
+            continue
+        fp = 0
+        for vid in g.succ(nid):
+            info = g.nodes[vid].value
+            if info is not None and not info.is_param:
+                fp += size1(info, vid)
+        dl = []
+        for vid in g.pred(nid):
+            info = g.nodes[vid].value
+            if info is None or info.is_param:
+                continue
+            if vid in inputs_of_atom[a]:
+                own = in_owner[in_index[vid]]
+                if own >= 0:
+                    dl.append((own, size1(info, vid)))
+                # model input / unowned: always an input of G, never counted
+            else:
+                if atom_of.get(vid) != a:
+                    raise UnsupportedGraph(f"task {nid!r} reads {vid!r} across atoms "
+                                           f"without listing it as an input")
+                fp += size1(info, vid)
+        atom_tasks[a].append(len(task_atom))
+        task_atom.append(a)
+        task_flops.append(float(node.task.flops_per_sample))
+        task_fp1.append(fp)
+        deps.append(dl)
+
+    succ = [[] for _ in range(n)]
+    pred = [[] for _ in range(n)]
+    for a, b in partition.dependencies():      # sorted unique pairs
+        succ[a].append(b)
+        pred[b].append(a)
+    nbr = [sorted(set(succ[i]) | set(pred[i])) for i in range(n)]
+
+    tr_owner, tr_size, tr_cons = [], [], []
+    atom_tr = [[] for _ in range(n)]
+    for vid in pg.value_ids():                   # blocks.py:96-102
+        consumers = partition.consumer_atoms(vid)
+        owner = partition.owner_of_value(vid)
+        foreign = tuple(sorted(consumers - {owner}))
+        if foreign:
+            e = len(tr_owner)
+            tr_owner.append(owner)
+            tr_size.append(_as_int(pg.value_size(vid, 1), vid))
+            tr_cons.append(list(foreign))
+            for x in sorted({owner, *foreign}):
+                atom_tr[x].append(e)
+
+    d_off, d_flat = _csr([[o for o, _ in dl] for dl in deps])
+    ds = [s for dl in deps for _, s in dl]
+    at_off, at = _csr(atom_tasks)
+    ai_off, ai = _csr([[in_index[v] for v in sorted(ins)] for ins in inputs_of_atom])
+    ia_off, ia = _csr(in_atoms)
+    s_off, s = _csr(succ)
+    p_off, p = _csr(pred)
+    n_off, nn = _csr(nbr)
+    tc_off, tc = _csr(tr_cons)
+    atr_off, atr = _csr(atom_tr)
+    return FlatAtoms(
+        n=n, atom_param=_i64(atom_param), task_atom=_i32(task_atom),
+        task_flops=_f64(task_flops), task_fp1=_i64(task_fp1),
+        dep_off=d_off, dep_owner=d_flat, dep_size=_i64(ds),
+        atom_task_off=at_off, atom_tasks=at, atom_in_off=ai_off, atom_in=ai,
+        in_owner=_i32(in_owner), in_size=_i64(in_size), in_atoms_off=ia_off, in_atoms=ia,
+        succ_off=s_off, succ=s, pred_off=p_off, pred=p, nbr_off=n_off, nbr=nn,
+        tr_owner=_i32(tr_owner), tr_size=_i64(tr_size), tr_cons_off=tc_off, tr_cons=tc,
+        atom_tr_off=atr_off, atom_tr=atr,
+        budget=_as_int(model.cluster.device_memory_bytes, "device_memory_bytes"),
+        flops_per_sec=float(cfg.device_flops_per_sec), bwd_fwd_ratio=float(cfg.bwd_fwd_ratio),
+        factor_g=float(cfg.grad_factor), factor_o=float(cfg.optimizer_state_factor),
+    )

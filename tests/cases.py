@@ -114,3 +114,56 @@ def search_instance(rng):
 # ---------------------------------------------------------------- configs
 from paper_2103_16063_b200.workloads import (  # noqa: E402,F401
     CONFIGS, bert_layer_chain, c5_blockset, config_partition)
+
+
+def layered_graph(rng, n_layers=None, branch=2):
+    """Same RNG sequence as pkg/tests/helpers.py:random_layered_graph."""
+    n_layers = n_layers or rng.randint(2, 8)
+    nodes, edges, produced = [_val("in", per_sample=rng.randint(1, 64) * 4)], [], ["in"]
+    for i in range(n_layers):
+        for j in range(rng.randint(1, branch)):
+            tid = f"t{i:02d}_{j}"
+            vid = f"{tid}.out"
+            nodes.append(_task(tid, float(rng.randint(1, 1000))))
+            nodes.append(_val(vid, per_sample=rng.randint(0, 64) * 4, fixed=rng.randint(0, 16) * 4))
+            k = rng.randint(1, min(2, len(produced)))
+            for src in rng.sample(produced, k):
+                edges.append((src, tid))
+            if rng.random() < 0.5:
+                wid = f"{tid}.w"
+                nodes.append(_val(wid, fixed=rng.randint(1, 256) * 4, param=True))
+                edges.append((wid, tid))
+            edges.append((tid, vid))
+            produced.append(vid)
+    return TaskGraph(nodes, edges, ["in"], [produced[-1]])
+
+
+def weighted_chain(flops_list, sizes=None):
+    """pkg/tests/test_blocks.py:31-42."""
+    sizes = sizes or [4.0] * len(flops_list)
+    nodes, edges, prev = [_val("x", per_sample=4.0)], [], "x"
+    for i, (f, s) in enumerate(zip(flops_list, sizes)):
+        t, v = f"t{i:02d}", f"v{i:02d}"
+        nodes += [_task(t, f), _val(v, per_sample=s)]
+        edges += [(prev, t), (t, v)]
+        prev = v
+    return TaskGraph(nodes, edges, ["x"], [prev])
+
+
+def param_chain(flops_list, param_bytes):
+    """pkg/tests/test_blocks.py:45-56."""
+    nodes, edges, prev = [_val("x", per_sample=4.0)], [], "x"
+    for i, f in enumerate(flops_list):
+        t, v, w = f"t{i:02d}", f"v{i:02d}", f"w{i:02d}"
+        nodes += [_task(t, f), _val(v, per_sample=4.0), _val(w, fixed=param_bytes, param=True)]
+        edges += [(prev, t), (w, t), (t, v)]
+        prev = v
+    return TaskGraph(nodes, edges, ["x"], [prev])
+
+
+def blocks_inputs(g, mem=2 ** 40, flops=1e9):
+    """(partition, model) as pkg/tests/test_blocks.py:23-28 builds them."""
+    cl = pc.ClusterSpec(num_nodes=2, devices_per_node=2, device_memory_bytes=mem,
+                        bw_intra=50e9, bw_inter=10e9)
+    p = pc.build_atomic_subcomponents(g)
+    return p, pc.CostModel(p.graph, pc.CostModelConfig(device_flops_per_sec=flops), cl)
