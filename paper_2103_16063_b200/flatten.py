@@ -31,6 +31,8 @@ violates one raises ``UnsupportedGraph`` instead of silently diverging.
 
 from __future__ import annotations
 
+import itertools
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -43,6 +45,8 @@ class UnsupportedGraph(ValueError):
 
 
 def _as_int(x, what: str) -> int:
+    if type(x) is int:
+        return x
     if isinstance(x, (int, np.integer)) and not isinstance(x, bool):
         return int(x)
     xf = float(x)
@@ -316,14 +320,50 @@ class FlatAtoms:
 
 
 def _csr(lists):
+    lens = np.fromiter((len(l) for l in lists), dtype=np.int64, count=len(lists))
     off = np.zeros(len(lists) + 1, np.int64)
-    for i, l in enumerate(lists):
-        off[i + 1] = off[i] + len(l)
-    flat = [x for l in lists for x in l]
+    np.cumsum(lens, out=off[1:])
+    flat = np.fromiter(itertools.chain.from_iterable(lists), dtype=np.int64, count=int(off[-1]))
     return _i32(off), _i32(flat)
 
 
+def _dependencies(partition, n):
+    """AtomicPartition.dependencies() (atoms.py:115-125) with numpy:
+    (owner atom, consumer atom) of every produced value, unique, sorted."""
+    g = partition.graph
+    own, con = [], []
+    for vid in g.value_ids():
+        if g.producer(vid) is None:
+            continue
+        o = partition.owner_of_value(vid)
+        for c in partition.consumer_atoms(vid):
+            if c != o:
+                own.append(o)
+                con.append(c)
+    if not own:
+        return []
+    key = np.unique(np.asarray(own, np.int64) * n + np.asarray(con, np.int64))
+    return list(zip((key // n).tolist(), (key % n).tolist()))
+
+
+_ATOM_CACHE: dict = {}
+
+
 def flatten_atoms(partition, model) -> FlatAtoms:
+    """Cached per (partition, model) object pair (the reference never mutates
+    either); entries are validated by weak references, so a recycled id()
+    never returns a stale flattening."""
+    hit = _ATOM_CACHE.get(id(partition))
+    if hit is not None and hit[0]() is partition and hit[1]() is model:
+        return hit[2]
+    fa = _flatten_atoms(partition, model)
+    if len(_ATOM_CACHE) > 64:
+        _ATOM_CACHE.clear()
+    _ATOM_CACHE[id(partition)] = (weakref.ref(partition), weakref.ref(model), fa)
+    return fa
+
+
+def _flatten_atoms(partition, model) -> FlatAtoms:
     cfg = model.config
     if cfg.cost_table is not None:
         raise UnsupportedGraph("measured cost tables are not supported by the "
@@ -393,7 +433,7 @@ def flatten_atoms(partition, model) -> FlatAtoms:
 
     succ = [[] for _ in range(n)]
     pred = [[] for _ in range(n)]
-    for a, b in partition.dependencies():      # sorted unique pairs
+    for a, b in _dependencies(partition, n):   # sorted unique pairs
         succ[a].append(b)
         pred[b].append(a)
     nbr = [sorted(set(succ[i]) | set(pred[i])) for i in range(n)]
