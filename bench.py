@@ -113,16 +113,30 @@ def _ref_worker_init(nb, D):
     _REF_BS = c5_blockset(nb, D, jitter_seed=JITTER_SEED)
 
 
-def _ref_worker_call(args):
-    """The reference's own form_stage_dp on one call of the workload, bounded
-    by a visit budget (it raises SearchBudgetExceeded after `budget` visits)."""
+class _Deadline:
+    """SearchOptions-compatible options for the unmodified reference: pruning
+    off, and `visit_budget` None until the deadline, then -1 -- the reference's
+    own per-cell check (stages.py:214-216) then raises SearchBudgetExceeded
+    carrying the exact visit count reached."""
+
+    disable_pruning = True
+
+    def __init__(self, seconds):
+        self._end = time.perf_counter() + seconds
+
+    @property
+    def visit_budget(self):
+        return None if time.perf_counter() < self._end else -1
+
+
+def _ref_run(args):
+    """The reference's own form_stage_dp on one call of the workload for about
+    `seconds` of wall time; returns (visits, seconds)."""
     import pipecut
-    (S, D, R, MB), bs_batch, budget = args
+    (S, D, R, MB), bs_batch, seconds = args
     t0 = time.perf_counter()
     try:
-        res = pipecut.form_stage_dp(_REF_BS, S, D, bs_batch, R, MB,
-                                    pipecut.SearchOptions(disable_pruning=True,
-                                                          visit_budget=budget))
+        res = pipecut.form_stage_dp(_REF_BS, S, D, bs_batch, R, MB, _Deadline(seconds))
         visits = res.stats.visits
     except pipecut.SearchBudgetExceeded as exc:
         visits = exc.visits
@@ -134,29 +148,30 @@ def sample_calls(calls, k):
     return [calls[(i * step) % len(calls)] for i in range(k)]
 
 
-def cpu_reference_rate(nb, D, calls, seconds, cores):
-    """Reference visits/s on `cores` host processes, one budget-bounded call
-    each (budget sized from a short calibration to take ~`seconds`)."""
-    import multiprocessing as mp
-    _ref_worker_init(nb, D)
-    probe = sample_calls(calls, 1)[0]
-    v, t = _ref_worker_call((probe, 8 * D, 200_000))
-    rate = v / max(t, 1e-6)
-    budget = max(10_000, int(rate * seconds))
-    work = [(c, 8 * D, budget) for c in sample_calls(calls, cores)]
-    if cores == 1:
-        t0 = time.perf_counter()
-        out = [_ref_worker_call(w) for w in work]
-        wall = time.perf_counter() - t0
-    else:
-        ctx = mp.get_context("fork")
-        with ctx.Pool(cores, initializer=_ref_worker_init, initargs=(nb, D)) as pool:
-            pool.map(_ref_worker_call, [(probe, 8 * D, 1000)] * cores)  # warm workers
-            t0 = time.perf_counter()
-            out = pool.map(_ref_worker_call, work)
-            wall = time.perf_counter() - t0
-    visits = sum(o[0] for o in out)
-    return visits / wall, budget, work
+class RefSampler:
+    """Reference visits/s on `cores` host processes, each running one call of
+    the workload (calls spread over the enumeration) for `seconds`."""
+
+    def __init__(self, nb, D, calls, seconds, cores):
+        import multiprocessing as mp
+        self.cores = cores
+        self.calls = sample_calls(calls, cores)
+        self.work = [(c, 8 * D, seconds) for c in self.calls]
+        if cores == 1:
+            _ref_worker_init(nb, D)
+            self.pool = None
+        else:
+            self.pool = mp.get_context("fork").Pool(cores, initializer=_ref_worker_init,
+                                                    initargs=(nb, D))
+
+    def rate(self):
+        out = self.pool.map(_ref_run, self.work) if self.pool else [_ref_run(w) for w in self.work]
+        return sum(o[0] for o in out) / max(o[1] for o in out)
+
+    def close(self):
+        if self.pool:
+            self.pool.close()
+            self.pool.join()
 
 
 def run_reference_arm(a):
@@ -170,16 +185,18 @@ def run_reference_arm(a):
     calls, _ = enumerate_calls(nodes, dpn, 8 * a.D, a.nb)
     cores = os.cpu_count() or 1
     per_step = max(2.0, min(a.cpu_sample_sec, 120.0 / max(1, a.steps + a.warmup)))
+    sampler = RefSampler(a.nb, a.D, calls, per_step, cores)
     rates = []
-    budget = None
     for i in range(a.warmup + a.steps):
-        r, budget, _ = cpu_reference_rate(a.nb, a.D, calls, per_step, cores)
+        r = sampler.rate()
         if i >= a.warmup:
             rates.append(r)
+    sampler.close()
     value = sorted(rates)[len(rates) // 2]
     sample = (f"{cores} processes x one call of the workload each (calls spread over the "
-              f"enumeration), reference pipecut.form_stage_dp with disable_pruning and "
-              f"visit_budget={budget} (stops after exactly that many visits)")
+              f"enumeration), the reference's pipecut.form_stage_dp with pruning off, each "
+              f"stopped after ~{per_step:.0f} s by its own visit-budget check; "
+              f"value = total visits / slowest worker")
     line = {
         "impl": "reference", "metric": "dp_cells_per_sec", "value": value,
         "unit": "visits/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
@@ -345,12 +362,13 @@ def run_ours(a):
         "clocks": clk.summary(),
     }
     if world == 1 and not a.no_cpu_baseline:
-        rate, budget, work = cpu_reference_rate(nb, a.D, calls, a.cpu_sample_sec, 1)
+        sampler = RefSampler(nb, a.D, calls, a.cpu_sample_sec, 1)
+        rate = sampler.rate()
         line["cpu_baseline"] = {
             "value": rate, "unit": "visits/s", "cores": 1, "kind": "reference",
             "sample": f"reference pipecut.form_stage_dp (baseline/_ref, unmodified) on one call "
-                      f"{work[0][0]} of the workload with disable_pruning and "
-                      f"visit_budget={budget}; single thread"}
+                      f"{sampler.calls[0]} of the workload with pruning off, stopped after "
+                      f"~{a.cpu_sample_sec:.0f} s by its own visit-budget check; single thread"}
     if not a.no_latency and world == 1:
         line["latency_ms"] = config_latencies(ctx)
     print(json.dumps(line), flush=True)
@@ -360,24 +378,32 @@ def run_ours(a):
 
 
 def config_latencies(ctx):
-    """Reference-semantics form_stage latency on C1-C4 through the public API
-    (median of 5 warm runs + 1 cold), reported beside the headline."""
-    from paper_2103_16063_b200 import form_stage
-    from paper_2103_16063_b200._host import pipecut as pc
+    """Reference-semantics partition search on C1-C4 through the public API:
+    partition_blocks + form_stage (median of 5 warm runs + 1 cold), beside the
+    headline; the reference's own times for the same calls are in
+    tests/golden/configs.json (ref_seconds, measured in the build container)."""
+    from paper_2103_16063_b200 import form_stage, partition_blocks
+    from paper_2103_16063_b200 import flatten as _flat
     from paper_2103_16063_b200.workloads import config_partition
     out = {}
     for name in ("C1", "C2", "C3", "C4"):
         part, model, k, batch, cl = config_partition(name)
-        bs = pc.partition_blocks(part, model, k)
-        ts = []
+        tb, ts = [], []
         for i in range(6):
+            _flat._ATOM_CACHE.clear()
             ctx.problem_owner = None
             ctx.lib.pc_reset_cache(ctx.h)
             t0 = time.perf_counter()
+            bs = partition_blocks(part, model, k)
+            t1 = time.perf_counter()
             res = form_stage(cl.num_nodes, cl.devices_per_node, batch, bs)
-            ts.append((time.perf_counter() - t0) * 1e3)
-        warm = sorted(ts[1:])
-        out[name] = {"cold_ms": ts[0], "warm_ms": warm[len(warm) // 2],
+            t2 = time.perf_counter()
+            tb.append((t1 - t0) * 1e3)
+            ts.append((t2 - t1) * 1e3)
+        med = lambda v: sorted(v[1:])[len(v[1:]) // 2]
+        out[name] = {"partition_blocks_ms": med(tb), "form_stage_ms": med(ts),
+                     "total_ms": med([a + b for a, b in zip(tb, ts)]),
+                     "cold_total_ms": tb[0] + ts[0],
                      "visits": res.stats.visits, "dp_calls": res.stats.dp_calls,
                      "objective": None if res.plan is None else res.plan.objective}
     return out
