@@ -202,6 +202,11 @@ extern "C" int pc_set_problem(pc_ctx *ctx, const pc_problem *p) {
         int ex = 0;
         const double fr = frexp(p->bwd_fwd_ratio, &ex);
         ctx->derived = p->bwd_fwd_ratio > 0 && fr == 0.5;
+        // span times are folds of (f*m)/F: non-negative terms make them monotone
+        // in the span, which the DP's prefix skip relies on
+        bool nonneg = p->flops_per_sec > 0 && p->bwd_fwd_ratio >= 0;
+        for (int t = 0; t < T && nonneg; ++t) nonneg = p->task_flops[t] >= 0.0;
+        ctx->mono_skip = nonneg;
     }
     ctx->has_problem = true;
     return PC_OK;
@@ -462,6 +467,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.key_cut = ((const double *const *)ctx->key_ptrs.p) + 2 * nk;
         bt.key_ffb = ((const int32_t *const *)ctx->key_ptrs.p) + 3 * nk;
         bt.beta = P.beta;
+        bt.mono_skip = ctx->mono_skip ? 1 : 0;
         bt.num_nodes = P.num_nodes;
         bt.dpn = P.dpn;
         bt.val_cells = val_cells;
@@ -490,9 +496,9 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.hspill_used = used + 3 * (size_t)n + 2;
         bt.hist_cells = hist_cells;
         CUDA_TRY(ctx, cudaMemsetAsync(ob, 0, 64 + 3 * sizeof(unsigned long long) * (size_t)n + 64, ctx->st));
-        CUDA_TRY(ctx, ctx->counters_d.ensure((4 + FMAX) * sizeof(unsigned long long)));
+        CUDA_TRY(ctx, ctx->counters_d.ensure((8 + FMAX) * sizeof(unsigned long long)));
         bt.counters = ctx->counters_d.as<unsigned long long>();
-        CUDA_TRY(ctx, cudaMemsetAsync(bt.counters, 0, (4 + FMAX) * sizeof(unsigned long long), ctx->st));
+        CUDA_TRY(ctx, cudaMemsetAsync(bt.counters, 0, (8 + FMAX) * sizeof(unsigned long long), ctx->st));
         int64_t launches = 0;
         for (int s = 1; s <= maxS; ++s) {
             int n_active = 0;
@@ -508,7 +514,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         if (int rc = check_launch(ctx, "dp_level")) return rc;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev2, ctx->st));
         int ovf = 0;
-        unsigned long long cnt[4 + FMAX] = {0};
+        unsigned long long cnt[8 + FMAX] = {0};
         CUDA_TRY(ctx, cudaMemcpyAsync(&ovf, bt.overflow, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaMemcpyAsync(cnt, bt.counters, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
@@ -520,7 +526,8 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
                     n, cnt[0], cnt[1], cnt[2], ovf, vcap, hcap);
             for (int q = 0; q <= FMAX; ++q)
                 if (cnt[3 + q]) fprintf(stderr, " %d:%llu", q, cnt[3 + q]);
-            fprintf(stderr, "\n");
+            fprintf(stderr, "\n  warp rounds %llu, warp iterations %llu, corner-pruned pairs %llu, window entries %llu\n",
+                    cnt[4 + FMAX], cnt[5 + FMAX], cnt[6 + FMAX], cnt[7 + FMAX]);
         }
         float ms = 0;
         cudaEventElapsedTime(&ms, ctx->ev1, ctx->ev2);

@@ -73,7 +73,7 @@ __host__ __device__ inline int inter_of(int num_nodes, int dpn, int64_t cum) {
 
 // ------------------------------------------------------------------ key tables
 // One (microbatch share m, checkpointing) key:
-//   tf[hm_idx(lo,hi)]  t_fwd of span [lo,hi) at m, NaN if mem > budget
+//   tf[hm_idx(lo,hi)]  t_fwd of span [lo,hi) at m, sign bit set if mem > budget
 //   tb[hm_idx(lo,hi)]  t_bwd (absent when it is derived as beta * t_fwd)
 //   cut[inter][c]      cut_time(c, m, inter) for c in [0, nb]
 
@@ -111,6 +111,7 @@ struct DPBatch {
     const int32_t *const *key_ffb;  // per key: first feasible lo for each hi
     double beta;
     int num_nodes, dpn;
+    int mono_skip;                  // t_fwd(b', b) non-increasing in b' (flops >= 0): enable skip
     // per level, per (call, d column): smallest / largest b of a non-empty cell
     int32_t *col_min[2];
     int32_t *col_max[2];

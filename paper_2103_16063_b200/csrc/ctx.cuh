@@ -70,6 +70,7 @@ struct pc_ctx {
     DBuf key_ptrs;   // [3][n_keys] device pointers (tf, tb, cut)
     size_t key_bytes = 0;
     bool derived = false;    // t_bwd derived as beta * t_fwd (beta a power of two)
+    bool mono_skip = false;  // span times monotone (non-negative flops): DP prefix skip
     DBuf mismatch_d;
     // batch scratch
     DBuf calls_d, warp_prefix_d, keyidx_d, val_d, hist_d, overflow_d;

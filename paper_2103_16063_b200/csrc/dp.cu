@@ -24,6 +24,10 @@
 
 #include "common.cuh"
 
+#ifndef DP_MIN_BLOCKS
+#define DP_MIN_BLOCKS 4
+#endif
+
 namespace pcb {
 
 __device__ __forceinline__ double dmax_ref(double a, double b) {
@@ -38,18 +42,47 @@ __device__ __forceinline__ bool dominates(double ex, double ey, uint32_t ek, dou
 }
 
 // Per-warp Pareto frontiers in shared memory, each sorted by x ascending
-// (y strictly descending).  Namespace scope so every access compiles to
-// LDS/STS rather than generic loads.
+// (y strictly descending).  Accessed through one 32-bit shared-window base
+// per warp (ld/st.shared), so no generic addressing and no per-access
+// rematerialization of the warp index.
 __shared__ double g_fx[DP_WARPS][FMAX];
 __shared__ double g_fy[DP_WARPS][FMAX];
 __shared__ uint32_t g_fk[DP_WARPS][FMAX];
 
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 struct WarpFront {
-    int w;
-    __device__ __forceinline__ double &x(int j) const { return g_fx[w][j]; }
-    __device__ __forceinline__ double &y(int j) const { return g_fy[w][j]; }
-    __device__ __forceinline__ uint32_t &k(int j) const { return g_fk[w][j]; }
+    uint32_t bx, by, bk;   // shared-window addresses of this warp's arrays
+    __device__ __forceinline__ double x(int j) const { return lds_f64(bx + 8u * j); }
+    __device__ __forceinline__ double y(int j) const { return lds_f64(by + 8u * j); }
+    __device__ __forceinline__ uint32_t k(int j) const { return lds_u32(bk + 4u * j); }
+    __device__ __forceinline__ void put(int j, double vx, double vy, uint32_t vk) const {
+        sts_f64(bx + 8u * j, vx);
+        sts_f64(by + 8u * j, vy);
+        sts_u32(bk + 4u * j, vk);
+    }
 };
+
+__device__ __forceinline__ WarpFront warp_front(int w) {
+    return WarpFront{(uint32_t)__cvta_generic_to_shared(&g_fx[w][0]),
+                     (uint32_t)__cvta_generic_to_shared(&g_fy[w][0]),
+                     (uint32_t)__cvta_generic_to_shared(&g_fk[w][0])};
+}
 
 __device__ __forceinline__ int log2_steps(int n) {
     // number of binary-search halvings covering n entries (n >= 1)
@@ -82,13 +115,32 @@ __device__ __forceinline__ bool corner_dominated(const WarpFront &f, int n, doub
 }
 
 // Warp-cooperative exact insert of c (same c in every lane); lane l owns
-// slots l and l + 32.  Returns the new size, or -1 beyond FMAX.
-__device__ __forceinline__ int front_insert(WarpFront &f, int n, int lane, double cx, double cy,
+// slots l and l + 32 (the second only once the frontier exceeds 32).
+// Returns the new size, or -1 beyond FMAX.
+__device__ __forceinline__ int front_insert(const WarpFront &f, int n, int lane, double cx, double cy,
                                             uint32_t ck) {
-    const bool h0 = lane < n, h1 = lane + 32 < n;
-    double x0 = 0, y0 = 0, x1 = 0, y1 = 0;
-    uint32_t k0 = 0, k1 = 0;
+    const bool h0 = lane < n;
+    double x0 = 0, y0 = 0;
+    uint32_t k0 = 0;
     if (h0) { x0 = f.x(lane); y0 = f.y(lane); k0 = f.k(lane); }
+    if (n <= 32) {
+        if (__any_sync(0xffffffffu, h0 && dominates(x0, y0, k0, cx, cy, ck))) return n;
+        const bool keep0 = h0 && !dominates(cx, cy, ck, x0, y0, k0);
+        const uint32_t m0 = __ballot_sync(0xffffffffu, keep0);
+        const bool lt0 = keep0 && x0 < cx;
+        const int pos_c = __popc(__ballot_sync(0xffffffffu, lt0));
+        const int nn = __popc(m0) + 1;
+        if (nn > FMAX) return -1;
+        const int p0 = __popc(m0 & ((1u << lane) - 1u)) + (lt0 ? 0 : 1);
+        __syncwarp();
+        if (keep0) f.put(p0, x0, y0, k0);
+        if (lane == 0) f.put(pos_c, cx, cy, ck);
+        __syncwarp();
+        return nn;
+    }
+    const bool h1 = lane + 32 < n;
+    double x1 = 0, y1 = 0;
+    uint32_t k1 = 0;
     if (h1) { x1 = f.x(lane + 32); y1 = f.y(lane + 32); k1 = f.k(lane + 32); }
     if (__any_sync(0xffffffffu, (h0 && dominates(x0, y0, k0, cx, cy, ck)) ||
                                     (h1 && dominates(x1, y1, k1, cx, cy, ck))))
@@ -105,9 +157,9 @@ __device__ __forceinline__ int front_insert(WarpFront &f, int n, int lane, doubl
     const int p0 = __popc(m0 & below) + (lt0 ? 0 : 1);
     const int p1 = __popc(m0) + __popc(m1 & below) + (lt1 ? 0 : 1);
     __syncwarp();
-    if (keep0) { f.x(p0) = x0; f.y(p0) = y0; f.k(p0) = k0; }
-    if (keep1) { f.x(p1) = x1; f.y(p1) = y1; f.k(p1) = k1; }
-    if (lane == 0) { f.x(pos_c) = cx; f.y(pos_c) = cy; f.k(pos_c) = ck; }
+    if (keep0) f.put(p0, x0, y0, k0);
+    if (keep1) f.put(p1, x1, y1, k1);
+    if (lane == 0) f.put(pos_c, cx, cy, ck);
     __syncwarp();
     return nn;
 }
@@ -136,7 +188,7 @@ __device__ __forceinline__ int lex_min_lane(bool live, double x, double y, uint3
 }
 
 template <bool DERIVED>
-__global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s, int n_active) {
+__global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBatch B, int s, int n_active) {
     const int64_t cta = blockIdx.x;
     if (cta >= B.cta_prefix[n_active]) return;
     int lo = 0, hi = n_active;
@@ -163,11 +215,12 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
     const int inter_d = inter_of(B.num_nodes, B.dpn, d);
     const int64_t row = (int64_t)b * (b - 1) / 2;       // hm_idx(0, b)
     const double beta = B.beta;
-    WarpFront F{w};
+    const WarpFront F = warp_front(w);
     int n = 0;
     bool ovf = false;
     bool zero = false;
     uint32_t n_pairs = 0, n_cands = 0, n_ins = 0;
+    uint32_t n_corner = 0, n_win = 0, n_rounds = 0, n_iters = 0;
 
     if (s == 1) {
         // level 0 holds the single cell (0, 0) with entry (0.0, 0.0) (stages.py:201)
@@ -176,15 +229,11 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
             zero = true;
         } else {
             const double tf = B.key_tf[kk][row];
-            if (!isnan(tf)) {
+            if (!signbit(tf)) {
                 double tfc = tf;
                 if (b < nb) tfc = __dadd_rn(tf, B.key_cut[kk][inter_d * (nb + 1) + b]);
                 const double tbc = DERIVED ? __dmul_rn(beta, tf) : B.key_tb[kk][row];
-                if (lane == 0) {
-                    F.x(0) = dmax_ref(0.0, tfc);
-                    F.y(0) = dmax_ref(0.0, tbc);
-                    F.k(0) = pack_key(0, 0, 0);
-                }
+                if (lane == 0) F.put(0, dmax_ref(0.0, tfc), dmax_ref(0.0, tbc), pack_key(0, 0, 0));
                 __syncwarp();
                 n = 1;
                 n_pairs = lane == 0;
@@ -225,22 +274,34 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
             const double *cutb = B.key_cut[kk] + inter_of(B.num_nodes, B.dpn, dp) * (nb + 1);
             const uint8_t *ccol = pcnt + (int64_t)(dp - base) * cd.A - base;
             const uint32_t *ocol = poff + (int64_t)(dp - base) * cd.A - base;
-            for (int bp0 = bp_lo; bp0 <= bp_hi; bp0 += 32) {
-                const int bp = bp0 + lane;
-                int cnt = bp <= bp_hi ? (ccol[bp] & CNT_MASK) : 0;
+            // Scan b' downward from bp_hi.  Every candidate of pair b' is >= its
+            // corner (tfc, tbc) and tbc >= t_bwd(b', b); t_fwd(b', b) and t_bwd
+            // only grow as b' falls (a fold of non-negative terms), so "some
+            // frontier entry strictly dominates (tf + cut(b), t_bwd)" holds on
+            // a prefix of b': a 32-ary warp search finds its end, and b' up to
+            // there are skipped without loading their predecessors.
+            int lim = bp_lo - 1;          // b' <= lim are settled
+            int lim_v = -1;               // insert count lim was computed at
+            // One chunk of 32 predecessors b' in (top-32, top], minus an already
+            // processed window [ex_lo, ex_hi].
+            auto chunk = [&](int top, int ex_lo, int ex_hi) {
+                const int bp = top - lane;
+                int cnt = (bp > lim && bp >= bp_lo && (bp < ex_lo || bp > ex_hi))
+                              ? (ccol[bp] & CNT_MASK) : 0;
                 double tfc = 0.0, tbc = 0.0;
                 int wlo = 0, whi = -1;
                 const double *etf = qtf, *etb = qtb;
                 int64_t pbase = 0;
                 if (cnt > 0) {
                     const double tf = tfrow[bp];
-                    if (!isnan(tf)) {                               // mem <= budget (stages.py:230)
+                    if (!signbit(tf)) {                             // mem <= budget (stages.py:230)
                         tfc = b < nb ? __dadd_rn(tf, cutf) : tf;
                         tbc = DERIVED ? __dmul_rn(beta, tf) : tbrow[bp];
                         if (bp > 0) tbc = __dadd_rn(tbc, cutb[bp]);
                         ++n_pairs;
                         n_cands += cnt;
-                        if (n == 0 || !corner_dominated(F, n, tfc, tbc)) {
+                        if (n > 0 && corner_dominated(F, n, tfc, tbc)) ++n_corner;
+                        else {
                             const uint32_t praw = ocol[bp];
                             pbase = (int64_t)(praw & ~SPILL_BIT);
                             if (praw & SPILL_BIT) { etf = stf; etb = stb; }
@@ -257,6 +318,9 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
                     }
                 }
                 const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)(whi - wlo + 1));
+                n_win += whi - wlo + 1;
+                n_rounds += rounds;
+                ++n_iters;
                 for (int r = 0; r < rounds; ++r) {
                     const int i = wlo + r;
                     double cx = 0.0, cy = 0.0;
@@ -281,6 +345,151 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
                         surv = surv && lane != t && !dominates(tx, ty, tk, cx, cy, ck);
                     }
                 }
+            };
+            const int ex_lo = 1, ex_hi = 0;   // no excluded window
+            // Scan b' downward from bp_hi.  Every candidate of pair b' is >= its
+            // corner (tfc, tbc) and tbc >= t_bwd(b', b); t_fwd(b', b) and t_bwd
+            // only grow as b' falls (a fold of non-negative terms), so "some
+            // frontier entry strictly dominates (tf + cut(b), t_bwd)" holds on
+            // a prefix of b': a 32-ary warp search finds its end, and b' up to
+            // there are skipped without loading their predecessors.
+            int lim = bp_lo - 1;          // b' <= lim are settled
+            int lim_v = -1;               // insert count lim was computed at
+            // One chunk of 32 predecessors b' in (top-32, top], minus an already
+            // processed window [ex_lo, ex_hi].
+            auto chunk = [&](int top, int ex_lo, int ex_hi) {
+                const int bp = top - lane;
+                int cnt = (bp > lim && bp >= bp_lo && (bp < ex_lo || bp > ex_hi))
+                              ? (ccol[bp] & CNT_MASK) : 0;
+                double tfc = 0.0, tbc = 0.0;
+                int wlo = 0, whi = -1;
+                const double *etf = qtf, *etb = qtb;
+                int64_t pbase = 0;
+                if (cnt > 0) {
+                    const double tf = tfrow[bp];
+                    if (!signbit(tf)) {                             // mem <= budget (stages.py:230)
+                        tfc = b < nb ? __dadd_rn(tf, cutf) : tf;
+                        tbc = DERIVED ? __dmul_rn(beta, tf) : tbrow[bp];
+                        if (bp > 0) tbc = __dadd_rn(tbc, cutb[bp]);
+                        ++n_pairs;
+                        n_cands += cnt;
+                        if (n > 0 && corner_dominated(F, n, tfc, tbc)) ++n_corner;
+                        else {
+                            const uint32_t praw = ocol[bp];
+                            pbase = (int64_t)(praw & ~SPILL_BIT);
+                            if (praw & SPILL_BIT) { etf = stf; etb = stb; }
+                            // exact window: entries with ptf <= tfc collapse onto the
+                            // last of them, entries with ptb <= tbc onto the first
+                            int i0 = -1, i1 = cnt;
+                            for (int i = 0; i < cnt; ++i) {
+                                if (etf[pbase + i] <= tfc) i0 = i;
+                                if (i1 == cnt && etb[pbase + i] <= tbc) i1 = i;
+                            }
+                            if (i1 <= i0) { wlo = i1; whi = i1; }
+                            else { wlo = i0 < 0 ? 0 : i0; whi = i1 < cnt ? i1 : cnt - 1; }
+                        }
+                    }
+                }
+                const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)(whi - wlo + 1));
+                n_win += whi - wlo + 1;
+                n_rounds += rounds;
+                ++n_iters;
+                for (int r = 0; r < rounds; ++r) {
+                    const int i = wlo + r;
+                    double cx = 0.0, cy = 0.0;
+                    uint32_t ck = 0;
+                    bool surv = false;
+                    if (i <= whi) {
+                        cx = dmax_ref(etf[pbase + i], tfc);
+                        cy = dmax_ref(etb[pbase + i], tbc);
+                        ck = pack_key(bp, dp, i);
+                        surv = n == 0 || !front_dominated(F, n, cx, cy, ck);
+                    }
+                    while (__any_sync(0xffffffffu, surv)) {
+                        // insert the lexicographically smallest survivor first: nothing
+                        // among the survivors can dominate it, and it removes the most
+                        const int t = lex_min_lane(surv, cx, cy, ck);
+                        const double tx = __shfl_sync(0xffffffffu, cx, t);
+                        const double ty = __shfl_sync(0xffffffffu, cy, t);
+                        const uint32_t tk = __shfl_sync(0xffffffffu, ck, t);
+                        ++n_ins;
+                        const int nn = front_insert(F, n, lane, tx, ty, tk);
+                        if (nn < 0) ovf = true; else n = nn;
+                        surv = surv && lane != t && !dominates(tx, ty, tk, cx, cy, ck);
+                    }
+                }
+            };
+            // Ordering only (the frontier is order-independent): probe 32 b'
+            // across the range and start at the one whose best predecessor
+            // entry gives the smallest tf + tb -- the balance between the
+            // prefix and the last stage -- so later chunks mostly fail the
+            // dominance tests instead of replacing frontier entries.
+            int ex_lo = 1, ex_hi = 0;
+            if (bp_hi - bp_lo + 1 > 32) {
+                const int span = bp_hi - bp_lo + 1;
+                const int step = span / 32;
+                const int p = bp_lo + lane * step + step / 2;
+                double score = __longlong_as_double(0x7ff0000000000000LL);
+                const int c = ccol[p] & CNT_MASK;
+                const double tf = tfrow[p];
+                if (c > 0 && !signbit(tf)) {
+                    const double tfc = b < nb ? __dadd_rn(tf, cutf) : tf;
+                    double tbc = DERIVED ? __dmul_rn(beta, tf) : tbrow[p];
+                    if (p > 0) tbc = __dadd_rn(tbc, cutb[p]);
+                    const uint32_t praw = ocol[p];
+                    const int64_t pb = (int64_t)(praw & ~SPILL_BIT);
+                    const double *etf = (praw & SPILL_BIT) ? stf : qtf;
+                    const double *etb = (praw & SPILL_BIT) ? stb : qtb;
+                    const double s0 = dmax_ref(etf[pb], tfc) + dmax_ref(etb[pb], tbc);
+                    const double s1 = dmax_ref(etf[pb + c - 1], tfc) + dmax_ref(etb[pb + c - 1], tbc);
+                    score = s0 < s1 ? s0 : s1;
+                }
+                int best = p;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double os = __shfl_xor_sync(0xffffffffu, score, o);
+                    const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    if (os < score || (os == score && ob < best)) { score = os; best = ob; }
+                }
+                if (score < __longlong_as_double(0x7ff0000000000000LL)) {
+                    const int top = min(bp_hi, best + 16);
+                    chunk(top, 1, 0);
+                    ex_lo = top - 31;
+                    ex_hi = top;
+                }
+            }
+            // Scan b' downward from bp_hi.  Every candidate of pair b' is >= its
+            // corner (tfc, tbc) and tbc >= t_bwd(b', b); t_fwd(b', b) and t_bwd
+            // only grow as b' falls (a fold of non-negative terms), so "some
+            // frontier entry strictly dominates (tf + cut(b), t_bwd)" holds on
+            // a prefix of b': a 32-ary warp search finds its end, and b' up to
+            // there are skipped without loading their predecessors.
+            for (int top = bp_hi; top > lim; top -= 32) {
+                if (B.mono_skip && n > 0 && (int)n_ins != lim_v) {
+                    int lo_b = lim, hi_b = top + 1;   // cond true <= lo_b, false >= hi_b
+                    while (hi_b - lo_b > 1) {
+                        const int span = hi_b - lo_b - 1;
+                        const int step = (span + 31) / 32;
+                        const int p = lo_b + (lane + 1) * step;
+                        bool cond = false;
+                        if (p < hi_b) {
+                            const double tv = fabs(tfrow[p]);
+                            const double tfc = b < nb ? __dadd_rn(tv, cutf) : tv;
+                            const double tbl = DERIVED ? __dmul_rn(beta, tv) : fabs(tbrow[p]);
+                            cond = corner_dominated(F, n, tfc, tbl);
+                        }
+                        const uint32_t m = __ballot_sync(0xffffffffu, cond);
+                        const int k = __popc(m);              // a prefix of the lanes
+                        if (k > 0) lo_b = lo_b + k * step;
+                        const int nh = lo_b + step;           // first false sample
+                        if (k < 32 && nh < hi_b) hi_b = nh;
+                        if (lo_b >= hi_b - 1) break;
+                    }
+                    lim = lo_b;
+                    lim_v = (int)n_ins;
+                    if (top <= lim) break;
+                }
+                chunk(top, ex_lo, ex_hi);
             }
         }
         (void)tfrow_base;
@@ -296,6 +505,20 @@ __global__ void __launch_bounds__(DP_WARPS * 32, 4) k_dp_level(DPBatch B, int s,
         atomicAdd(&B.counters[1], (unsigned long long)n_cands);
         atomicAdd(&B.counters[2], (unsigned long long)n_ins);
         atomicAdd(&B.counters[3 + min(n, FMAX)], 1ull);     // frontier-size histogram
+        atomicAdd(&B.counters[4 + FMAX + 0], (unsigned long long)n_rounds);
+        atomicAdd(&B.counters[4 + FMAX + 1], (unsigned long long)n_iters);
+    }
+    {
+        unsigned a = n_corner, bw = n_win;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            bw += __shfl_xor_sync(0xffffffffu, bw, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&B.counters[4 + FMAX + 2], (unsigned long long)a);
+            atomicAdd(&B.counters[4 + FMAX + 3], (unsigned long long)bw);
+        }
     }
     const bool any_zero = __any_sync(0xffffffffu, zero);
 

@@ -168,7 +168,9 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
         const int64_t mem = (int64_t)memd;
         const bool ok = mem <= p.mem_budget;                   // stages.py:230
         const int64_t o = hm_idx(lo, hi);
-        out_f[o] = ok ? f : __longlong_as_double(0x7ff8000000000000LL);
+        // infeasible spans keep |t_fwd| with the sign bit set: the DP skip
+        // search needs the magnitude, the DP tests signbit for feasibility
+        out_f[o] = ok ? f : -f;
         if (derived) {
             bad |= ok && __dmul_rn(p.beta, f) != b;
         } else {
@@ -202,7 +204,7 @@ __global__ void k_first_feasible(int nb, int n_keys, const double *const *tf, in
     const int hi = (int)(gid % (nb + 1));
     const double *row = tf[k] + hm_idx(0, hi);
     int lo = 0;
-    while (lo < hi && isnan(row[lo])) ++lo;
+    while (lo < hi && signbit(row[lo])) ++lo;
     ffb[k][hi] = lo;
 }
 

@@ -31,19 +31,14 @@ for hi, r in enumerate(rows):
 h = rows[hi]
 ie = h.index("Instructions Executed")
 ws = h.index("Warp Stall Sampling (All Samples)")
-cur, agg = None, {}
+agg = {}
 for r in rows[hi + 1:]:
-    if not r:
-        continue
-    if r[0] and not r[0].startswith("0x"):
-        cur = (r[0], r[1].strip())
-        agg.setdefault(cur, [0.0, 0.0])
-        continue
-    if cur is None or len(r) <= ie:
+    # source-line rows carry the line's aggregated metrics (SASS rows have an
+    # empty first column)
+    if not r or not r[0] or r[0].startswith("0x") or len(r) <= ie:
         continue
     try:
-        agg[cur][0] += float(r[ie] or 0)
-        agg[cur][1] += float(r[ws] or 0)
+        agg[(r[0], r[1].strip())] = [float(r[ie] or 0), float(r[ws] or 0)]
     except ValueError:
         pass
 tot = sum(v[0] for v in agg.values()) or 1
