@@ -201,8 +201,10 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
     // warps take consecutive cells of the call in (b, d) order, so every warp
     // of the CTA has a cell whatever B is
     const int w = threadIdx.x >> 5;
-    const int64_t idx = (cta - B.cta_prefix[c]) * DP_WARPS + w;
-    if (idx >= (int64_t)cd.A * cd.B) return;          // whole warp
+    // heaviest cells (largest b: most predecessors) are dispatched first so
+    // the level's tail is short
+    const int64_t idx = (int64_t)cd.A * cd.B - 1 - ((cta - B.cta_prefix[c]) * DP_WARPS + w);
+    if (idx < 0) return;                              // whole warp
     const int bi = (int)(idx / cd.B);
     const int di = (int)(idx % cd.B);
     const int lane = threadIdx.x & 31;
@@ -274,12 +276,6 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
             const double *cutb = B.key_cut[kk] + inter_of(B.num_nodes, B.dpn, dp) * (nb + 1);
             const uint8_t *ccol = pcnt + (int64_t)(dp - base) * cd.A - base;
             const uint32_t *ocol = poff + (int64_t)(dp - base) * cd.A - base;
-            // Scan b' downward from bp_hi.  Every candidate of pair b' is >= its
-            // corner (tfc, tbc) and tbc >= t_bwd(b', b); t_fwd(b', b) and t_bwd
-            // only grow as b' falls (a fold of non-negative terms), so "some
-            // frontier entry strictly dominates (tf + cut(b), t_bwd)" holds on
-            // a prefix of b': a 32-ary warp search finds its end, and b' up to
-            // there are skipped without loading their predecessors.
             int lim = bp_lo - 1;          // b' <= lim are settled
             int lim_v = -1;               // insert count lim was computed at
             // One chunk of 32 predecessors b' in (top-32, top], minus an already
@@ -300,11 +296,16 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                         if (bp > 0) tbc = __dadd_rn(tbc, cutb[bp]);
                         ++n_pairs;
                         n_cands += cnt;
-                        if (n > 0 && corner_dominated(F, n, tfc, tbc)) ++n_corner;
+                        const uint32_t praw = ocol[bp];
+                        pbase = (int64_t)(praw & ~SPILL_BIT);
+                        if (praw & SPILL_BIT) { etf = stf; etb = stb; }
+                        // every candidate of the pair is >= its ideal point: the
+                        // predecessor frontier's smallest tf (entry 0) and smallest
+                        // tb (last entry), each clipped by the new stage
+                        const double ix = dmax_ref(etf[pbase], tfc);
+                        const double iy = dmax_ref(etb[pbase + cnt - 1], tbc);
+                        if (n > 0 && corner_dominated(F, n, ix, iy)) ++n_corner;
                         else {
-                            const uint32_t praw = ocol[bp];
-                            pbase = (int64_t)(praw & ~SPILL_BIT);
-                            if (praw & SPILL_BIT) { etf = stf; etb = stb; }
                             // exact window: entries with ptf <= tfc collapse onto the
                             // last of them, entries with ptb <= tbc onto the first
                             int i0 = -1, i1 = cnt;
@@ -347,117 +348,6 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                 }
             };
             const int ex_lo = 1, ex_hi = 0;   // no excluded window
-            // Scan b' downward from bp_hi.  Every candidate of pair b' is >= its
-            // corner (tfc, tbc) and tbc >= t_bwd(b', b); t_fwd(b', b) and t_bwd
-            // only grow as b' falls (a fold of non-negative terms), so "some
-            // frontier entry strictly dominates (tf + cut(b), t_bwd)" holds on
-            // a prefix of b': a 32-ary warp search finds its end, and b' up to
-            // there are skipped without loading their predecessors.
-            int lim = bp_lo - 1;          // b' <= lim are settled
-            int lim_v = -1;               // insert count lim was computed at
-            // One chunk of 32 predecessors b' in (top-32, top], minus an already
-            // processed window [ex_lo, ex_hi].
-            auto chunk = [&](int top, int ex_lo, int ex_hi) {
-                const int bp = top - lane;
-                int cnt = (bp > lim && bp >= bp_lo && (bp < ex_lo || bp > ex_hi))
-                              ? (ccol[bp] & CNT_MASK) : 0;
-                double tfc = 0.0, tbc = 0.0;
-                int wlo = 0, whi = -1;
-                const double *etf = qtf, *etb = qtb;
-                int64_t pbase = 0;
-                if (cnt > 0) {
-                    const double tf = tfrow[bp];
-                    if (!signbit(tf)) {                             // mem <= budget (stages.py:230)
-                        tfc = b < nb ? __dadd_rn(tf, cutf) : tf;
-                        tbc = DERIVED ? __dmul_rn(beta, tf) : tbrow[bp];
-                        if (bp > 0) tbc = __dadd_rn(tbc, cutb[bp]);
-                        ++n_pairs;
-                        n_cands += cnt;
-                        if (n > 0 && corner_dominated(F, n, tfc, tbc)) ++n_corner;
-                        else {
-                            const uint32_t praw = ocol[bp];
-                            pbase = (int64_t)(praw & ~SPILL_BIT);
-                            if (praw & SPILL_BIT) { etf = stf; etb = stb; }
-                            // exact window: entries with ptf <= tfc collapse onto the
-                            // last of them, entries with ptb <= tbc onto the first
-                            int i0 = -1, i1 = cnt;
-                            for (int i = 0; i < cnt; ++i) {
-                                if (etf[pbase + i] <= tfc) i0 = i;
-                                if (i1 == cnt && etb[pbase + i] <= tbc) i1 = i;
-                            }
-                            if (i1 <= i0) { wlo = i1; whi = i1; }
-                            else { wlo = i0 < 0 ? 0 : i0; whi = i1 < cnt ? i1 : cnt - 1; }
-                        }
-                    }
-                }
-                const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)(whi - wlo + 1));
-                n_win += whi - wlo + 1;
-                n_rounds += rounds;
-                ++n_iters;
-                for (int r = 0; r < rounds; ++r) {
-                    const int i = wlo + r;
-                    double cx = 0.0, cy = 0.0;
-                    uint32_t ck = 0;
-                    bool surv = false;
-                    if (i <= whi) {
-                        cx = dmax_ref(etf[pbase + i], tfc);
-                        cy = dmax_ref(etb[pbase + i], tbc);
-                        ck = pack_key(bp, dp, i);
-                        surv = n == 0 || !front_dominated(F, n, cx, cy, ck);
-                    }
-                    while (__any_sync(0xffffffffu, surv)) {
-                        // insert the lexicographically smallest survivor first: nothing
-                        // among the survivors can dominate it, and it removes the most
-                        const int t = lex_min_lane(surv, cx, cy, ck);
-                        const double tx = __shfl_sync(0xffffffffu, cx, t);
-                        const double ty = __shfl_sync(0xffffffffu, cy, t);
-                        const uint32_t tk = __shfl_sync(0xffffffffu, ck, t);
-                        ++n_ins;
-                        const int nn = front_insert(F, n, lane, tx, ty, tk);
-                        if (nn < 0) ovf = true; else n = nn;
-                        surv = surv && lane != t && !dominates(tx, ty, tk, cx, cy, ck);
-                    }
-                }
-            };
-            // Ordering only (the frontier is order-independent): probe 32 b'
-            // across the range and start at the one whose best predecessor
-            // entry gives the smallest tf + tb -- the balance between the
-            // prefix and the last stage -- so later chunks mostly fail the
-            // dominance tests instead of replacing frontier entries.
-            int ex_lo = 1, ex_hi = 0;
-            if (bp_hi - bp_lo + 1 > 32) {
-                const int span = bp_hi - bp_lo + 1;
-                const int step = span / 32;
-                const int p = bp_lo + lane * step + step / 2;
-                double score = __longlong_as_double(0x7ff0000000000000LL);
-                const int c = ccol[p] & CNT_MASK;
-                const double tf = tfrow[p];
-                if (c > 0 && !signbit(tf)) {
-                    const double tfc = b < nb ? __dadd_rn(tf, cutf) : tf;
-                    double tbc = DERIVED ? __dmul_rn(beta, tf) : tbrow[p];
-                    if (p > 0) tbc = __dadd_rn(tbc, cutb[p]);
-                    const uint32_t praw = ocol[p];
-                    const int64_t pb = (int64_t)(praw & ~SPILL_BIT);
-                    const double *etf = (praw & SPILL_BIT) ? stf : qtf;
-                    const double *etb = (praw & SPILL_BIT) ? stb : qtb;
-                    const double s0 = dmax_ref(etf[pb], tfc) + dmax_ref(etb[pb], tbc);
-                    const double s1 = dmax_ref(etf[pb + c - 1], tfc) + dmax_ref(etb[pb + c - 1], tbc);
-                    score = s0 < s1 ? s0 : s1;
-                }
-                int best = p;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double os = __shfl_xor_sync(0xffffffffu, score, o);
-                    const int ob = __shfl_xor_sync(0xffffffffu, best, o);
-                    if (os < score || (os == score && ob < best)) { score = os; best = ob; }
-                }
-                if (score < __longlong_as_double(0x7ff0000000000000LL)) {
-                    const int top = min(bp_hi, best + 16);
-                    chunk(top, 1, 0);
-                    ex_lo = top - 31;
-                    ex_hi = top;
-                }
-            }
             // Scan b' downward from bp_hi.  Every candidate of pair b' is >= its
             // corner (tfc, tbc) and tbc >= t_bwd(b', b); t_fwd(b', b) and t_bwd
             // only grow as b' falls (a fold of non-negative terms), so "some
