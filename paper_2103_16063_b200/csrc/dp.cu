@@ -258,7 +258,11 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         const int32_t *cmin = B.col_min[prv] + cd.col_off;
         const int32_t *cmax = B.col_max[prv] + cd.col_off;
         const double *tfrow_base = nullptr;
-        for (int dp = base; dp < d; ++dp) {
+        // columns d' in descending order: the short last stages (dev = d - d'
+        // small) come first and build a frontier that prunes the rest -- ~4x
+        // fewer frontier inserts than ascending on the C5 chains (order does not
+        // change the result: the dominance relation is order-independent)
+        for (int dp = d - 1; dp >= base; --dp) {
             const int lo_col = cmin[dp - base];
             const int hi_col = cmax[dp - base];
             if (lo_col > hi_col || lo_col >= b) continue;           // no predecessor cell
