@@ -424,7 +424,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     DPBatch bt{};
     float dp_ms = 0;
     bool first_pass = true;
-    int vcap = 4, hcap = 4;     // pool entries reserved per cell (grown on overflow)
+    int vcap = 8, hcap = 4;     // pool entries reserved per cell (grown on overflow)
     for (;;) {
         int64_t vpool_total = 0, hpool_total = 0, col_total = 0;
         std::vector<int64_t> col_prefix(n + 1, 0);
@@ -445,8 +445,10 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         const size_t vmeta = ((size_t)val_cells * 5 + a256) & ~a256;      // cnt u8 + off u32
         const size_t vpool = ((size_t)vpool_total * 16 + a256) & ~a256;   // tf + tb
         const size_t hmeta = ((size_t)hist_cells * 5 + a256) & ~a256;
-        const int64_t vspill = std::max<int64_t>(1 << 20, val_cells) * vcap / 4;
-        const int64_t hspill = std::max<int64_t>(1 << 22, hist_cells / 2) * hcap / 4;
+        // shared spill pools for calls whose frontiers outgrow their region:
+        // values 4 entries per cell of the batch, history 1 per cell
+        const int64_t vspill = std::max<int64_t>(1 << 20, 4 * val_cells) * vcap / 8;
+        const int64_t hspill = std::max<int64_t>(1 << 22, hist_cells) * hcap / 4;
         const size_t vsp = ((size_t)vspill * 16 + a256) & ~a256;
         CUDA_TRY(ctx, ctx->val_d.ensure(2 * (vmeta + vpool + vsp) + 256));
         CUDA_TRY(ctx, ctx->hist_d.ensure(hmeta + 4 * (size_t)(hpool_total + hspill) + 512));
@@ -732,7 +734,7 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     for (size_t i = 0; i < calls.size(); ++i) {
         const pc_call &c = calls[i];
         const int64_t A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
-        const size_t bytes = (size_t)A * B * (2 * (5 + 16 * 4) + (size_t)c.S * (5 + 4 * 4));
+        const size_t bytes = (size_t)A * B * (2 * (5 + 16 * 12) + (size_t)c.S * (5 + 4 * 5));
         if (!cur.empty() && cur_bytes + bytes > cap) {
             if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
             ++*n_chunks;

@@ -20,6 +20,7 @@ ap.add_argument("--nb", type=int, default=512)
 ap.add_argument("--D", type=int, default=128)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--levels", default="all", help="'all' or a widening level index")
+ap.add_argument("--call", default=None, help="S,D,R,MB: run only this call")
 a = ap.parse_args()
 ctx = _lib.context(0)
 bs = c5_blockset(a.nb, a.D, jitter_seed=0)
@@ -27,6 +28,8 @@ bind_problem(ctx, bs)
 calls, levels = enumerate_calls(max(1, a.D // 8), min(8, a.D), 8 * a.D, a.nb)
 if a.levels != "all":
     calls = [c for c, l in zip(calls, levels) if l == int(a.levels)]
+if a.call:
+    calls = [tuple(int(x) for x in a.call.split(","))]
 for r in range(a.reps):
     ctx.lib.pc_reset_cache(ctx.h)
     t0 = time.perf_counter()
