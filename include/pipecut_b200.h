@@ -57,6 +57,8 @@ typedef struct pc_problem {
     const double  *task_flops;  /* [n_tasks] flops_per_sample (costs.py:137) */
     const int64_t *task_fp_fix; /* [n_tasks] produced + span-independent preds */
     const int64_t *task_fp_ps;  /* [n_tasks] per-sample part */
+    const int64_t *task_prod_fix; /* [n_tasks] produced bytes alone (cost tables replace it) */
+    const int64_t *task_prod_ps;
     const int32_t *task_dep_off;/* [n_tasks+1] CSR: preds owned in block dep_ob */
     const int32_t *dep_ob;      /*   count in the footprint iff dep_ob >= lo  */
     const int64_t *dep_fix;
@@ -82,6 +84,8 @@ typedef struct pc_problem {
     int32_t num_nodes;
     int32_t devices_per_node;
     int32_t monotone;           /* task_block non-decreasing: incremental folds */
+    int32_t has_cost_table;     /* CostModelConfig.cost_table set: every microbatch share
+                                   used must be resolved by pc_set_overrides */
     int64_t mem_budget;
     double bw_intra;
     double bw_inter;
@@ -117,6 +121,10 @@ typedef struct pc_atoms {
     const int64_t *tr_size;
     const int32_t *tr_cons_off, *tr_cons;        /* foreign consumer atoms */
     const int32_t *atom_tr_off, *atom_tr;        /* traffic entries touching each atom */
+    const int64_t *task_prod1;  /* [n_tasks] produced bytes alone at m=1 */
+    const uint8_t *ov_has;      /* [n_tasks] or NULL: cost-table entry at m=1 (costs.py:130-148) */
+    const double  *ov_tf, *ov_tb;               /* ov_tb NaN: bwd_fwd_ratio * ov_tf */
+    const int64_t *ov_act;                      /* -1: keep the produced bytes */
     int64_t budget;             /* ClusterSpec.device_memory_bytes */
     double flops_per_sec, bwd_fwd_ratio, grad_factor, opt_factor;
 } pc_atoms;
@@ -173,6 +181,14 @@ int  pc_device_info(pc_ctx *ctx, int32_t *sm_count, int32_t *cc_major, int32_t *
 
 /* ---- problem ------------------------------------------------------------ */
 int pc_set_problem(pc_ctx *ctx, const pc_problem *p);
+
+/* Measured cost-table overrides (costs.py:130-148) resolved on the host for
+ * n_m microbatch shares m_values[i]: for task t (sorted-id order) with
+ * has[i*n_tasks + t] != 0, t_fwd = tf[...], t_bwd = tb[...] (NaN: bwd_fwd_ratio
+ * * t_fwd) and, when act[...] >= 0, produced bytes = act[...].  Replaces the
+ * previous set; drops cached span tables. */
+int pc_set_overrides(pc_ctx *ctx, int32_t n_m, const int64_t *m_values, const uint8_t *has,
+                     const double *tf, const double *tb, const int64_t *act);
 
 /* CostModel.profile over block spans: n queries (lo, hi, m, ckpt). */
 int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const int32_t *hi,

@@ -34,8 +34,9 @@ def build() -> str:
 def load():
     global _lib
     if _lib is None:
-        src = os.path.join(_HERE, "pipecut_oracle.c")
-        if not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(src):
+        deps = [os.path.join(_HERE, "pipecut_oracle.c"),
+                os.path.join(os.path.dirname(_HERE), "include", "pipecut_b200.h")]
+        if not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(d) for d in deps):
             build()
         lib = C.CDLL(_LIB)
         lib.orc_span_record.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int,

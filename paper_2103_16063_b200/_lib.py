@@ -65,6 +65,8 @@ def load():
         lib.pc_partition_blocks.argtypes = [C.c_void_p, P(abi.PcAtoms), C.c_int32, P(C.c_int32),
                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_void_p, C.c_void_p]
+        lib.pc_set_overrides.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p]
         lib.pc_reset_cache.argtypes = [C.c_void_p]
         lib.pc_timer_start.argtypes = [C.c_void_p]
         lib.pc_timer_stop.argtypes = [C.c_void_p, P(C.c_double)]
@@ -72,7 +74,7 @@ def load():
         for name in ("pc_ctx_create", "pc_device_info", "pc_set_problem", "pc_profile_spans",
                      "pc_form_stage_dp", "pc_run_calls", "pc_last_crossing", "pc_form_stage",
                      "pc_reset_cache", "pc_timer_start", "pc_timer_stop",
-                     "pc_measure_fp64_peak", "pc_partition_blocks"):
+                     "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
         return lib
@@ -81,7 +83,7 @@ def load():
 EXPORTS = ("pc_ctx_create", "pc_ctx_destroy", "pc_last_error", "pc_device_info",
            "pc_set_problem", "pc_profile_spans", "pc_form_stage_dp", "pc_run_calls",
            "pc_last_crossing", "pc_form_stage", "pc_reset_cache", "pc_timer_start",
-           "pc_timer_stop", "pc_measure_fp64_peak", "pc_partition_blocks")
+           "pc_timer_stop", "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides")
 
 
 class Context:
@@ -98,6 +100,7 @@ class Context:
         self.device = device
         self.problem_owner = None   # weakref to the BlockSet currently uploaded
         self.problem_flat = None
+        self.problem_shares = frozenset()   # cost-table shares resolved on device
 
     def error(self) -> str:
         return self.lib.pc_last_error(self.h).decode(errors="replace")

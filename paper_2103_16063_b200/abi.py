@@ -28,6 +28,8 @@ class PcProblem(C.Structure):
         ("task_flops", _f64p),
         ("task_fp_fix", _i64p),
         ("task_fp_ps", _i64p),
+        ("task_prod_fix", _i64p),
+        ("task_prod_ps", _i64p),
         ("task_dep_off", _i32p),
         ("dep_ob", _i32p),
         ("dep_fix", _i64p),
@@ -51,6 +53,7 @@ class PcProblem(C.Structure):
         ("num_nodes", C.c_int32),
         ("devices_per_node", C.c_int32),
         ("monotone", C.c_int32),
+        ("has_cost_table", C.c_int32),
         ("mem_budget", C.c_int64),
         ("bw_intra", C.c_double),
         ("bw_inter", C.c_double),
@@ -71,6 +74,8 @@ class PcAtoms(C.Structure):
         ("nbr_off", _i32p), ("nbr", _i32p),
         ("tr_owner", _i32p), ("tr_size", _i64p), ("tr_cons_off", _i32p), ("tr_cons", _i32p),
         ("atom_tr_off", _i32p), ("atom_tr", _i32p),
+        ("task_prod1", _i64p),
+        ("ov_has", C.POINTER(C.c_uint8)), ("ov_tf", _f64p), ("ov_tb", _f64p), ("ov_act", _i64p),
         ("budget", C.c_int64),
         ("flops_per_sec", C.c_double), ("bwd_fwd_ratio", C.c_double),
         ("grad_factor", C.c_double), ("opt_factor", C.c_double),
@@ -84,7 +89,7 @@ def atoms_struct(fa) -> PcAtoms:
     s.n_in = int(fa.in_owner.shape[0])
     s.n_traffic = int(fa.tr_owner.shape[0])
     ctypes_of = {np.dtype(np.int32): C.c_int32, np.dtype(np.int64): C.c_int64,
-                 np.dtype(np.float64): C.c_double}
+                 np.dtype(np.float64): C.c_double, np.dtype(np.uint8): C.c_uint8}
     for name, _ in PcAtoms._fields_:
         v = getattr(fa, name, None)
         if isinstance(v, np.ndarray):
@@ -154,6 +159,8 @@ def problem_struct(fp) -> PcProblem:
     s.task_flops = _ptr(fp.task_flops, C.c_double)
     s.task_fp_fix = _ptr(fp.task_fp_fix, C.c_int64)
     s.task_fp_ps = _ptr(fp.task_fp_ps, C.c_int64)
+    s.task_prod_fix = _ptr(fp.task_prod_fix, C.c_int64)
+    s.task_prod_ps = _ptr(fp.task_prod_ps, C.c_int64)
     s.task_dep_off = _ptr(fp.task_dep_off, C.c_int32)
     s.dep_ob = _ptr(fp.dep_ob, C.c_int32)
     s.dep_fix = _ptr(fp.dep_fix, C.c_int64)
@@ -177,6 +184,7 @@ def problem_struct(fp) -> PcProblem:
     s.num_nodes = fp.num_nodes
     s.devices_per_node = fp.devices_per_node
     s.monotone = int(fp.monotone)
+    s.has_cost_table = int(fp.has_cost_table)
     s.mem_budget = fp.mem_budget
     s.bw_intra = fp.bw_intra
     s.bw_inter = fp.bw_inter

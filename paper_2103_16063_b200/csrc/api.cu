@@ -128,6 +128,8 @@ extern "C" int pc_set_problem(pc_ctx *ctx, const pc_problem *p) {
     size_t i_tf = add(p->task_flops, 8 * (size_t)T);
     size_t i_ff = add(p->task_fp_fix, 8 * (size_t)T);
     size_t i_fp = add(p->task_fp_ps, 8 * (size_t)T);
+    size_t i_qf = add(p->task_prod_fix, 8 * (size_t)T);
+    size_t i_qp = add(p->task_prod_ps, 8 * (size_t)T);
     size_t i_do = add(p->task_dep_off, 4 * (size_t)(T + 1));
     size_t i_dob = add(p->dep_ob, 4 * (size_t)ndep);
     size_t i_df = add(p->dep_fix, 8 * (size_t)ndep);
@@ -172,6 +174,9 @@ extern "C" int pc_set_problem(pc_ctx *ctx, const pc_problem *p) {
     D.task_flops = (const double *)at(i_tf);
     D.fp_fix = (const int64_t *)at(i_ff);
     D.fp_ps = (const int64_t *)at(i_fp);
+    D.prod_fix = (const int64_t *)at(i_qf);
+    D.prod_ps = (const int64_t *)at(i_qp);
+    D.n_ov = 0;
     D.dep_off = (const int32_t *)at(i_do);
     D.dep_ob = (const int32_t *)at(i_dob);
     D.dep_fix = (const int64_t *)at(i_df);
@@ -206,8 +211,14 @@ extern "C" int pc_set_problem(pc_ctx *ctx, const pc_problem *p) {
         // in the span, which the DP's prefix skip relies on
         bool nonneg = p->flops_per_sec > 0 && p->bwd_fwd_ratio >= 0;
         for (int t = 0; t < T && nonneg; ++t) nonneg = p->task_flops[t] >= 0.0;
+        ctx->mono_flops = nonneg;
         ctx->mono_skip = nonneg;
     }
+    ctx->has_cost_table = p->has_cost_table != 0;
+    ctx->ov_m.clear();
+    ctx->h_task_block.assign(p->task_block, p->task_block + T);
+    ctx->h_prod_fix.assign(p->task_prod_fix, p->task_prod_fix + T);
+    ctx->h_prod_ps.assign(p->task_prod_ps, p->task_prod_ps + T);
     ctx->has_problem = true;
     return PC_OK;
 }
@@ -220,6 +231,10 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
     for (auto &k : want)
         if (!ctx->key_map.count(k)) fresh.push_back(k);
     if (fresh.empty()) return PC_OK;
+    if (ctx->has_cost_table)
+        for (auto &k : fresh)
+            if (std::find(ctx->ov_m.begin(), ctx->ov_m.end(), k.first) == ctx->ov_m.end())
+                return fail(ctx, PC_ERR_INVALID, "cost table: microbatch share not resolved by pc_set_overrides");
     for (int attempt = 0; attempt < 2; ++attempt) {
         const size_t per_key = sizeof(double) * ((ctx->derived ? 1 : 2) * (size_t)tri + 2 * (size_t)(P.nb + 1)) + sizeof(int32_t) * (size_t)(P.nb + 1);
         // bounded cache: drop keys the current batch does not need when the cache
@@ -502,6 +517,21 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.counters = ctx->counters_d.as<unsigned long long>();
         CUDA_TRY(ctx, cudaMemsetAsync(bt.counters, 0, (8 + FMAX) * sizeof(unsigned long long), ctx->st));
         int64_t launches = 0;
+        // the reference's pruning break drops cells only when a cost table can
+        // make memory non-monotone in the share (dp.cu: pruning cut)
+        const bool cut = pruning && ctx->has_cost_table;
+        int64_t *cut_rows = nullptr, *cut_cols = nullptr;
+        int32_t *row_e = nullptr;
+        std::vector<int64_t> row_prefix(n + 1, 0);
+        if (cut) {
+            for (int i = 0; i < n; ++i) row_prefix[i + 1] = row_prefix[i] + cds[i].A;
+            CUDA_TRY(ctx, ctx->cut_d.ensure(16 * (size_t)(n + 1) + 4 * (size_t)row_prefix[n] + 64));
+            cut_rows = ctx->cut_d.as<int64_t>();
+            cut_cols = cut_rows + (n + 1);
+            row_e = (int32_t *)(cut_cols + (n + 1));
+            CUDA_TRY(ctx, cudaMemcpyAsync(cut_rows, row_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
+            CUDA_TRY(ctx, cudaMemcpyAsync(cut_cols, col_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
+        }
         for (int s = 1; s <= maxS; ++s) {
             int n_active = 0;
             while (n_active < n && cds[n_active].S >= s) ++n_active;
@@ -512,6 +542,9 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, ctx->st);
             ++launches;
             ctx->launches++;
+            if (cut)
+                ctx->launches += launch_prune_cut(bt, s, n_active, row_prefix[n_active], col_prefix[n_active],
+                                                  cut_rows, cut_cols, row_e, ctx->st);
         }
         if (int rc = check_launch(ctx, "dp_level")) return rc;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev2, ctx->st));
@@ -1004,9 +1037,12 @@ extern "C" int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const
                                 int64_t *mem) {
     if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
     cudaSetDevice(ctx->device);
-    for (int i = 0; i < n; ++i)
+    for (int i = 0; i < n; ++i) {
         if (lo[i] < 0 || hi[i] <= lo[i] || hi[i] > ctx->nb || m[i] < 0)
             return fail(ctx, PC_ERR_INVALID, "span out of range");
+        if (ctx->has_cost_table && std::find(ctx->ov_m.begin(), ctx->ov_m.end(), m[i]) == ctx->ov_m.end())
+            return fail(ctx, PC_ERR_INVALID, "cost table: microbatch share not resolved by pc_set_overrides");
+    }
     if (n == 0) return PC_OK;
     size_t in_bytes = (8 + 4 * 3) * (size_t)n + 64;
     CUDA_TRY(ctx, ctx->q_d.ensure(in_bytes));
@@ -1063,5 +1099,51 @@ extern "C" int pc_measure_fp64_peak(pc_ctx *ctx, double *gops) {
     cudaSetDevice(ctx->device);
     *gops = measure_fp64_gops(ctx->st, ctx->sm_count);
     if (*gops <= 0) return fail(ctx, PC_ERR_CUDA, "fp64 peak kernel failed");
+    return PC_OK;
+}
+
+extern "C" int pc_set_overrides(pc_ctx *ctx, int32_t n_m, const int64_t *m_values, const uint8_t *has,
+                                const double *tf, const double *tb, const int64_t *act) {
+    if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
+    cudaSetDevice(ctx->device);
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    free_keys(ctx);
+    const int T = ctx->P.n_tasks, nb = ctx->nb;
+    // resident corrections: act_bytes replaces the produced bytes of a task
+    std::vector<int64_t> corr((size_t)n_m * (nb + 1), 0);
+    bool nonneg = ctx->mono_flops;
+    for (int i = 0; i < n_m; ++i) {
+        int64_t *c = corr.data() + (size_t)i * (nb + 1);
+        for (int t = 0; t < T; ++t) {
+            const size_t q = (size_t)i * T + t;
+            if (!has[q]) continue;
+            if (!(tf[q] >= 0.0) || (!std::isnan(tb[q]) && !(tb[q] >= 0.0))) nonneg = false;
+            if (act[q] >= 0)
+                c[ctx->h_task_block[t] + 1] += act[q] - (ctx->h_prod_fix[t] + m_values[i] * ctx->h_prod_ps[t]);
+        }
+        for (int b = 0; b < nb; ++b) c[b + 1] += c[b];
+    }
+    ctx->mono_skip = nonneg;
+    const size_t KT = (size_t)n_m * T;
+    const size_t bytes = 8 * (size_t)n_m + KT + 8 * KT * 3 + 8 * corr.size() + 256;
+    CUDA_TRY(ctx, ctx->ov_d.ensure(bytes));
+    char *base = ctx->ov_d.as<char>();
+    size_t off = 0;
+    auto put = [&](const void *src, size_t nbytes) {
+        void *dst = base + off;
+        if (nbytes) cudaMemcpy(dst, src, nbytes, cudaMemcpyHostToDevice);
+        off = (off + nbytes + 15) & ~size_t(15);
+        return dst;
+    };
+    DevProblem &D = ctx->P;
+    D.ov_m = (const int64_t *)put(m_values, 8 * (size_t)n_m);
+    D.ov_has = (const uint8_t *)put(has, KT);
+    D.ov_tf = (const double *)put(tf, 8 * KT);
+    D.ov_tb = (const double *)put(tb, 8 * KT);
+    D.ov_act = (const int64_t *)put(act, 8 * KT);
+    D.ov_corr = (const int64_t *)put(corr.data(), 8 * corr.size());
+    D.n_ov = n_m;
+    ctx->ov_m.assign(m_values, m_values + n_m);
+    CUDA_TRY(ctx, cudaGetLastError());
     return PC_OK;
 }

@@ -45,7 +45,22 @@ struct DevAtoms {
     const int64_t *tr_size;
     const int32_t *tr_cons_off, *tr_cons;
     const int32_t *atom_tr_off, *atom_tr;
+    const int64_t *task_prod1;
+    const uint8_t *ov_has;          // null without a cost table
+    const double *ov_tf, *ov_tb;
+    const int64_t *ov_act;
 };
+
+// per-task time at m = 1, cost-table entry first (costs.py:130-140)
+__device__ __forceinline__ void atom_task_times(const DevAtoms &A, int t, double &x, double &y) {
+    if (A.ov_has && A.ov_has[t]) {
+        x = A.ov_tf[t];
+        y = isnan(A.ov_tb[t]) ? __dmul_rn(A.beta, x) : A.ov_tb[t];
+    } else {
+        x = __ddiv_rn(__dmul_rn(A.task_flops[t], 1.0), A.flops);
+        y = __dmul_rn(A.beta, x);
+    }
+}
 
 // Group memberships of the coarsening levels: grp[l*n + x] = group of atom x
 // at level l; CSR goff[l*(n+1) + g] / gat[l*n + j] lists each group's atoms
@@ -111,6 +126,7 @@ __device__ int64_t set_mem(const DevAtoms &A, const DevLevels &L, const SetDesc 
         for (int q = A.atom_task_off[x]; q < A.atom_task_off[x + 1]; ++q) {
             const int t = A.atom_tasks[q];
             int64_t fp = A.task_fp1[t];
+            if (A.ov_has && A.ov_has[t] && A.ov_act[t] >= 0) fp += A.ov_act[t] - A.task_prod1[t];
             for (int d = A.dep_off[t]; d < A.dep_off[t + 1]; ++d)
                 if (in_set(L, s, A.dep_owner[d])) fp += A.dep_size[d];
             mfp = fp > mfp ? fp : mfp;
@@ -206,17 +222,19 @@ __global__ void k_group_profiles(DevAtoms A, DevLevels L, int level, int ngroups
         const int x = L.gat[(int64_t)level * L.n + L.goff[(int64_t)level * (L.n + 1) + g]];
         for (int q = A.atom_task_off[x]; q < A.atom_task_off[x + 1]; ++q) {
             const int t = A.atom_tasks[q];
-            const double v = __ddiv_rn(__dmul_rn(A.task_flops[t], 1.0), A.flops);
+            double v, w;
+            atom_task_times(A, t, v, w);
             tf = __dadd_rn(tf, v);
-            tb = __dadd_rn(tb, __dmul_rn(A.beta, v));
+            tb = __dadd_rn(tb, w);
         }
     } else {
         const int32_t *grp = L.grp + (int64_t)level * L.n;
         for (int t = 0; t < A.T; ++t) {
             if (grp[A.task_atom[t]] != g) continue;
-            const double v = __ddiv_rn(__dmul_rn(A.task_flops[t], 1.0), A.flops);
+            double v, w;
+            atom_task_times(A, t, v, w);
             tf = __dadd_rn(tf, v);
-            tb = __dadd_rn(tb, __dmul_rn(A.beta, v));
+            tb = __dadd_rn(tb, w);
         }
     }
     out_tf[g] = tf;
@@ -306,6 +324,10 @@ struct Coarsener {
         size_t i15 = add(H->pred_off, 4 * (N + 1)), i16 = add(H->pred, 4 * np), i17 = add(H->tr_owner, 4 * E);
         size_t i18 = add(H->tr_size, 8 * E), i19 = add(H->tr_cons_off, 4 * (E + 1)), i20 = add(H->tr_cons, 4 * nc);
         size_t i21 = add(H->atom_tr_off, 4 * (N + 1)), i22 = add(H->atom_tr, 4 * ntr);
+        size_t i23 = add(H->task_prod1, 8 * T);
+        const bool ov = H->ov_has != nullptr;
+        size_t i24 = ov ? add(H->ov_has, T) : 0, i25 = ov ? add(H->ov_tf, 8 * T) : 0;
+        size_t i26 = ov ? add(H->ov_tb, 8 * T) : 0, i27 = ov ? add(H->ov_act, 8 * T) : 0;
         CUDA_TRY(ctx, atoms_d.ensure(total + 64));
         std::vector<char> staging(total + 64, 0);
         for (auto &p : parts)
@@ -344,6 +366,11 @@ struct Coarsener {
         A.tr_cons = (const int32_t *)at(i20);
         A.atom_tr_off = (const int32_t *)at(i21);
         A.atom_tr = (const int32_t *)at(i22);
+        A.task_prod1 = (const int64_t *)at(i23);
+        A.ov_has = ov ? (const uint8_t *)at(i24) : nullptr;
+        A.ov_tf = ov ? (const double *)at(i25) : nullptr;
+        A.ov_tb = ov ? (const double *)at(i26) : nullptr;
+        A.ov_act = ov ? (const int64_t *)at(i27) : nullptr;
         return PC_OK;
     }
 

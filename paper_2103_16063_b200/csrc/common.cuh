@@ -30,6 +30,7 @@ struct DevProblem {
     const int32_t *task_block = nullptr;
     const double *task_flops = nullptr;
     const int64_t *fp_fix = nullptr, *fp_ps = nullptr;
+    const int64_t *prod_fix = nullptr, *prod_ps = nullptr;   // produced bytes alone
     const int32_t *dep_off = nullptr, *dep_ob = nullptr;
     const int64_t *dep_fix = nullptr, *dep_ps = nullptr;
     // block -> task CSR (task indices ascending)
@@ -44,7 +45,49 @@ struct DevProblem {
     const double *cut_ps = nullptr;
     // span input tables, triangular [tri(nb)]
     const int64_t *in_tab_fix = nullptr, *in_tab_ps = nullptr;
+    // measured cost-table overrides (costs.py:130-148), per resolved share m
+    int n_ov = 0;
+    const int64_t *ov_m = nullptr;       // [n_ov]
+    const uint8_t *ov_has = nullptr;     // [n_ov][n_tasks]
+    const double *ov_tf = nullptr, *ov_tb = nullptr;
+    const int64_t *ov_act = nullptr;
+    const int64_t *ov_corr = nullptr;    // [n_ov][nb+1] prefix of resident corrections
 };
+
+__device__ inline int ov_index(const DevProblem &p, int64_t m) {
+    for (int i = 0; i < p.n_ov; ++i)
+        if (p.ov_m[i] == m) return i;
+    return -1;
+}
+
+// per-task forward/backward time at share m (costs.py:130-140)
+__device__ inline void task_times(const DevProblem &p, int ov, int t, double md, double &x, double &y) {
+    if (ov >= 0 && p.ov_has[(int64_t)ov * p.n_tasks + t]) {
+        x = p.ov_tf[(int64_t)ov * p.n_tasks + t];
+        const double b = p.ov_tb[(int64_t)ov * p.n_tasks + t];
+        y = isnan(b) ? __dmul_rn(p.beta, x) : b;
+    } else {
+        x = __ddiv_rn(__dmul_rn(p.task_flops[t], md), p.flops);
+        y = __dmul_rn(p.beta, x);
+    }
+}
+
+// base footprint of a task (produced + span-independent preds), with the
+// cost table's act_bytes replacing the produced bytes (costs.py:147-148)
+__device__ inline int64_t task_fp(const DevProblem &p, int ov, int t, int64_t m) {
+    int64_t fp = p.fp_fix[t] + m * p.fp_ps[t];
+    if (ov >= 0 && p.ov_has[(int64_t)ov * p.n_tasks + t]) {
+        const int64_t a = p.ov_act[(int64_t)ov * p.n_tasks + t];
+        if (a >= 0) fp += a - (p.prod_fix[t] + m * p.prod_ps[t]);
+    }
+    return fp;
+}
+
+__device__ inline int64_t res_corr(const DevProblem &p, int ov, int lo, int hi) {
+    if (ov < 0) return 0;
+    const int64_t *c = p.ov_corr + (int64_t)ov * (p.nb + 1);
+    return c[hi] - c[lo];
+}
 
 // Triangular span index, rows by lo with hi contiguous:
 // row lo holds hi = lo+1 .. nb.
@@ -173,6 +216,11 @@ void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const
                             int64_t *mem, cudaStream_t st);
 // dp.cu
 void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool derived,
+                     cudaStream_t st);
+// cost tables: the reference's pruning break applied to the level's cells;
+// returns the number of kernels launched
+int launch_prune_cut(const DPBatch &b, int s, int n_active, int64_t n_rows, int64_t n_cols,
+                     const int64_t *row_prefix, const int64_t *col_prefix, int32_t *row_e,
                      cudaStream_t st);
 void launch_row_visits(const DPBatch &b, int pruning, int64_t *level_sums, int64_t *row_sums,
                        const int64_t *level_row_off, int64_t n_rows_total, cudaStream_t st);

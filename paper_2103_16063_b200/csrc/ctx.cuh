@@ -71,6 +71,12 @@ struct pc_ctx {
     size_t key_bytes = 0;
     bool derived = false;    // t_bwd derived as beta * t_fwd (beta a power of two)
     bool mono_skip = false;  // span times monotone (non-negative flops): DP prefix skip
+    bool mono_flops = false; // the flops part of mono_skip
+    bool has_cost_table = false;
+    std::vector<int32_t> h_task_block;
+    std::vector<int64_t> h_prod_fix, h_prod_ps;
+    std::vector<int64_t> ov_m;           // resolved shares (host copy)
+    DBuf ov_d;
     DBuf mismatch_d;
     // batch scratch
     DBuf calls_d, warp_prefix_d, keyidx_d, val_d, hist_d, overflow_d;
@@ -78,6 +84,7 @@ struct pc_ctx {
     DBuf plan_off_d, seg_d, objective_d, feasible_d;
     DBuf q_d, q_out_d, sim_d;
     DBuf raw_d, keys_m_d, keys_ckpt_d, colb_d;
+    DBuf cut_d;      // pruning cut (cost tables): row/column prefixes, row_e
     // last batch (for budget crossing queries)
     std::vector<CallDesc> last_calls;   // sorted order
     std::vector<int> last_pos;          // orig -> sorted position

@@ -475,6 +475,106 @@ void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool
         k_dp_level<false><<<blocks, tpb, 0, st>>>(b, s, n_active);
 }
 
+// ---------------------------------------------------------------- pruning cut
+// With pruning the reference ends a row (s, b) at its first empty cell that
+// saw no zero-share candidate, scanning d down, and the cells below are never
+// created (stages.py:244-251); at level 1 the floor d_min = d + 1 also holds
+// for every later row.  Memory growing with the share makes those cells empty
+// anyway, so the DP computes whole rows; measured cost tables break that
+// (an act_bytes entry can make a larger share fit where a smaller one did
+// not), and then the level is cut here before the next one reads it:
+//   k_cut_rows   e(row) = largest di that ends the row (-1: none)
+//   k_cut_level1 e(row) = prefix max of e over the call's rows (the carried d_min)
+//   k_cut_cols   cells di <= e(row) lose their entries (count 0, zero-share
+//                flag kept so the visit scan sees the reference's rows), and the
+//                per-column non-empty b range the next level reads is rebuilt.
+__device__ __forceinline__ int call_of(const int64_t *prefix, int n, int64_t x) {
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (prefix[mid] <= x) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_cut_rows(DPBatch Bt, int s, int n_active, const int64_t *row_prefix,
+                           int32_t *row_e) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= row_prefix[n_active]) return;
+    const int c = call_of(row_prefix, n_active, r);
+    const CallDesc cd = Bt.calls[c];
+    const int bi = (int)(r - row_prefix[c]);
+    const uint8_t *cell = Bt.val_cnt[s & 1] + cd.val_off + bi;
+    int e = -1;
+    for (int di = cd.B - 1; di >= 0; --di) {
+        const uint8_t v = cell[(int64_t)di * cd.A];
+        if ((v & CNT_MASK) == 0 && !(v & CNT_ZERO)) {
+            e = di;
+            break;
+        }
+    }
+    row_e[r] = e;
+}
+
+__global__ void k_cut_level1(DPBatch Bt, int n_active, const int64_t *row_prefix, int32_t *row_e) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_active) return;
+    int32_t *e = row_e + row_prefix[c];
+    int run = -1;
+    for (int bi = 0; bi < Bt.calls[c].A; ++bi) {
+        run = max(run, e[bi]);
+        e[bi] = run;
+    }
+}
+
+__global__ void k_cut_cols(DPBatch Bt, int s, int n_active, const int64_t *col_prefix,
+                           const int64_t *row_prefix, const int32_t *row_e) {
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= col_prefix[n_active]) return;
+    const int c = call_of(col_prefix, n_active, g);
+    const CallDesc cd = Bt.calls[c];
+    const int di = (int)(g - col_prefix[c]);
+    const int cur = s & 1;
+    uint8_t *vcol = Bt.val_cnt[cur] + cd.val_off + (int64_t)di * cd.A;
+    uint8_t *hcol = Bt.hist_cnt + cd.hist_off + (int64_t)(s - 1) * cd.A * cd.B + (int64_t)di * cd.A;
+    const int32_t *e = row_e + row_prefix[c];
+    int mn = 0x7f7f7f7f, mx = -1;
+    for (int bi = lane; bi < cd.A; bi += 32) {
+        uint8_t v = vcol[bi];
+        if ((v & CNT_MASK) == 0) continue;
+        if (di <= e[bi]) {
+            v &= (uint8_t)CNT_ZERO;
+            vcol[bi] = v;
+            hcol[bi] = v;
+            continue;
+        }
+        mn = min(mn, s + bi);
+        mx = max(mx, s + bi);
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) {
+        Bt.col_min[cur][cd.col_off + di] = mn;
+        Bt.col_max[cur][cd.col_off + di] = mx;
+    }
+}
+
+int launch_prune_cut(const DPBatch &b, int s, int n_active, int64_t n_rows, int64_t n_cols,
+                     const int64_t *row_prefix, const int64_t *col_prefix, int32_t *row_e,
+                     cudaStream_t st) {
+    if (n_rows <= 0) return 0;
+    k_cut_rows<<<(unsigned)((n_rows + 127) / 128), 128, 0, st>>>(b, s, n_active, row_prefix, row_e);
+    int launches = 1;
+    if (s == 1) {
+        k_cut_level1<<<(n_active + 127) / 128, 128, 0, st>>>(b, n_active, row_prefix, row_e);
+        ++launches;
+    }
+    k_cut_cols<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(b, s, n_active, col_prefix,
+                                                                      row_prefix, row_e);
+    return launches + 1;
+}
+
 // ---------------------------------------------------------------- visits (K7)
 // Pruned SearchStats.visits (stages.py:212-249) from the per-cell flags:
 // a row (s, b) is scanned from d = D-(S-s) down; the first cell that is

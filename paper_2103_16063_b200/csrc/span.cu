@@ -73,12 +73,13 @@ __global__ void k_span_time_general(DevProblem p, int n_keys, const int64_t *key
     if (lo + 1 + chunk * 32 > nb) return;
     const int hi = lo + 1 + chunk * 32 + lane;
     const double m = (double)keys_m[k];
+    const int ov = ov_index(p, keys_m[k]);
     double tf = 0.0, tb = 0.0;
     for (int t = 0; t < p.n_tasks; ++t) {
         const int b = p.task_block[t];
         if (b < lo) continue;
-        const double x = __ddiv_rn(__dmul_rn(p.task_flops[t], m), p.flops);
-        const double y = __dmul_rn(p.beta, x);
+        double x, y;
+        task_times(p, ov, t, m, x, y);
         if (b < hi) {
             tf = __dadd_rn(tf, x);
             tb = __dadd_rn(tb, y);
@@ -134,6 +135,7 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
         cut[(int64_t)i * (nb + 1) + lo] = cut_time_dev(p, lo, m, i);
         if (lo == nb - 1) cut[(int64_t)i * (nb + 1) + nb] = cut_time_dev(p, nb, m, i);
     }
+    const int ov = ov_index(p, m);
     double tf = 0.0, tb = 0.0;
     int64_t run_fp = 0;
     bool bad = false;
@@ -142,13 +144,13 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
         const int blk = hi - 1;
         for (int q = p.blk_off[blk]; q < p.blk_off[blk + 1]; ++q) {
             const int t = p.blk_tasks[q];
-            int64_t fp = p.fp_fix[t] + m * p.fp_ps[t];
+            int64_t fp = task_fp(p, ov, t, m);
             for (int d = p.dep_off[t]; d < p.dep_off[t + 1]; ++d)
                 if (p.dep_ob[d] >= lo) fp += p.dep_fix[d] + m * p.dep_ps[d];
             run_fp = fp > run_fp ? fp : run_fp;
             if (MONO) {
-                const double x = __ddiv_rn(__dmul_rn(p.task_flops[t], md), p.flops);
-                const double y = __dmul_rn(p.beta, x);
+                double x, y;
+                task_times(p, ov, t, md, x, y);
                 tf = __dadd_rn(tf, x);
                 tb = __dadd_rn(tb, y);
             }
@@ -162,7 +164,7 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
         const int64_t param = p.pre_param[hi] - p.pre_param[lo];
         const int64_t inb = p.in_tab_fix[idx] + m * p.in_tab_ps[idx];
         const int64_t res = (p.pre_res_fix[hi] - p.pre_res_fix[lo]) +
-                            m * (p.pre_res_ps[hi] - p.pre_res_ps[lo]);
+                            m * (p.pre_res_ps[hi] - p.pre_res_ps[lo]) + res_corr(p, ov, lo, hi);
         const int64_t act = inb + (ckpt ? run_fp : res);
         const double memd = __dadd_rn(__dmul_rn((double)param, p.factor), (double)act);
         const int64_t mem = (int64_t)memd;
@@ -172,7 +174,9 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
         // search needs the magnitude, the DP tests signbit for feasibility
         out_f[o] = ok ? f : -f;
         if (derived) {
-            bad |= ok && __dmul_rn(p.beta, f) != b;
+            // every span, feasible or not: the DP's skip search reads
+            // beta * |t_fwd| as t_bwd on infeasible spans too
+            bad |= __dmul_rn(p.beta, f) != b;
         } else {
             out_b[o] = b;
         }
@@ -225,14 +229,15 @@ __global__ void k_profile_queries(DevProblem p, int n, const int32_t *qlo, const
     const int lo = qlo[i], hi = qhi[i];
     const int64_t m = qm[i];
     const double md = (double)m;
+    const int ov = ov_index(p, m);
     double tf = 0.0, tb = 0.0;
     int t0 = 0, t1 = p.n_tasks;
     if (p.monotone) { t0 = p.blk_off[lo]; t1 = p.blk_off[hi]; }
     for (int t = t0; t < t1; ++t) {
         const int b = p.task_block[t];
         if (b < lo || b >= hi) continue;
-        const double x = __ddiv_rn(__dmul_rn(p.task_flops[t], md), p.flops);
-        const double y = __dmul_rn(p.beta, x);
+        double x, y;
+        task_times(p, ov, t, md, x, y);
         tf = __dadd_rn(tf, x);
         tb = __dadd_rn(tb, y);
     }
@@ -240,7 +245,7 @@ __global__ void k_profile_queries(DevProblem p, int n, const int32_t *qlo, const
     for (int blk = lo; blk < hi; ++blk)
         for (int q = p.blk_off[blk]; q < p.blk_off[blk + 1]; ++q) {
             const int t = p.blk_tasks[q];
-            int64_t fp = p.fp_fix[t] + m * p.fp_ps[t];
+            int64_t fp = task_fp(p, ov, t, m);
             for (int d = p.dep_off[t]; d < p.dep_off[t + 1]; ++d)
                 if (p.dep_ob[d] >= lo) fp += p.dep_fix[d] + m * p.dep_ps[d];
             run_fp = fp > run_fp ? fp : run_fp;
@@ -249,7 +254,7 @@ __global__ void k_profile_queries(DevProblem p, int n, const int32_t *qlo, const
     const int64_t param = p.pre_param[hi] - p.pre_param[lo];
     const int64_t inb = p.in_tab_fix[idx] + m * p.in_tab_ps[idx];
     const int64_t res = (p.pre_res_fix[hi] - p.pre_res_fix[lo]) +
-                        m * (p.pre_res_ps[hi] - p.pre_res_ps[lo]);
+                        m * (p.pre_res_ps[hi] - p.pre_res_ps[lo]) + res_corr(p, ov, lo, hi);
     const int64_t act = inb + (qckpt[i] ? run_fp : res);
     const double memd = __dadd_rn(__dmul_rn((double)param, p.factor), (double)act);
     otf[i] = tf;

@@ -63,6 +63,8 @@ class FlatProblem:
     task_flops: np.ndarray      # float64 [T]
     task_fp_fix: np.ndarray     # int64 [T] produced + span-independent preds (fixed)
     task_fp_ps: np.ndarray      # int64 [T] ... per sample
+    task_prod_fix: np.ndarray   # int64 [T] produced bytes alone (cost-table act_bytes replaces it)
+    task_prod_ps: np.ndarray    # int64 [T]
     task_dep_off: np.ndarray    # int32 [T+1] CSR of span-dependent preds
     dep_ob: np.ndarray          # int32 owner block of the pred value
     dep_fix: np.ndarray         # int64
@@ -94,6 +96,9 @@ class FlatProblem:
     bw_inter: float
     latency: float
     monotone: bool              # task_block non-decreasing along sorted ids
+    has_cost_table: bool = False
+    task_nodes: list = field(default_factory=list, repr=False)   # TaskInfo per task
+    cost_config: object = field(default=None, repr=False)        # CostConfig (cost table)
     keepalive: list = field(default_factory=list, repr=False)
 
     @property
@@ -127,9 +132,6 @@ def atom_node_tables(partition):
 def flatten_blockset(bs) -> FlatProblem:
     model = bs.model
     cfg = model.config
-    if cfg.cost_table is not None:
-        raise UnsupportedGraph("measured cost tables are not supported by the "
-                               "device span-cost kernel yet (SURVEY.md §8f)")
     cl = model.cluster
     g = model.graph
     part = bs.partition
@@ -181,8 +183,9 @@ def flatten_blockset(bs) -> FlatProblem:
     blk_param = [0] * nb
     blk_res_fix = [0] * nb
     blk_res_ps = [0] * nb
-    task_block, task_flops = [], []
+    task_block, task_flops, task_nodes = [], [], []
     fp_fix, fp_ps, dep_off, dep_ob, dep_fix, dep_ps = [], [], [0], [], [], []
+    prod_fix, prod_ps = [], []
     for nid, node in g.nodes.items():  # sorted id order (graph.py:90-93)
         b = blk_of_node(nid)
         if b < 0:
@@ -237,8 +240,11 @@ def flatten_blockset(bs) -> FlatProblem:
             dep_ps.append(vp)
         task_block.append(b)
         task_flops.append(float(task.flops_per_sample))
+        task_nodes.append(task)
         fp_fix.append(bf)
         fp_ps.append(bp)
+        prod_fix.append(pf)
+        prod_ps.append(pp)
         dep_off.append(len(dep_ob))
 
     tb = _i32(task_block)
@@ -249,6 +255,7 @@ def flatten_blockset(bs) -> FlatProblem:
         nb=nb,
         task_block=tb, task_flops=_f64(task_flops),
         task_fp_fix=_i64(fp_fix), task_fp_ps=_i64(fp_ps),
+        task_prod_fix=_i64(prod_fix), task_prod_ps=_i64(prod_ps),
         task_dep_off=_i32(dep_off), dep_ob=_i32(dep_ob),
         dep_fix=_i64(dep_fix), dep_ps=_i64(dep_ps),
         in_ob=_i32(in_ob), in_cons_off=_i32(in_off), in_cons=_i32(in_cons),
@@ -266,6 +273,9 @@ def flatten_blockset(bs) -> FlatProblem:
         bw_intra=float(cl.bw_intra), bw_inter=float(cl.bw_inter),
         latency=float(cl.link_latency_sec),
         monotone=monotone,
+        has_cost_table=cfg.cost_table is not None,
+        task_nodes=task_nodes,
+        cost_config=cfg,
     )
 
 
@@ -289,6 +299,7 @@ class FlatAtoms:
     task_atom: np.ndarray       # int32 [T] sorted node-id order
     task_flops: np.ndarray      # float64 [T]
     task_fp1: np.ndarray        # int64 [T] produced + always-counted preds, at m=1
+    task_prod1: np.ndarray      # int64 [T] produced bytes alone at m=1
     dep_off: np.ndarray         # int32 [T+1]
     dep_owner: np.ndarray       # int32 owner atom of an anchor input pred
     dep_size: np.ndarray        # int64 size at m=1
@@ -317,6 +328,10 @@ class FlatAtoms:
     bwd_fwd_ratio: float
     factor_g: float
     factor_o: float
+    ov_has: np.ndarray = None   # uint8 [T] cost-table entry at m=1 (costs.py:130-148)
+    ov_tf: np.ndarray = None    # float64 [T]
+    ov_tb: np.ndarray = None    # float64 [T], NaN: bwd_fwd_ratio * t_fwd
+    ov_act: np.ndarray = None   # int64 [T], -1: keep produced bytes
 
 
 def _csr(lists):
@@ -365,9 +380,6 @@ def flatten_atoms(partition, model) -> FlatAtoms:
 
 def _flatten_atoms(partition, model) -> FlatAtoms:
     cfg = model.config
-    if cfg.cost_table is not None:
-        raise UnsupportedGraph("measured cost tables are not supported by the "
-                               "device span-cost kernel yet (SURVEY.md §8f)")
     g = model.graph
     pg = partition.graph
     n = len(partition.atoms)
@@ -395,7 +407,7 @@ def _flatten_atoms(partition, model) -> FlatAtoms:
         in_atoms.append(sorted(listing[v]))
 
     atom_param = [0] * n
-    task_atom, task_flops, task_fp1, deps = [], [], [], []
+    task_atom, task_flops, task_fp1, deps, task_prod1, tnodes = [], [], [], [], [], []
     atom_tasks = [[] for _ in range(n)]
     for nid, node in g.nodes.items():           # sorted id order (graph.py:90-93)
         a = atom_of.get(nid)
@@ -410,6 +422,8 @@ def _flatten_atoms(partition, model) -> FlatAtoms:
             info = g.nodes[vid].value
             if info is not None and not info.is_param:
                 fp += size1(info, vid)
+        task_prod1.append(fp)
+        tnodes.append(node.task)
         dl = []
         for vid in g.pred(nid):
             info = g.nodes[vid].value
@@ -462,9 +476,12 @@ def _flatten_atoms(partition, model) -> FlatAtoms:
     n_off, nn = _csr(nbr)
     tc_off, tc = _csr(tr_cons)
     atr_off, atr = _csr(atom_tr)
+    ov = resolve_overrides(cfg, tnodes, [1]) if cfg.cost_table is not None else None
     return FlatAtoms(
         n=n, atom_param=_i64(atom_param), task_atom=_i32(task_atom),
-        task_flops=_f64(task_flops), task_fp1=_i64(task_fp1),
+        task_flops=_f64(task_flops), task_fp1=_i64(task_fp1), task_prod1=_i64(task_prod1),
+        ov_has=None if ov is None else ov[1][0], ov_tf=None if ov is None else ov[2][0],
+        ov_tb=None if ov is None else ov[3][0], ov_act=None if ov is None else ov[4][0],
         dep_off=d_off, dep_owner=d_flat, dep_size=_i64(ds),
         atom_task_off=at_off, atom_tasks=at, atom_in_off=ai_off, atom_in=ai,
         in_owner=_i32(in_owner), in_size=_i64(in_size), in_atoms_off=ia_off, in_atoms=ia,
@@ -475,3 +492,40 @@ def _flatten_atoms(partition, model) -> FlatAtoms:
         flops_per_sec=float(cfg.device_flops_per_sec), bwd_fwd_ratio=float(cfg.bwd_fwd_ratio),
         factor_g=float(cfg.grad_factor), factor_o=float(cfg.optimizer_state_factor),
     )
+
+
+# --------------------------------------------------------------------------- cost tables
+def _sig_prefixes(tasks):
+    """op_signature(task, m) = prefix + str(m) (costs.py:51-54), prefix per task."""
+    out = []
+    for task in tasks:
+        attrs = ",".join(f"{k}={task.attrs[k]}" for k in sorted(task.attrs))
+        out.append(f"{task.op}|{attrs}|mb=")
+    return out
+
+
+def resolve_overrides(cfg, tasks, m_values):
+    """Measured cost-table entries per (m, task) (costs.py:130-148), dense:
+    (m array, has[K,T] u8, tf[K,T], tb[K,T] NaN = ratio*tf, act[K,T] -1 = keep)."""
+    table = cfg.cost_table
+    ms = sorted({int(m) for m in m_values})
+    T = len(tasks)
+    has = np.zeros((len(ms), T), np.uint8)
+    tf = np.zeros((len(ms), T), np.float64)
+    tb = np.full((len(ms), T), np.nan, np.float64)
+    act = np.full((len(ms), T), -1, np.int64)
+    if table:
+        pre = _sig_prefixes(tasks)
+        for i, m in enumerate(ms):
+            suffix = str(m)
+            for t, p in enumerate(pre):
+                e = table.get(p + suffix)
+                if e is None:
+                    continue
+                has[i, t] = 1
+                tf[i, t] = float(e.t_fwd)
+                if e.t_bwd is not None:
+                    tb[i, t] = float(e.t_bwd)
+                if e.act_bytes is not None:
+                    act[i, t] = _as_int(e.act_bytes, "act_bytes")
+    return _i64(ms), has, tf, tb, act

@@ -26,7 +26,7 @@ import numpy as np
 
 from . import _lib, abi
 from .stages import (InvalidArgs, Plan, SearchBudgetExceeded, SearchOptions, SearchResult,
-                     SearchStats, StagePlan, bind_problem)
+                     SearchStats, StagePlan, bind_overrides, bind_problem, call_shares)
 
 
 def enumerate_calls(num_nodes: int, dpn: int, batch_size: int, nb: int):
@@ -98,6 +98,8 @@ class BatchResult:
 def run_calls(ctx: _lib.Context, calls, batch_size: int, disable_pruning: bool = False,
               want_iteration: bool = True) -> BatchResult:
     n = len(calls)
+    if ctx.problem_flat is not None:
+        bind_overrides(ctx, ctx.problem_flat, call_shares(calls, batch_size))
     arr = (abi.PcCall * max(n, 1))(*[abi.PcCall(*c) for c in calls])
     res = (abi.PcCallResult * max(n, 1))()
     bufs = [abi.PlanBuffers(c[0]) for c in calls]

@@ -15,7 +15,7 @@ import weakref
 
 from . import _lib, abi
 from ._host import pipecut as _pc
-from .flatten import flatten_blockset
+from .flatten import flatten_blockset, resolve_overrides
 
 _stages = _pc.stages
 InvalidArgs = _stages.InvalidArgs
@@ -37,7 +37,36 @@ def bind_problem(ctx: _lib.Context, blocks):
     ctx.check(ctx.lib.pc_set_problem(ctx.h, C.byref(st)), "pc_set_problem")
     ctx.problem_owner = weakref.ref(blocks)
     ctx.problem_flat = flat
+    ctx.problem_shares = frozenset()
     return flat
+
+
+def call_shares(calls, batch_size: int):
+    """Microbatch shares m = batch // (MB * R * devices) the calls' span
+    profiles are taken at (stages.py:201-206)."""
+    out = set()
+    for S, D, R, MB in calls:
+        for dev in range(1, D - S + 2):
+            m = batch_size // (MB * R * dev)
+            if m >= 1:
+                out.add(m)
+    return out
+
+
+def bind_overrides(ctx: _lib.Context, flat, shares) -> None:
+    """Resolve measured cost-table entries (costs.py:130-148) for every share
+    a search will touch; the device profiles take them from there.  Shares
+    accumulate per bound BlockSet so cached span tables survive."""
+    if not flat.has_cost_table:
+        return
+    want = ctx.problem_shares | frozenset(int(m) for m in shares)
+    if want == ctx.problem_shares:
+        return
+    ms, has, tf, tb, act = resolve_overrides(flat.cost_config, flat.task_nodes, want)
+    ctx.check(ctx.lib.pc_set_overrides(ctx.h, len(ms), ms.ctypes.data, has.ctypes.data,
+                                       tf.ctypes.data, tb.ctypes.data, act.ctypes.data),
+              "pc_set_overrides")
+    ctx.problem_shares = want
 
 
 def _check_args(blocks, S, D, batch_size, replica_factor, microbatches):
@@ -74,7 +103,8 @@ def form_stage_dp(blocks, S: int, D: int, batch_size: int, replica_factor: int,
     _check_args(blocks, S, D, batch_size, replica_factor, microbatches)
     opts = options or SearchOptions()
     ctx = _lib.context()
-    bind_problem(ctx, blocks)
+    flat = bind_problem(ctx, blocks)
+    bind_overrides(ctx, flat, call_shares([(S, D, replica_factor, microbatches)], batch_size))
     buf = abi.PlanBuffers(S)
     st = abi.PcStats()
     rc = ctx.lib.pc_form_stage_dp(ctx.h, S, D, batch_size, replica_factor, microbatches,
@@ -100,7 +130,11 @@ def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
         raise InvalidArgs("node count, devices per node and batch size must be at least 1")
     opts = options or SearchOptions()
     ctx = _lib.context()
-    bind_problem(ctx, blocks)
+    flat = bind_problem(ctx, blocks)
+    if flat.has_cost_table:
+        from .search import enumerate_calls
+        calls, _ = enumerate_calls(num_nodes, devices_per_node, batch_size, len(blocks))
+        bind_overrides(ctx, flat, call_shares(calls, batch_size))
     buf = abi.PlanBuffers(max(1, len(blocks)))
     st = abi.PcStats()
     rc = ctx.lib.pc_form_stage(ctx.h, num_nodes, devices_per_node, batch_size,

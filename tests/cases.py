@@ -167,3 +167,67 @@ def blocks_inputs(g, mem=2 ** 40, flops=1e9):
                         bw_intra=50e9, bw_inter=10e9)
     p = pc.build_atomic_subcomponents(g)
     return p, pc.CostModel(p.graph, pc.CostModelConfig(device_flops_per_sec=flops), cl)
+
+
+# ---------------------------------------------------------------- measured cost tables
+TYPED_OPS = (("matmul", {"h": 1024}), ("matmul", {"h": 4096}), ("gelu", {}),
+             ("layernorm", {"eps": 1e-05, "h": 1024}))
+
+
+def typed_chain(rng, n):
+    """Chain whose tasks share a few op signatures, so table entries hit
+    several tasks at once (op_signature, costs.py:51-54)."""
+    nodes, edges, prev = [_val("x", per_sample=rng.choice([0, 16]))], [], "x"
+    for i in range(n):
+        op, attrs = rng.choice(TYPED_OPS)
+        t, v = f"t{i:02d}", f"v{i:02d}"
+        nodes.append(Node(t, task=TaskInfo(op=op, flops_per_sample=round(rng.uniform(0.5, 4.0), 3),
+                                           attrs=dict(attrs))))
+        nodes.append(_val(v, per_sample=rng.choice([0, 64, 256, 1024])))
+        edges += [(prev, t), (t, v)]
+        p = rng.choice([0, 0, 512, 2048])
+        if p:
+            w = f"w{i:02d}"
+            nodes.append(_val(w, fixed=p, param=True))
+            edges.append((w, t))
+        prev = v
+    return TaskGraph(nodes, edges, ["x"], [prev])
+
+
+def random_cost_table(rng, sigs, shares):
+    """Entries for a random subset of (signature, microbatch); t_bwd and
+    act_bytes optional as load_cost_table allows (costs.py:57-80)."""
+    table = {}
+    for op, attrs in sigs:
+        info = TaskInfo(op=op, flops_per_sample=0.0, attrs=dict(attrs))
+        for m in shares:
+            if rng.random() < 0.5:
+                continue
+            tb = None if rng.random() < 0.5 else round(rng.uniform(0.0, 8.0), 4)
+            act = None if rng.random() < 0.5 else rng.choice([0, 7, 300, 4096, 65536])
+            table[pc.costs.op_signature(info, m)] = pc.CostTableEntry(
+                microbatch=m, t_fwd=round(rng.uniform(0.0, 6.0), 4), t_bwd=tb, act_bytes=act)
+    return table
+
+
+def cost_table_instance(rng):
+    """Typed chain + random measured table; one block per atom (stage DP
+    cases) and a coarsened BlockSet (partition_blocks with overrides)."""
+    n = rng.randint(3, 10)
+    g = typed_chain(rng, n)
+    S = rng.randint(1, min(4, n))
+    nodes, dpn = rng.choice([(1, 4), (2, 2), (1, 6)])
+    D = rng.randint(S, nodes * dpn)
+    R = rng.choice([1, 2])
+    MB = rng.choice([1, 2, 4])
+    BS = R * MB * D * rng.randint(1, 3)
+    table = random_cost_table(rng, TYPED_OPS, range(1, BS + 1))
+    ckpt = rng.random() < 0.5
+    budget = rng.choice([2 ** 40, rng.randint(4096, 65536)])
+    k = rng.choice([10 ** 6, rng.randint(1, n)])
+    lat = rng.choice([0.0, 0.01])
+    cl = pc.ClusterSpec(num_nodes=nodes, devices_per_node=dpn, device_memory_bytes=budget,
+                        bw_intra=1e3, bw_inter=5e2, link_latency_sec=lat)
+    part = pc.build_atomic_subcomponents(g)
+    cfg = pc.CostModelConfig(device_flops_per_sec=1.0, checkpointing=ckpt, cost_table=table)
+    return part, pc.CostModel(part.graph, cfg, cl), k, (nodes, dpn, S, D, BS, R, MB)

@@ -23,6 +23,7 @@ assert pipecut.__file__.startswith("/root/reference"), pipecut.__file__
 
 import cases  # noqa: E402
 from plans import result_doc  # noqa: E402
+from paper_2103_16063_b200.search import enumerate_calls  # noqa: E402
 
 pc = pipecut
 
@@ -79,6 +80,46 @@ def chains():
     dump("chains.json", out)
 
 
+def cost_tables():
+    """Measured cost tables (costs.py:43-80, 130-148): partition_blocks, span
+    profiles, form_stage_dp and form_stage with overrides."""
+    out = []
+    rng = random.Random(4242)
+    for i in range(80):
+        part, model, k, (nodes, dpn, S, D, BS, R, MB) = cases.cost_table_instance(rng)
+        rec = {"index": i, "k": k, "args": [nodes, dpn, S, D, BS, R, MB]}
+        try:
+            bs = pc.partition_blocks(part, model, k)
+        except pc.InfeasibleAtom as e:
+            rec["error"] = ["InfeasibleAtom", str(e)]
+            out.append(rec)
+            continue
+        rec["block_atoms"] = [list(g) for g in bs.block_atoms]
+        rec["costs"] = [[c.t_fwd_sec.hex(), c.t_bwd_sec.hex(), c.mem_bytes] for c in bs.costs]
+        nb = len(bs)
+        shares = sorted({BS // (MB * R * d) for d in range(1, D - S + 2)} - {0})
+        spans = {}
+        for m in shares:
+            for lo in range(nb):
+                for hi in range(lo + 1, nb + 1):
+                    for ck in (False, True):
+                        c = bs.model.profile(bs.span(lo, hi), m, checkpointing=ck)
+                        spans[f"{lo},{hi},{m},{int(ck)}"] = [c.t_fwd_sec.hex(), c.t_bwd_sec.hex(),
+                                                             c.mem_bytes]
+        rec["spans"] = spans
+        if S <= nb:
+            for prune in (True, False):
+                res = pc.form_stage_dp(bs, S, D, BS, R, MB,
+                                       pc.SearchOptions(disable_pruning=not prune))
+                rec["dp_pruned" if prune else "dp_unpruned"] = result_doc(res)
+        rec["form_stage"] = result_doc(pc.form_stage(nodes, dpn, BS, bs))
+        calls, _ = enumerate_calls(nodes, dpn, BS, nb)
+        rec["calls"] = [[list(c), result_doc(pc.form_stage_dp(bs, c[0], c[1], BS, c[2], c[3]))]
+                        for c in calls]
+        out.append(rec)
+    dump("cost_tables.json", out)
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["random", "configs", "chains"]
     if "random" in what:
@@ -87,3 +128,5 @@ if __name__ == "__main__":
         chains()
     if "configs" in what:
         configs()
+    if "cost_tables" in what:
+        cost_tables()
