@@ -49,14 +49,10 @@ extern "C" int pc_ctx_create(int device, pc_ctx **out) {
 }
 
 static void free_keys(pc_ctx *ctx) {
-    for (auto &k : ctx->keys) {
-        if (k.tf) cudaFree(k.tf);
-        if (k.tb) cudaFree(k.tb);
-        if (k.cut) cudaFree(k.cut);
-    }
     ctx->keys.clear();
     ctx->key_map.clear();
     ctx->key_bytes = 0;
+    ctx->slot_used.assign(ctx->key_cap, 0);
 }
 
 extern "C" void pc_ctx_destroy(pc_ctx *ctx) {
@@ -236,40 +232,62 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
             if (std::find(ctx->ov_m.begin(), ctx->ov_m.end(), k.first) == ctx->ov_m.end())
                 return fail(ctx, PC_ERR_INVALID, "cost table: microbatch share not resolved by pc_set_overrides");
     for (int attempt = 0; attempt < 2; ++attempt) {
-        const size_t per_key = sizeof(double) * ((ctx->derived ? 1 : 2) * (size_t)tri + 2 * (size_t)(P.nb + 1)) + sizeof(int32_t) * (size_t)(P.nb + 1);
-        // bounded cache: drop keys the current batch does not need when the cache
-        // would outgrow a third of free device memory
-        size_t free_b = 0, total_b = 0;
-        cudaMemGetInfo(&free_b, &total_b);
-        if (ctx->key_bytes + fresh.size() * per_key > (ctx->key_bytes + free_b) / 3) {
+        const size_t raw_key = sizeof(double) * ((ctx->derived ? 1 : 2) * (size_t)tri + 2 * (size_t)(P.nb + 1)) + sizeof(int32_t) * (size_t)(P.nb + 1);
+        const size_t per_key = (raw_key + 255) & ~size_t(255);
+        if (per_key != ctx->key_slot) {          // new layout (nb or derived changed)
+            free_keys(ctx);
+            ctx->key_arena.release();
+            ctx->key_slot = per_key;
+            ctx->key_cap = 0;
+            ctx->slot_used.clear();
+            fresh = want;
+        }
+        if (ctx->keys.size() + fresh.size() > (size_t)ctx->key_cap) {
+            // drop cached keys this batch does not need
             std::map<std::pair<int64_t, int>, int> need;
             for (auto &k : want) need[k] = 1;
             std::vector<CachedKey> kept;
             for (auto &k : ctx->keys) {
-                if (need.count({k.m, k.ckpt})) {
-                    kept.push_back(k);
-                } else {
-                    cudaFree(k.tf);
-                    if (k.tb) cudaFree(k.tb);
-                    cudaFree(k.cut);
-                    ctx->key_bytes -= per_key;
-                }
+                if (need.count({k.m, k.ckpt})) kept.push_back(k);
+                else ctx->slot_used[k.slot] = 0;
             }
             ctx->keys = kept;
             ctx->key_map.clear();
             for (size_t i = 0; i < ctx->keys.size(); ++i)
                 ctx->key_map[{ctx->keys[i].m, ctx->keys[i].ckpt}] = (int)i;
         }
+        if (ctx->keys.size() + fresh.size() > (size_t)ctx->key_cap) {
+            // grow the arena (bounded by a third of device memory) and rebuild
+            // every key of the batch in it
+            size_t free_b = 0, total_b = 0;
+            cudaMemGetInfo(&free_b, &total_b);
+            const size_t limit = (free_b + ctx->key_arena.n) / 3;
+            size_t slots = std::max(want.size(), (size_t)ctx->key_cap * 3 / 2);
+            if (slots * per_key > limit) slots = std::max(want.size(), limit / per_key);
+            free_keys(ctx);
+            ctx->key_arena.release();
+            ctx->key_cap = 0;
+            CUDA_TRY(ctx, ctx->key_arena.ensure(slots * per_key));
+            ctx->key_cap = (int)(ctx->key_arena.n / per_key);
+            ctx->slot_used.assign(ctx->key_cap, 0);
+            fresh = want;
+        }
         const int nf = (int)fresh.size();
         std::vector<int64_t> km(nf);
         std::vector<int32_t> kc(nf);
         std::vector<double *> pf(nf), pb(nf, nullptr), pcut(nf);
+        std::vector<int> slot(nf);
+        int cursor = 0;
         for (int i = 0; i < nf; ++i) {
             km[i] = fresh[i].first;
             kc[i] = fresh[i].second;
-            CUDA_TRY(ctx, cudaMalloc(&pf[i], sizeof(double) * (size_t)tri));
-            if (!ctx->derived) CUDA_TRY(ctx, cudaMalloc(&pb[i], sizeof(double) * (size_t)tri));
-            CUDA_TRY(ctx, cudaMalloc(&pcut[i], sizeof(double) * 2 * (size_t)(P.nb + 1) + sizeof(int32_t) * (size_t)(P.nb + 1)));
+            while (ctx->slot_used[cursor]) ++cursor;     // capacity checked above
+            ctx->slot_used[cursor] = 1;
+            slot[i] = cursor;
+            char *base = ctx->key_arena.as<char>() + (size_t)cursor * per_key;
+            pf[i] = (double *)base;
+            if (!ctx->derived) pb[i] = pf[i] + tri;
+            pcut[i] = pf[i] + (ctx->derived ? 1 : 2) * (size_t)tri;
             ctx->key_bytes += per_key;
         }
         const size_t hdr = (sizeof(int64_t) * nf + sizeof(int32_t) * nf + 15) & ~size_t(15);
@@ -318,6 +336,7 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
             ck.tf = pf[i];
             ck.tb = pb[i];
             ck.cut = pcut[i];
+            ck.slot = slot[i];
             ctx->key_map[{km[i], kc[i]}] = (int)ctx->keys.size();
             ctx->keys.push_back(ck);
         }

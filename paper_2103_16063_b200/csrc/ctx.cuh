@@ -41,7 +41,8 @@ struct CachedKey {
     int ckpt;
     double *tf = nullptr;    // [tri] hi-major, NaN = infeasible
     double *tb = nullptr;    // [tri] or null when derived as beta * tf
-    double *cut = nullptr;   // [2][nb+1]
+    double *cut = nullptr;   // [2][nb+1], then ffb int32 [nb+1]
+    int slot = -1;           // slot in the key arena
 };
 
 }  // namespace pcb
@@ -67,6 +68,10 @@ struct pc_ctx {
     // key cache
     std::vector<CachedKey> keys;
     std::map<std::pair<int64_t, int>, int> key_map;
+    DBuf key_arena;  // fixed-size key slots (grow-only; a reset forgets keys, keeps memory)
+    size_t key_slot = 0;
+    int key_cap = 0;
+    std::vector<char> slot_used;
     DBuf key_ptrs;   // [3][n_keys] device pointers (tf, tb, cut)
     size_t key_bytes = 0;
     bool derived = false;    // t_bwd derived as beta * t_fwd (beta a power of two)

@@ -22,5 +22,7 @@ for world in (1, 2, 4, 8):
         mine = [c for c, o in zip(calls, own) if o == r]
         ctx.lib.pc_reset_cache(ctx.h)
         b = run_calls(ctx, mine, 8 * D)
-        ts.append(round(b.stats.device_ms + b.stats.span_ms))
-    print(world, "per-rank DP+span ms:", ts, flush=True)
+        st = b.stats
+        ts.append(f"{st.device_ms:.0f}+{st.span_ms:.0f}ms/{len(mine)}c/{st.dp_launches}L/"
+                  f"{st.pairs/1e6:.0f}Mp")
+    print(world, "per-rank DP+span:", ts, flush=True)
