@@ -286,7 +286,7 @@ def run_ours(a):
     for _ in range(a.warmup):
         step_resident()
     times = []
-    pairs = cands = dp_ms = launches = dp_launches = 0
+    pairs = cands = dp_ms = span_ms = launches = dp_launches = 0
     with Clocks(local) as clk:
         for _ in range(a.steps):
             times.append(step_resident())
@@ -294,6 +294,7 @@ def run_ours(a):
             pairs += st.pairs
             cands += st.candidates
             dp_ms += st.device_ms
+            span_ms += st.span_ms
             launches += st.kernel_launches
             dp_launches += st.dp_launches
     ms_per_step = sum(times) / len(times)
@@ -320,10 +321,16 @@ def run_ours(a):
     # ---- roofline of the dominant kernel (DP level kernel)
     peak = C.c_double()
     ctx.check(ctx.lib.pc_measure_fp64_peak(ctx.h, C.byref(peak)), "peak")
-    # algorithmic fp64 work: 2 comm adds per feasible (cell, pred) pair
-    # (stages.py:232-237) + per candidate 2 max (stages.py:239) + 2 compares (_pareto)
-    ops = 2.0 * pairs + 4.0 * cands
+    # Algorithmic fp64 work per SURVEY §8(d): 2 + 4*F ops per visit (2 comm
+    # adds, stages.py:232-237, then per predecessor frontier entry 2 max,
+    # stages.py:239, and 2 compares, _pareto) over the step's unpruned visits;
+    # F = mean predecessor frontier size over the feasible pairs (cands/pairs).
+    f_bar = cands / pairs if pairs else 0.0
+    ops = unpruned * a.steps * (2.0 + 4.0 * f_bar)
     achieved = ops / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
+    # what the kernel executes after its exact pruning (corner, window, prefix skip)
+    ops_exec = 2.0 * pairs + 4.0 * cands
+    achieved_exec = ops_exec / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
     traffic = None
     prof = os.path.join(ROOT, "profiles", "dp_level_traffic.json")
     if os.path.exists(prof):
@@ -348,11 +355,19 @@ def run_ours(a):
                 "h2d_bytes_per_step": int(tim.get("h2d_bytes", 0)),
                 "d2h_bytes_per_step": int(tim.get("d2h_bytes", 0)) + plan_bytes},
         "gpu_launches": int(launches // max(1, a.steps)),
+        "breakdown_ms": {"dp_levels": dp_ms / a.steps, "span_tables": span_ms / a.steps,
+                         "rest": ms_per_step - (dp_ms + span_ms) / a.steps},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
                      "unit": "Gop/s", "frac": achieved / peak.value if peak.value else None,
                      "traffic": traffic,
                      "kernel": "k_dp_level", "avg_launch_ms": dp_ms / max(1, dp_launches),
-                     "ops_per_step": ops / a.steps,
+                     "ops_per_step": ops / a.steps, "f_bar": f_bar,
+                     "basis": "SURVEY 8(d): (2 + 4*F_bar) fp64 ops per unpruned visit",
+                     "executed": {"achieved": achieved_exec,
+                                  "frac": achieved_exec / peak.value if peak.value else None,
+                                  "ops_per_step": ops_exec / a.steps,
+                                  "note": "ops the kernel actually runs after exact pruning; "
+                                          "ncu: issue-bound on frontier bookkeeping"},
                      "peak_source": "measured on this GPU: pc_measure_fp64_peak "
                                     "(DADD+DSETP.MAX+DSETP chains, full occupancy)"},
         "plan": None if result.plan is None else {

@@ -14,7 +14,8 @@ from . import abi
 from .abi import PcCall, PcCallResult, PcPlan, PcProblem, PcStats
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpipecut_b200.so")
+# PIPECUT_B200_LIB: an alternative build of the same library (A/B timing)
+LIB_PATH = os.environ.get("PIPECUT_B200_LIB") or os.path.join(_HERE, "libpipecut_b200.so")
 
 
 class DeviceUnavailable(RuntimeError):

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
     const int64_t cells = (int64_t)cd.A * cd.B;
     const int cur = s & 1, prv = (s - 1) & 1;
     const int16_t *keyidx = B.keyidx + cd.key_off;
-    const int inter_d = inter_of(B.num_nodes, B.dpn, d);
+    const int inter_d = (B.num_nodes > 1 && (unsigned)d % (unsigned)B.dpn == 0) ? 1 : 0;
     const int64_t row = (int64_t)b * (b - 1) / 2;       // hm_idx(0, b)
     const double beta = B.beta;
     const WarpFront F = warp_front(w);
@@ -262,7 +262,10 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         // small) come first and build a frontier that prunes the rest -- ~4x
         // fewer frontier inserts than ascending on the C5 chains (order does not
         // change the result: the dominance relation is order-independent)
-        for (int dp = d - 1; dp >= base; --dp) {
+        const int dpn = B.dpn;
+        const bool multi_node = B.num_nodes > 1;
+        int rem = (int)((unsigned)(d - 1) % (unsigned)dpn);
+        for (int dp = d - 1; dp >= base; --dp, rem = rem == 0 ? dpn - 1 : rem - 1) {
             const int lo_col = cmin[dp - base];
             const int hi_col = cmax[dp - base];
             if (lo_col > hi_col || lo_col >= b) continue;           // no predecessor cell
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
             const double *tfrow = B.key_tf[kk] + row;
             const double *tbrow = DERIVED ? nullptr : B.key_tb[kk] + row;
             const double cutf = b < nb ? B.key_cut[kk][inter_d * (nb + 1) + b] : 0.0;
-            const double *cutb = B.key_cut[kk] + inter_of(B.num_nodes, B.dpn, dp) * (nb + 1);
+            const double *cutb = B.key_cut[kk] + ((multi_node && rem == 0) ? (nb + 1) : 0);
             const uint8_t *ccol = pcnt + (int64_t)(dp - base) * cd.A - base;
             const uint32_t *ocol = poff + (int64_t)(dp - base) * cd.A - base;
             int lim = bp_lo - 1;          // b' <= lim are settled
