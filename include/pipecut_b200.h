@@ -190,6 +190,15 @@ int pc_set_problem(pc_ctx *ctx, const pc_problem *p);
 int pc_set_overrides(pc_ctx *ctx, int32_t n_m, const int64_t *m_values, const uint8_t *has,
                      const double *tf, const double *tb, const int64_t *act);
 
+/* brute_force_partition (pkg/src/pipecut/stages.py:304-369): every (cut
+ * combination, composition of D into S parts) pair, objective
+ * max(tf) + max(tb), ties by the reference's lex (bounds, devs) order;
+ * stats->visits = number of pairs.  The reference's nb <= 12 / D <= 8 guard
+ * (TooLarge) is the caller's; here the cap is 1e12 pairs and S <= 64
+ * (PC_ERR_CAPACITY beyond).  Returns PC_OK or PC_INFEASIBLE. */
+int pc_brute_force(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_size, int32_t R,
+                   int32_t MB, pc_plan *plan, pc_stats *stats);
+
 /* CostModel.profile over block spans: n queries (lo, hi, m, ckpt). */
 int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const int32_t *hi,
                      const int64_t *m, const int32_t *ckpt,

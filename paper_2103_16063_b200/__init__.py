@@ -17,9 +17,9 @@ CLI and library users pick the GPU path up unchanged.
 from ._host import pipecut as _pc  # noqa: F401  (host API package)
 from .blocks import partition_blocks
 from .search import form_stage_sharded
-from .stages import form_stage, form_stage_dp
+from .stages import brute_force_partition, form_stage, form_stage_dp
 
-__all__ = ["form_stage", "form_stage_dp", "form_stage_sharded", "install", "partition_blocks"]
+__all__ = ["brute_force_partition", "form_stage", "form_stage_dp", "form_stage_sharded", "install", "partition_blocks"]
 
 
 def install():
@@ -31,6 +31,7 @@ def install():
 
     for mod in (pipecut, pipecut.stages, pipecut.blocks, pipecut.cli):
         for name, fn in (("form_stage", form_stage), ("form_stage_dp", form_stage_dp),
-                         ("partition_blocks", partition_blocks)):
+                         ("partition_blocks", partition_blocks),
+                         ("brute_force_partition", brute_force_partition)):
             if hasattr(mod, name):
                 setattr(mod, name, fn)

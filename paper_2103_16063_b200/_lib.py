@@ -68,6 +68,8 @@ def load():
                                             C.c_void_p, C.c_void_p]
         lib.pc_set_overrides.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.pc_brute_force.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
+                                       C.c_int32, P(PcPlan), P(PcStats)]
         lib.pc_reset_cache.argtypes = [C.c_void_p]
         lib.pc_timer_start.argtypes = [C.c_void_p]
         lib.pc_timer_stop.argtypes = [C.c_void_p, P(C.c_double)]
@@ -75,7 +77,8 @@ def load():
         for name in ("pc_ctx_create", "pc_device_info", "pc_set_problem", "pc_profile_spans",
                      "pc_form_stage_dp", "pc_run_calls", "pc_last_crossing", "pc_form_stage",
                      "pc_reset_cache", "pc_timer_start", "pc_timer_stop",
-                     "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides"):
+                     "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides",
+                     "pc_brute_force"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
         return lib
@@ -84,7 +87,8 @@ def load():
 EXPORTS = ("pc_ctx_create", "pc_ctx_destroy", "pc_last_error", "pc_device_info",
            "pc_set_problem", "pc_profile_spans", "pc_form_stage_dp", "pc_run_calls",
            "pc_last_crossing", "pc_form_stage", "pc_reset_cache", "pc_timer_start",
-           "pc_timer_stop", "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides")
+           "pc_timer_stop", "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides",
+           "pc_brute_force")
 
 
 class Context:

@@ -1087,6 +1087,158 @@ extern "C" int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const
     return PC_OK;
 }
 
+// brute_force_partition (stages.py:304-369) over the DP's key tables: every
+// (cut combination, composition) pair on the device (brute.cu), then the
+// winner's stage records as profile queries.
+extern "C" int pc_brute_force(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_size, int32_t R,
+                              int32_t MB, pc_plan *plan, pc_stats *stats) {
+    if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
+    cudaSetDevice(ctx->device);
+    const pc_call call{S, D, R, MB};
+    if (int rc = validate_call(ctx, call, batch_size)) return rc;
+    if (S > BF_MAXS) return fail(ctx, PC_ERR_CAPACITY, "brute force: more than 64 stages");
+    if (plan && S > plan->cap_stages) return fail(ctx, PC_ERR_CAPACITY, "plan capacity");
+    const DevProblem &P = ctx->P;
+    const int nb = ctx->nb, k = S - 1, kcols = S;
+    const int nmax = std::max(nb, D);
+    const int64_t SAT = (int64_t)1 << 62;
+    std::vector<int64_t> binom((size_t)(nmax + 1) * kcols, 0);
+    for (int a = 0; a <= nmax; ++a) {
+        binom[(size_t)a * kcols] = 1;
+        for (int j = 1; j < kcols && a > 0; ++j) {
+            const int64_t x = binom[(size_t)(a - 1) * kcols + j - 1], y = binom[(size_t)(a - 1) * kcols + j];
+            binom[(size_t)a * kcols + j] = (x >= SAT - y) ? SAT : x + y;
+        }
+    }
+    const int64_t n_comb = binom[(size_t)(nb - 1) * kcols + k];
+    const int64_t n_comp = binom[(size_t)(D - 1) * kcols + k];
+    if (n_comb >= SAT || n_comp >= SAT || (double)n_comb * (double)n_comp > 1e12)
+        return fail(ctx, PC_ERR_CAPACITY, "brute force: more than 1e12 assignments");
+    // keys of every device count (stages.py:326-330)
+    const int ckpt = (P.checkpointing && S > 1) ? 1 : 0;
+    const int B = D - S + 1;
+    std::vector<std::pair<int64_t, int>> want, dkey(B + 1, {0, -1});
+    for (int dev = 1; dev <= B; ++dev) {
+        const int64_t m = batch_size / ((int64_t)MB * R * dev);
+        if (m >= 1) {
+            dkey[dev] = {m, ckpt};
+            want.push_back(dkey[dev]);
+        }
+    }
+    std::sort(want.begin(), want.end());
+    want.erase(std::unique(want.begin(), want.end()), want.end());
+    ctx->launches = 0;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->st));
+    if (int rc = ensure_keys(ctx, want)) return rc;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->st));
+    std::vector<int16_t> keyidx(B + 1, -1);
+    for (int dev = 1; dev <= B; ++dev)
+        if (dkey[dev].second >= 0) keyidx[dev] = (int16_t)ctx->key_map[dkey[dev]];
+    const int64_t n_chunks = (n_comp + BF_CHUNK - 1) / BF_CHUNK;
+    const int64_t items = n_comb * n_chunks;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((items + BF_THREADS - 1) / BF_THREADS,
+                                                                   (int64_t)ctx->sm_count * 8));
+    const size_t b_bytes = 8 * binom.size(), k_bytes = 2 * keyidx.size();
+    const size_t off_k = (b_bytes + 255) & ~size_t(255);
+    const size_t off_o = (off_k + k_bytes + 255) & ~size_t(255);
+    CUDA_TRY(ctx, ctx->bf_d.ensure(off_o + 24 * (size_t)blocks + 64));
+    char *base = ctx->bf_d.as<char>();
+    CUDA_TRY(ctx, cudaMemcpyAsync(base, binom.data(), b_bytes, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(base + off_k, keyidx.data(), k_bytes, cudaMemcpyHostToDevice, ctx->st));
+    const size_t nk = ctx->keys.size();
+    BruteArgs a{};
+    a.key_tf = (const double *const *)ctx->key_ptrs.p;
+    a.key_tb = ((const double *const *)ctx->key_ptrs.p) + nk;
+    a.key_cut = ((const double *const *)ctx->key_ptrs.p) + 2 * nk;
+    a.keyidx = (const int16_t *)(base + off_k);
+    a.binom = (const int64_t *)base;
+    a.kcols = kcols;
+    a.nb = nb; a.S = S; a.D = D;
+    a.derived = ctx->derived ? 1 : 0;
+    a.num_nodes = P.num_nodes; a.dpn = P.dpn;
+    a.beta = P.beta;
+    a.n_comb = n_comb; a.n_comp = n_comp; a.n_chunks = n_chunks;
+    a.out_key = (unsigned long long *)(base + off_o);
+    a.out_idx = (long long *)(a.out_key + blocks);
+    a.out_obj = (double *)(a.out_idx + blocks);
+    launch_brute(a, blocks, ctx->st);
+    ctx->launches++;
+    if (int rc = check_launch(ctx, "brute")) return rc;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev2, ctx->st));
+    std::vector<unsigned long long> okey(blocks);
+    std::vector<long long> oidx(blocks);
+    std::vector<double> oobj(blocks);
+    CUDA_TRY(ctx, cudaMemcpyAsync(okey.data(), a.out_key, 8 * (size_t)blocks, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(oidx.data(), a.out_idx, 8 * (size_t)blocks, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(oobj.data(), a.out_obj, 8 * (size_t)blocks, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    int win = -1;
+    for (int i = 0; i < blocks; ++i) {
+        if (oidx[i] < 0) continue;
+        if (win < 0 || okey[i] < okey[win] || (okey[i] == okey[win] && oidx[i] < oidx[win])) win = i;
+    }
+    float span_ms = 0, bf_ms = 0;
+    cudaEventElapsedTime(&span_ms, ctx->ev0, ctx->ev1);
+    cudaEventElapsedTime(&bf_ms, ctx->ev1, ctx->ev2);
+    if (stats) {
+        *stats = pc_stats{};
+        stats->visits = n_comb * n_comp;           // every pair counts (stages.py:321)
+        stats->dp_calls = 0;
+        stats->kernel_launches = ctx->launches;
+        stats->device_ms = bf_ms;
+        stats->span_ms = span_ms;
+    }
+    if (plan) {
+        plan->S = S; plan->D = D; plan->R = R; plan->MB = MB;
+        plan->iteration_time = NAN;
+        plan->n_stages = 0;
+        plan->objective = NAN;
+    }
+    if (win < 0) return PC_INFEASIBLE;
+    // the winner's bounds and devices (host unrank of the same lex ranks)
+    auto unrank_h = [&](int64_t r, int n, int *out) {
+        int v = 1;
+        for (int i = 0; i < k; ++i)
+            for (;;) {
+                const int64_t c = binom[(size_t)(n - v) * kcols + (k - 1 - i)];
+                if (r < c) { out[i] = v++; break; }
+                r -= c;
+                ++v;
+            }
+    };
+    std::vector<int> cuts(std::max(k, 1)), cps(std::max(k, 1));
+    unrank_h(oidx[win] / n_comp, nb - 1, cuts.data());
+    unrank_h(oidx[win] % n_comp, D - 1, cps.data());
+    std::vector<int32_t> qlo(S), qhi(S), qck(S, ckpt), qdev(S);
+    std::vector<int64_t> qm(S);
+    for (int i = 0, prev = 0; i < S; ++i) {
+        qlo[i] = i == 0 ? 0 : cuts[i - 1];
+        qhi[i] = i == k ? nb : cuts[i];
+        const int cum = i == k ? D : cps[i];
+        qdev[i] = cum - prev;
+        prev = cum;
+        qm[i] = batch_size / ((int64_t)MB * R * qdev[i]);
+    }
+    std::vector<double> tf(S), tb(S);
+    std::vector<int64_t> mem(S);
+    if (int rc = pc_profile_spans(ctx, S, qlo.data(), qhi.data(), qm.data(), qck.data(), tf.data(),
+                                  tb.data(), mem.data()))
+        return rc;
+    if (plan) {
+        plan->n_stages = S;
+        plan->objective = oobj[win];
+        for (int i = 0; i < S; ++i) {
+            plan->lo[i] = qlo[i];
+            plan->hi[i] = qhi[i];
+            plan->devices[i] = qdev[i];
+            plan->t_fwd[i] = tf[i];
+            plan->t_bwd[i] = tb[i];
+            plan->mem[i] = mem[i];
+        }
+    }
+    return PC_OK;
+}
+
 extern "C" int pc_reset_cache(pc_ctx *ctx) {
     cudaSetDevice(ctx->device);
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));

@@ -227,6 +227,25 @@ void launch_row_visits(const DPBatch &b, int pruning, int64_t *level_sums, int64
 void launch_backtrack(const DPBatch &b, int64_t batch_size, const int32_t *plan_off,
                       int32_t *seg_lo, int32_t *seg_hi, int32_t *seg_dev, double *objective,
                       int32_t *feasible, cudaStream_t st);
+// brute.cu: exhaustive (cuts x compositions) search, brute_force_partition
+constexpr int BF_MAXS = 64;       // stages per enumerated assignment
+constexpr int BF_CHUNK = 64;      // composition ranks per work item
+constexpr int BF_THREADS = 256;
+struct BruteArgs {
+    const double *const *key_tf;
+    const double *const *key_tb;
+    const double *const *key_cut;
+    const int16_t *keyidx;        // [D - S + 2] key of each device count (-1: m == 0)
+    const int64_t *binom;         // [(n_max + 1) * kcols] C(a, j), saturated
+    int kcols;
+    int nb, S, D, derived, num_nodes, dpn;
+    double beta;
+    int64_t n_comb, n_comp, n_chunks;
+    unsigned long long *out_key;  // per block winner
+    long long *out_idx;
+    double *out_obj;
+};
+void launch_brute(const BruteArgs &a, int blocks, cudaStream_t st);
 // peak.cu
 double measure_fp64_gops(cudaStream_t st, int sm_count);
 // sim.cu

@@ -89,6 +89,7 @@ struct pc_ctx {
     DBuf plan_off_d, seg_d, objective_d, feasible_d;
     DBuf q_d, q_out_d, sim_d;
     DBuf raw_d, keys_m_d, keys_ckpt_d, colb_d;
+    DBuf bf_d;       // brute force: binomials, keys, per-block winners
     DBuf cut_d;      // pruning cut (cost tables): row/column prefixes, row_e
     // last batch (for budget crossing queries)
     std::vector<CallDesc> last_calls;   // sorted order

@@ -20,6 +20,7 @@ from .flatten import flatten_blockset, resolve_overrides
 _stages = _pc.stages
 InvalidArgs = _stages.InvalidArgs
 SearchBudgetExceeded = _stages.SearchBudgetExceeded
+TooLarge = _stages.TooLarge
 SearchOptions = _stages.SearchOptions
 SearchResult = _stages.SearchResult
 SearchStats = _stages.SearchStats
@@ -148,5 +149,30 @@ def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
     if rc == abi.PC_ERR_BUDGET:
         raise SearchBudgetExceeded(int(st.visits), int(opts.visit_budget))
     stats = SearchStats(visits=int(st.visits), dp_calls=int(st.dp_calls))
+    plan = plan_from_buffers(buf, batch_size) if rc == abi.PC_OK else None
+    return SearchResult(plan, stats)
+
+
+def brute_force_partition(blocks, S: int, D: int, batch_size: int, replica_factor: int,
+                          microbatches: int, options=None, *, guard: bool = True):
+    """Exhaustive search over every (cut combination, device composition)
+    pair on the GPU (stages.py:304-369): same candidate rules as the DP,
+    objective max(t_fwd) + max(t_bwd), ties by (bounds, devices), visits =
+    pairs enumerated.  ``guard`` keeps the reference's TooLarge limit
+    (nb <= 12, D <= 8); with ``guard=False`` the device enumerates up to 1e12
+    pairs (S <= 64)."""
+    _check_args(blocks, S, D, batch_size, replica_factor, microbatches)
+    nb = len(blocks)
+    if guard and (nb > 12 or D > 8):
+        raise TooLarge(f"{nb} blocks on {D} devices is past the enumeration guard")
+    ctx = _lib.context()
+    flat = bind_problem(ctx, blocks)
+    bind_overrides(ctx, flat, call_shares([(S, D, replica_factor, microbatches)], batch_size))
+    buf = abi.PlanBuffers(S)
+    st = abi.PcStats()
+    rc = ctx.lib.pc_brute_force(ctx.h, S, D, batch_size, replica_factor, microbatches,
+                                C.byref(buf.s), C.byref(st))
+    ctx.check(rc, "brute_force_partition")
+    stats = SearchStats(visits=int(st.visits), dp_calls=0)
     plan = plan_from_buffers(buf, batch_size) if rc == abi.PC_OK else None
     return SearchResult(plan, stats)

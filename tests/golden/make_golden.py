@@ -48,6 +48,7 @@ def random_families():
                 res = pc.form_stage_dp(bs, S, D, BS, R, MB,
                                        pc.SearchOptions(disable_pruning=not prune))
                 rec["pruned" if prune else "unpruned"] = result_doc(res)
+            rec["brute"] = result_doc(pc.brute_force_partition(bs, S, D, BS, R, MB))
             out.append(rec)
     dump("random_dp.json", out)
 
@@ -112,6 +113,7 @@ def cost_tables():
                 res = pc.form_stage_dp(bs, S, D, BS, R, MB,
                                        pc.SearchOptions(disable_pruning=not prune))
                 rec["dp_pruned" if prune else "dp_unpruned"] = result_doc(res)
+            rec["brute"] = result_doc(pc.brute_force_partition(bs, S, D, BS, R, MB))
         rec["form_stage"] = result_doc(pc.form_stage(nodes, dpn, BS, bs))
         calls, _ = enumerate_calls(nodes, dpn, BS, nb)
         rec["calls"] = [[list(c), result_doc(pc.form_stage_dp(bs, c[0], c[1], BS, c[2], c[3]))]
