@@ -199,6 +199,23 @@ int pc_set_overrides(pc_ctx *ctx, int32_t n_m, const int64_t *m_values, const ui
 int pc_brute_force(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_size, int32_t R,
                    int32_t MB, pc_plan *plan, pc_stats *stats);
 
+/* validate_plan's fresh records (pkg/src/pipecut/stages.py:416-492) for the
+ * plan's stages: span profile at each stage's share (NaN / -1 where the share
+ * is zero), the comm-charged times and objective = max(tf) + max(tb) over the
+ * stages with a positive share (NaN if none).  Arrays are [plan->n_stages]. */
+int pc_check_plan(pc_ctx *ctx, const pc_plan *plan, int64_t batch_size, double *rec_tf,
+                  double *rec_tb, int64_t *rec_mem, double *charged_tf, double *charged_tb,
+                  double *objective);
+
+/* simulate (pkg/src/pipecut/simulate.py:79-179) of a plan: every lane event,
+ * stage-major, lane_off[n_stages+1]; phases 0 fwd, 1 recompute, 2 bwd, 3 comm,
+ * 4 allreduce; microbatch -1 for the gradient sync.  summary[5] = {iteration
+ * time, busy device-seconds, bubble fraction, samples/s, devices}.  ev_cap must
+ * be >= n_stages * (5 * MB + 1). */
+int pc_simulate(pc_ctx *ctx, const pc_plan *plan, int64_t batch_size, int32_t ev_cap,
+                int32_t *lane_off, int32_t *ev_mb, int8_t *ev_phase, double *ev_start,
+                double *ev_end, double *summary);
+
 /* CostModel.profile over block spans: n queries (lo, hi, m, ckpt). */
 int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const int32_t *hi,
                      const int64_t *m, const int32_t *ckpt,

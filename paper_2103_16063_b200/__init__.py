@@ -23,15 +23,35 @@ __all__ = ["brute_force_partition", "form_stage", "form_stage_dp", "form_stage_s
 
 
 def install():
-    """Point the reference's modules at the GPU entry points."""
+    """Point the reference's modules at the GPU entry points:
+    partition_blocks, form_stage_dp, form_stage, brute_force_partition,
+    validate_plan and simulate in pipecut, pipecut.blocks, pipecut.stages,
+    pipecut.simulate and pipecut.cli (the CLI binds the names at import,
+    cli.py:18-41).  Returns a function that restores the reference's own."""
+    import sys
+
     import pipecut
     import pipecut.blocks
     import pipecut.cli
+    import pipecut.simulate  # noqa: F401  (the package attribute is the function)
     import pipecut.stages
 
-    for mod in (pipecut, pipecut.stages, pipecut.blocks, pipecut.cli):
-        for name, fn in (("form_stage", form_stage), ("form_stage_dp", form_stage_dp),
-                         ("partition_blocks", partition_blocks),
-                         ("brute_force_partition", brute_force_partition)):
+    from .simulate import simulate, validate_plan
+
+    swaps = (("form_stage", form_stage), ("form_stage_dp", form_stage_dp),
+             ("partition_blocks", partition_blocks),
+             ("brute_force_partition", brute_force_partition),
+             ("validate_plan", validate_plan), ("simulate", simulate))
+    saved = []
+    mods = [sys.modules["pipecut" + x] for x in ("", ".stages", ".blocks", ".simulate", ".cli")]
+    for mod in mods:
+        for name, fn in swaps:
             if hasattr(mod, name):
+                saved.append((mod, name, getattr(mod, name)))
                 setattr(mod, name, fn)
+
+    def restore():
+        for mod, name, fn in reversed(saved):
+            setattr(mod, name, fn)
+
+    return restore

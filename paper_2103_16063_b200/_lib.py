@@ -70,6 +70,10 @@ def load():
                                          C.c_void_p, C.c_void_p, C.c_void_p]
         lib.pc_brute_force.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
                                        C.c_int32, P(PcPlan), P(PcStats)]
+        lib.pc_check_plan.argtypes = [C.c_void_p, P(PcPlan), C.c_int64, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_double)]
+        lib.pc_simulate.argtypes = [C.c_void_p, P(PcPlan), C.c_int64, C.c_int32, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         lib.pc_reset_cache.argtypes = [C.c_void_p]
         lib.pc_timer_start.argtypes = [C.c_void_p]
         lib.pc_timer_stop.argtypes = [C.c_void_p, P(C.c_double)]
@@ -78,7 +82,7 @@ def load():
                      "pc_form_stage_dp", "pc_run_calls", "pc_last_crossing", "pc_form_stage",
                      "pc_reset_cache", "pc_timer_start", "pc_timer_stop",
                      "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides",
-                     "pc_brute_force"):
+                     "pc_brute_force", "pc_check_plan", "pc_simulate"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
         return lib
@@ -88,7 +92,7 @@ EXPORTS = ("pc_ctx_create", "pc_ctx_destroy", "pc_last_error", "pc_device_info",
            "pc_set_problem", "pc_profile_spans", "pc_form_stage_dp", "pc_run_calls",
            "pc_last_crossing", "pc_form_stage", "pc_reset_cache", "pc_timer_start",
            "pc_timer_stop", "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides",
-           "pc_brute_force")
+           "pc_brute_force", "pc_check_plan", "pc_simulate")
 
 
 class Context:

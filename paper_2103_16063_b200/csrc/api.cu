@@ -1239,6 +1239,125 @@ extern "C" int pc_brute_force(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_s
     return PC_OK;
 }
 
+// validate_plan's fresh records (stages.py:452-492): per stage the span
+// profile at its share (stages with a zero share are skipped: NaN / -1), the
+// comm-charged times and the recomputed objective.
+extern "C" int pc_check_plan(pc_ctx *ctx, const pc_plan *plan, int64_t batch_size, double *rec_tf,
+                             double *rec_tb, int64_t *rec_mem, double *charged_tf,
+                             double *charged_tb, double *objective) {
+    if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
+    cudaSetDevice(ctx->device);
+    const int S = plan->n_stages;
+    if (S < 1 || plan->MB < 1 || plan->R < 1 || batch_size < 1) return fail(ctx, PC_ERR_INVALID, "empty plan or counts below 1");
+    const int ckpt = (ctx->P.checkpointing && S > 1) ? 1 : 0;
+    std::vector<int32_t> lo(S), hi(S), dv(S), qlo, qhi, qck;
+    std::vector<int64_t> m(S), qm;
+    std::vector<int> qi;
+    for (int i = 0; i < S; ++i) {
+        lo[i] = plan->lo[i];
+        hi[i] = plan->hi[i];
+        dv[i] = plan->devices[i];
+        if (lo[i] < 0 || hi[i] > ctx->nb || hi[i] <= lo[i] || dv[i] < 1)
+            return fail(ctx, PC_ERR_INVALID, "stage bounds or devices out of range");
+        m[i] = batch_size / ((int64_t)plan->MB * plan->R * dv[i]);
+        rec_tf[i] = rec_tb[i] = charged_tf[i] = charged_tb[i] = NAN;
+        rec_mem[i] = -1;
+        if (m[i] >= 1) {
+            qi.push_back(i);
+            qlo.push_back(lo[i]);
+            qhi.push_back(hi[i]);
+            qm.push_back(m[i]);
+            qck.push_back(ckpt);
+        }
+    }
+    const int nq = (int)qi.size();
+    std::vector<double> tf(S, 0.0), tb(S, 0.0);
+    if (nq) {
+        std::vector<double> qtf(nq), qtb(nq);
+        std::vector<int64_t> qmem(nq);
+        if (int rc = pc_profile_spans(ctx, nq, qlo.data(), qhi.data(), qm.data(), qck.data(),
+                                      qtf.data(), qtb.data(), qmem.data()))
+            return rc;
+        for (int j = 0; j < nq; ++j) {
+            tf[qi[j]] = rec_tf[qi[j]] = qtf[j];
+            tb[qi[j]] = rec_tb[qi[j]] = qtb[j];
+            rec_mem[qi[j]] = qmem[j];
+        }
+    }
+    const size_t b4 = 4 * (size_t)S, b8 = 8 * (size_t)S;
+    CUDA_TRY(ctx, ctx->sim_d.ensure(3 * b4 + 5 * b8 + 64));
+    char *base = ctx->sim_d.as<char>();
+    double *d_tf = (double *)base, *d_tb = d_tf + S, *d_ctf = d_tb + S, *d_ctb = d_ctf + S;
+    int64_t *d_m = (int64_t *)(d_ctb + S);
+    double *d_obj = (double *)(d_m + S);
+    int32_t *d_lo = (int32_t *)(d_obj + 1), *d_hi = d_lo + S, *d_dv = d_hi + S;
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_tf, tf.data(), b8, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_tb, tb.data(), b8, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_m, m.data(), b8, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_lo, lo.data(), b4, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_hi, hi.data(), b4, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_dv, dv.data(), b4, cudaMemcpyHostToDevice, ctx->st));
+    launch_charge_plan(ctx->P, S, d_lo, d_hi, d_dv, d_m, d_tf, d_tb, d_ctf, d_ctb, d_obj, ctx->st);
+    if (int rc = check_launch(ctx, "charge_plan")) return rc;
+    std::vector<double> ctf(S), ctb(S);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctf.data(), d_ctf, b8, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctb.data(), d_ctb, b8, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(objective, d_obj, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    for (int i = 0; i < S; ++i)
+        if (m[i] >= 1) {
+            charged_tf[i] = ctf[i];
+            charged_tb[i] = ctb[i];
+        }
+    return PC_OK;
+}
+
+// simulate() (simulate.py:79-179) of a validated plan: every lane event
+// (stage-major, lane_off[S+1]) and summary = {iteration time, busy device
+// time, bubble fraction, samples/s, devices}.
+extern "C" int pc_simulate(pc_ctx *ctx, const pc_plan *plan, int64_t batch_size, int32_t ev_cap,
+                           int32_t *lane_off, int32_t *ev_mb, int8_t *ev_phase, double *ev_start,
+                           double *ev_end, double *summary) {
+    if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
+    cudaSetDevice(ctx->device);
+    const int S = plan->n_stages, MB = plan->MB, R = plan->R;
+    if (S < 1 || MB < 1 || R < 1 || batch_size < 1) return fail(ctx, PC_ERR_INVALID, "empty plan or counts below 1");
+    const int64_t cap = (int64_t)S * (5 * (int64_t)MB + 1);
+    if (cap > ev_cap || cap > (int64_t)1 << 30) return fail(ctx, PC_ERR_CAPACITY, "event capacity");
+    for (int i = 0; i < S; ++i)
+        if (plan->lo[i] < 0 || plan->hi[i] > ctx->nb || plan->hi[i] <= plan->lo[i] || plan->devices[i] < 1)
+            return fail(ctx, PC_ERR_INVALID, "stage bounds or devices out of range");
+    const size_t b4 = 4 * (size_t)S, b8 = 8 * (size_t)S;
+    const size_t ev_bytes = (size_t)cap * (4 + 1 + 8 + 8);
+    CUDA_TRY(ctx, ctx->q_d.ensure(3 * b4 + 2 * b8 + 4 * (size_t)(S + 1) + 64 + 256));
+    CUDA_TRY(ctx, ctx->q_out_d.ensure(ev_bytes + 256));
+    char *qb = ctx->q_d.as<char>();
+    double *d_tf = (double *)qb, *d_tb = d_tf + S, *d_sum = d_tb + S;
+    int32_t *d_lo = (int32_t *)(d_sum + 8), *d_hi = d_lo + S, *d_dv = d_hi + S, *d_off = d_dv + S;
+    char *eb = ctx->q_out_d.as<char>();
+    double *d_st = (double *)eb, *d_en = d_st + cap;
+    int32_t *d_mb = (int32_t *)(d_en + cap);
+    int8_t *d_ph = (int8_t *)(d_mb + cap);
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_tf, plan->t_fwd, b8, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_tb, plan->t_bwd, b8, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_lo, plan->lo, b4, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_hi, plan->hi, b4, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(d_dv, plan->devices, b4, cudaMemcpyHostToDevice, ctx->st));
+    launch_schedule(ctx->P, S, R, MB, batch_size, d_lo, d_hi, d_dv, d_tf, d_tb, d_off, d_mb, d_ph,
+                    d_st, d_en, d_sum, ctx->st);
+    if (int rc = check_launch(ctx, "schedule")) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(lane_off, d_off, 4 * (size_t)(S + 1), cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(summary, d_sum, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    const int64_t n_ev = lane_off[S];
+    CUDA_TRY(ctx, cudaMemcpyAsync(ev_mb, d_mb, 4 * (size_t)n_ev, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ev_phase, d_ph, (size_t)n_ev, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ev_start, d_st, 8 * (size_t)n_ev, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ev_end, d_en, 8 * (size_t)n_ev, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    return PC_OK;
+}
+
 extern "C" int pc_reset_cache(pc_ctx *ctx) {
     cudaSetDevice(ctx->device);
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));

@@ -227,6 +227,14 @@ void launch_row_visits(const DPBatch &b, int pruning, int64_t *level_sums, int64
 void launch_backtrack(const DPBatch &b, int64_t batch_size, const int32_t *plan_off,
                       int32_t *seg_lo, int32_t *seg_hi, int32_t *seg_dev, double *objective,
                       int32_t *feasible, cudaStream_t st);
+// sim.cu: full schedule and validate_plan's charged times
+void launch_schedule(const DevProblem &p, int S, int R, int MB, int64_t BS, const int32_t *lo,
+                     const int32_t *hi, const int32_t *dev, const double *tf, const double *tb,
+                     int32_t *lane_off, int32_t *ev_mb, int8_t *ev_phase, double *ev_start,
+                     double *ev_end, double *summary, cudaStream_t st);
+void launch_charge_plan(const DevProblem &p, int S, const int32_t *lo, const int32_t *hi,
+                        const int32_t *dev, const int64_t *m, const double *rtf, const double *rtb,
+                        double *ctf, double *ctb, double *objective, cudaStream_t st);
 // brute.cu: exhaustive (cuts x compositions) search, brute_force_partition
 constexpr int BF_MAXS = 64;       // stages per enumerated assignment
 constexpr int BF_CHUNK = 64;      // composition ranks per work item
