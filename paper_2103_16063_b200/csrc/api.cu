@@ -452,6 +452,9 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     CUDA_TRY(ctx, ctx->keyidx_d.ensure(sizeof(int16_t) * keyidx.size() + 16));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->calls_d.p, cds.data(), sizeof(CallDesc) * n, cudaMemcpyHostToDevice, ctx->st));
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->warp_prefix_d.p, cta_prefix.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, ctx->cta_call_d.ensure(sizeof(int32_t) * (size_t)cta_prefix[n] + 16));
+    launch_cta_call(ctx->warp_prefix_d.as<int64_t>(), n, cta_prefix[n], ctx->cta_call_d.as<int32_t>(), ctx->st);
+    ctx->launches++;
     CUDA_TRY(ctx, cudaMemcpyAsync(ctx->keyidx_d.p, keyidx.data(), sizeof(int16_t) * keyidx.size(), cudaMemcpyHostToDevice, ctx->st));
 
     const size_t nk = ctx->keys.size();
@@ -497,6 +500,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.n_calls = n;
         bt.calls = ctx->calls_d.as<CallDesc>();
         bt.cta_prefix = ctx->warp_prefix_d.as<int64_t>();
+        bt.cta_call = ctx->cta_call_d.as<int32_t>();
         bt.keyidx = ctx->keyidx_d.as<int16_t>();
         bt.key_tf = (const double *const *)ctx->key_ptrs.p;
         bt.key_tb = ((const double *const *)ctx->key_ptrs.p) + nk;

@@ -84,6 +84,7 @@ struct pc_ctx {
     DBuf ov_d;
     DBuf mismatch_d;
     // batch scratch
+    DBuf cta_call_d;
     DBuf calls_d, warp_prefix_d, keyidx_d, val_d, hist_d, overflow_d;
     DBuf level_off_d, level_sums_d, row_prefix_d;
     DBuf plan_off_d, seg_d, objective_d, feasible_d;

@@ -17,7 +17,7 @@
 // dominates a candidate c iff e precedes c in the (tf, tb, key) order and
 // e.tb <= c.tb.  That relation is a strict partial order, so the frontier is
 // the set of its maximal elements whatever the insertion order.  The cell's
-// frontier lives in shared memory sorted by tf (capacity FMAX = 32); lanes
+// frontier lives in shared memory sorted by tf (capacity FMAX = 64); lanes
 // build candidates in parallel and test them against it by binary search,
 // and only the few survivors are inserted, one warp-cooperative step each.
 #include <math.h>
@@ -25,7 +25,12 @@
 #include "common.cuh"
 
 #ifndef DP_MIN_BLOCKS
-#define DP_MIN_BLOCKS 4
+#define DP_MIN_BLOCKS 10
+#endif
+// diagnostic counters (frontier-size histogram, rounds, chunks, corner-pruned
+// pairs, window entries) for PIPECUT_B200_DEBUG: build with -DPC_DP_DIAG=1
+#ifndef PC_DP_DIAG
+#define PC_DP_DIAG 0
 #endif
 
 namespace pcb {
@@ -189,14 +194,8 @@ __device__ __forceinline__ int lex_min_lane(bool live, double x, double y, uint3
 
 template <bool DERIVED>
 __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBatch B, int s, int n_active) {
-    const int64_t cta = blockIdx.x;
-    if (cta >= B.cta_prefix[n_active]) return;
-    int lo = 0, hi = n_active;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (B.cta_prefix[mid] <= cta) lo = mid; else hi = mid;
-    }
-    const int c = lo;
+    const int64_t cta = blockIdx.x;                  // grid = cta_prefix[n_active]
+    const int c = B.cta_call[cta];
     const CallDesc cd = B.calls[c];
     // warps take consecutive cells of the call in (b, d) order, so every warp
     // of the CTA has a cell whatever B is
@@ -311,7 +310,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                         // tb (last entry), each clipped by the new stage
                         const double ix = dmax_ref(etf[pbase], tfc);
                         const double iy = dmax_ref(etb[pbase + cnt - 1], tbc);
-                        if (n > 0 && corner_dominated(F, n, ix, iy)) ++n_corner;
+                        if (n > 0 && corner_dominated(F, n, ix, iy)) { if (PC_DP_DIAG) ++n_corner; }
                         else {
                             // exact window: entries with ptf <= tfc collapse onto the
                             // last of them, entries with ptb <= tbc onto the first
@@ -326,9 +325,11 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                     }
                 }
                 const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)(whi - wlo + 1));
-                n_win += whi - wlo + 1;
-                n_rounds += rounds;
-                ++n_iters;
+                if (PC_DP_DIAG) {
+                    n_win += whi - wlo + 1;
+                    n_rounds += rounds;
+                    ++n_iters;
+                }
                 for (int r = 0; r < rounds; ++r) {
                     const int i = wlo + r;
                     double cx = 0.0, cy = 0.0;
@@ -401,11 +402,13 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         atomicAdd(&B.counters[0], (unsigned long long)n_pairs);
         atomicAdd(&B.counters[1], (unsigned long long)n_cands);
         atomicAdd(&B.counters[2], (unsigned long long)n_ins);
-        atomicAdd(&B.counters[3 + min(n, FMAX)], 1ull);     // frontier-size histogram
-        atomicAdd(&B.counters[4 + FMAX + 0], (unsigned long long)n_rounds);
-        atomicAdd(&B.counters[4 + FMAX + 1], (unsigned long long)n_iters);
+        if (PC_DP_DIAG) {
+            atomicAdd(&B.counters[3 + min(n, FMAX)], 1ull);     // frontier-size histogram
+            atomicAdd(&B.counters[4 + FMAX + 0], (unsigned long long)n_rounds);
+            atomicAdd(&B.counters[4 + FMAX + 1], (unsigned long long)n_iters);
+        }
     }
-    {
+    if (PC_DP_DIAG) {
         unsigned a = n_corner, bw = n_win;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -466,6 +469,23 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         B.hist_cnt[hcell] = byte;
         if (ovf) atomicOr(B.overflow, 1);
     }
+}
+
+// CTA -> call of a batch, once per batch: the active calls of every level are
+// a prefix of the batch's calls, so the map holds for all levels.
+__global__ void k_cta_call(const int64_t *prefix, int n, int32_t *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= prefix[n]) return;
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (prefix[mid] <= i) lo = mid; else hi = mid;
+    }
+    out[i] = lo;
+}
+
+void launch_cta_call(const int64_t *prefix, int n, int64_t total, int32_t *out, cudaStream_t st) {
+    if (total > 0) k_cta_call<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(prefix, n, out);
 }
 
 void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool derived,
