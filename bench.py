@@ -326,7 +326,9 @@ def run_ours(a):
     # stages.py:239, and 2 compares, _pareto) over the step's unpruned visits;
     # F = mean predecessor frontier size over the feasible pairs (cands/pairs).
     f_bar = cands / pairs if pairs else 0.0
-    ops = unpruned * a.steps * (2.0 + 4.0 * f_bar)
+    # per GPU: this rank's calls over this rank's DP time (rank 0 reports)
+    local_unpruned = unpruned_visits(nb, my_calls)
+    ops = local_unpruned * a.steps * (2.0 + 4.0 * f_bar)
     achieved = ops / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
     # what the kernel executes after its exact pruning (corner, window, prefix skip)
     ops_exec = 2.0 * pairs + 4.0 * cands
@@ -362,6 +364,7 @@ def run_ours(a):
                      "traffic": traffic,
                      "kernel": "k_dp_level", "avg_launch_ms": dp_ms / max(1, dp_launches),
                      "ops_per_step": ops / a.steps, "f_bar": f_bar,
+                     "scope": "rank 0: its own calls' unpruned visits over its own DP time",
                      "basis": "SURVEY 8(d): (2 + 4*F_bar) fp64 ops per unpruned visit",
                      "executed": {"achieved": achieved_exec,
                                   "frac": achieved_exec / peak.value if peak.value else None,

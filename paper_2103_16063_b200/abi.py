@@ -217,3 +217,63 @@ class PlanBuffers:
         return [(int(self.lo[i]), int(self.hi[i]), int(self.devices[i]),
                  float(self.t_fwd[i]), float(self.t_bwd[i]), int(self.mem[i]))
                 for i in range(n)]
+
+
+def struct_dtype(struct) -> np.dtype:
+    """numpy dtype with the exact field offsets of a ctypes Structure
+    (pointers as uint64), so arrays of records cross the ABI without a
+    Python loop."""
+    conv = {C.c_int32: np.int32, C.c_int64: np.int64, C.c_double: np.float64,
+            C.c_uint8: np.uint8}
+    names, formats, offsets = [], [], []
+    for name, ctype in struct._fields_:
+        names.append(name)
+        formats.append(conv.get(ctype, np.uint64))
+        offsets.append(getattr(struct, name).offset)
+    return np.dtype({"names": names, "formats": formats, "offsets": offsets,
+                     "itemsize": C.sizeof(struct)})
+
+
+PLAN_DTYPE = struct_dtype(PcPlan)
+CALL_RESULT_DTYPE = struct_dtype(PcCallResult)
+
+
+class PlanView:
+    """One call's stages inside a PlanArena (the PlanBuffers field names)."""
+
+    __slots__ = ("lo", "hi", "devices", "t_fwd", "t_bwd", "mem")
+
+    def __init__(self, arena, i):
+        a, b = int(arena.off[i]), int(arena.off[i + 1])
+        self.lo, self.hi, self.devices = arena.lo[a:b], arena.hi[a:b], arena.devices[a:b]
+        self.t_fwd, self.t_bwd, self.mem = arena.t_fwd[a:b], arena.t_bwd[a:b], arena.mem[a:b]
+
+
+class PlanArena:
+    """Plan outputs of a whole batch: one contiguous array per field and a
+    PcPlan record per call pointing into it (no per-call Python objects)."""
+
+    def __init__(self, caps):
+        caps = np.asarray(caps, np.int64)
+        self.n = len(caps)
+        self.off = np.zeros(self.n + 1, np.int64)
+        np.cumsum(caps, out=self.off[1:])
+        tot = max(int(self.off[-1]), 1)
+        self.lo = np.zeros(tot, np.int32)
+        self.hi = np.zeros(tot, np.int32)
+        self.devices = np.zeros(tot, np.int32)
+        self.t_fwd = np.zeros(tot, np.float64)
+        self.t_bwd = np.zeros(tot, np.float64)
+        self.mem = np.zeros(tot, np.int64)
+        self.rec = np.zeros(max(self.n, 1), PLAN_DTYPE)
+        r, o = self.rec[:self.n], self.off[:-1]
+        r["cap_stages"] = caps
+        for name in ("lo", "hi", "devices", "t_fwd", "t_bwd", "mem"):
+            arr = getattr(self, name)
+            r[name] = arr.ctypes.data + arr.itemsize * o
+
+    def ptr(self):
+        return self.rec.ctypes.data_as(C.POINTER(PcPlan))
+
+    def __getitem__(self, i):
+        return PlanView(self, i)

@@ -646,23 +646,44 @@ __global__ void k_visit_rows(DPBatch Bt, int pruning, const int64_t *call_row_pr
     atomicAdd((unsigned long long *)&level_sums[level_off[c] + s - 1], (unsigned long long)v);
 }
 
+// Level 1 carries d_min from row to row (stages.py:205-209, 247-248): one
+// warp per call walks the rows in order, each row scanned 32 cells per ballot
+// from the top for its first dead cell.
 __global__ void k_visit_level1(DPBatch Bt, int pruning, const int64_t *level_off,
                                int64_t *level_sums) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (c >= Bt.n_calls) return;
     const CallDesc cd = Bt.calls[c];
     const uint8_t *lvl = Bt.hist_cnt + cd.hist_off;
     int64_t total = 0;
     int d_min = 1;
     for (int bi = 0; bi < cd.A; ++bi) {
-        const int bottom = d_min > 1 ? d_min : 1;      // max(d_min, s) with s = 1
-        const int bottom_di = bottom - 1;
+        const int bottom_di = d_min - 1;               // max(d_min, s) - 1 with s = 1
         if (bottom_di > cd.B - 1) continue;            // empty d range: no visits
-        int dead;
-        total += row_visits(lvl + bi, cd.A, 1, 1 + bi, cd.B, bottom_di, pruning, &dead);
-        if (dead >= 0) d_min = dead + 1 + 1;           // d_min = d + 1, d = 1 + dead
+        int stop = bottom_di, dead = -1;
+        if (pruning) {
+            for (int top = cd.B - 1; top >= bottom_di; top -= 32) {
+                const int di = top - lane;
+                bool is_dead = false;
+                if (di >= bottom_di) {
+                    const uint8_t v = lvl[(int64_t)di * cd.A + bi];
+                    is_dead = (v & CNT_MASK) == 0 && !(v & CNT_ZERO);
+                }
+                const uint32_t m = __ballot_sync(0xffffffffu, is_dead);
+                if (m) {
+                    dead = top - (__ffs(m) - 1);
+                    stop = dead;
+                    break;
+                }
+            }
+        }
+        // sum_{di=stop}^{B-1} (b-s+1)(di+1), b - s + 1 = bi + 1
+        const int64_t a1 = stop + 1, z = cd.B;
+        total += (int64_t)(bi + 1) * ((z * (z + 1) - (a1 - 1) * a1) / 2);
+        if (dead >= 0) d_min = dead + 2;               // d_min = d + 1, d = 1 + dead
     }
-    level_sums[level_off[c]] = total;
+    if (lane == 0) level_sums[level_off[c]] = total;
 }
 
 void launch_row_visits(const DPBatch &b, int pruning, int64_t *level_sums, int64_t *row_prefix,
@@ -670,7 +691,7 @@ void launch_row_visits(const DPBatch &b, int pruning, int64_t *level_sums, int64
     if (n_rows_total > 0)
         k_visit_rows<<<(unsigned)((n_rows_total + 255) / 256), 256, 0, st>>>(
             b, pruning, row_prefix, level_off, level_sums);
-    k_visit_level1<<<(b.n_calls + 127) / 128, 128, 0, st>>>(b, pruning, level_off, level_sums);
+    k_visit_level1<<<(unsigned)((b.n_calls * 32 + 127) / 128), 128, 0, st>>>(b, pruning, level_off, level_sums);
 }
 
 // ---------------------------------------------------------------- backtrack (K4)

@@ -69,7 +69,8 @@ def lpt_shard(nb: int, calls, world: int):
 
 
 class BatchResult:
-    """Per-call records of one device batch (+ plan buffers)."""
+    """Per-call records of one device batch: `results` is a structured array
+    with the PcCallResult fields, `bufs[i]` the call's stage arrays."""
 
     def __init__(self, calls, results, bufs, stats):
         self.calls = calls
@@ -78,10 +79,10 @@ class BatchResult:
         self.stats = stats
 
     def feasible(self, i):
-        return bool(self.results[i].feasible)
+        return bool(self.results[i]["feasible"])
 
     def plan(self, i, batch_size) -> Plan | None:
-        if not self.results[i].feasible:
+        if not self.results[i]["feasible"]:
             return None
         S, D, R, MB = self.calls[i]
         buf = self.bufs[i]
@@ -91,7 +92,7 @@ class BatchResult:
                       t_bwd=float(buf.t_bwd[k]), mem=int(buf.mem[k]))
             for k in range(S))
         return Plan(stages=stages, microbatches=MB, replica_factor=R,
-                    objective=float(self.results[i].objective), batch_size=batch_size,
+                    objective=float(self.results[i]["objective"]), batch_size=batch_size,
                     devices_total=D)
 
 
@@ -100,18 +101,17 @@ def run_calls(ctx: _lib.Context, calls, batch_size: int, disable_pruning: bool =
     n = len(calls)
     if ctx.problem_flat is not None:
         bind_overrides(ctx, ctx.problem_flat, call_shares(calls, batch_size))
-    arr = (abi.PcCall * max(n, 1))(*[abi.PcCall(*c) for c in calls])
-    res = (abi.PcCallResult * max(n, 1))()
-    bufs = [abi.PlanBuffers(c[0]) for c in calls]
-    plans = (abi.PcPlan * max(n, 1))(*[b.s for b in bufs])
+    arr = np.ascontiguousarray(np.asarray(calls, np.int32).reshape(n, 4)) if n else np.zeros((1, 4), np.int32)
+    res = np.zeros(max(n, 1), abi.CALL_RESULT_DTYPE)
+    plans = abi.PlanArena([c[0] for c in calls])
     st = abi.PcStats()
     if n:
-        rc = ctx.lib.pc_run_calls(ctx.h, n, arr, batch_size, int(bool(disable_pruning)),
-                                  int(bool(want_iteration)), res, plans, C.byref(st))
+        rc = ctx.lib.pc_run_calls(ctx.h, n, arr.ctypes.data_as(C.POINTER(abi.PcCall)), batch_size,
+                                  int(bool(disable_pruning)), int(bool(want_iteration)),
+                                  res.ctypes.data_as(C.POINTER(abi.PcCallResult)), plans.ptr(),
+                                  C.byref(st))
         ctx.check(rc, "pc_run_calls")
-        for i in range(n):
-            bufs[i].s.n_stages = plans[i].n_stages
-    return BatchResult(calls, res, bufs, st)
+    return BatchResult(calls, res[:n], plans, st)
 
 
 def rank_key(iteration, objective, MB, index):
@@ -159,12 +159,12 @@ def _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels, max_stages
     best = {}
     for li, gi in enumerate(local_idx):
         r = batch.results[li]
-        rec[gi * _REC + 0] = r.visits
-        rec[gi * _REC + 1] = r.feasible
-        rec[gi * _REC + 2] = r.iteration_time
-        rec[gi * _REC + 3] = r.objective
-        if r.feasible:
-            key = rank_key(r.iteration_time, r.objective, calls[gi][3], gi)
+        rec[gi * _REC + 0] = r["visits"]
+        rec[gi * _REC + 1] = r["feasible"]
+        rec[gi * _REC + 2] = r["iteration_time"]
+        rec[gi * _REC + 3] = r["objective"]
+        if r["feasible"]:
+            key = rank_key(float(r["iteration_time"]), float(r["objective"]), calls[gi][3], gi)
             lv = levels[gi]
             if lv not in best or key < best[lv][0]:
                 best[lv] = (key, li, gi)
@@ -176,7 +176,7 @@ def _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels, max_stages
         rec[o] = 1
         rec[o + 1] = gi
         rec[o + 2] = S
-        rec[o + 3] = batch.results[li].objective
+        rec[o + 3] = batch.results[li]["objective"]
         k = o + 4
         rec[k:k + S] = buf.lo[:S]
         rec[k + S:k + 2 * S] = buf.hi[:S]

@@ -60,6 +60,9 @@ class _FakeRes:
         self.iteration_time = iteration
         self.visits = visits
 
+    def __getitem__(self, field):      # run_calls' results are a structured array
+        return getattr(self, field)
+
 
 class _FakeBuf:
     def __init__(self, S, rng):
