@@ -225,7 +225,7 @@ def run_ours(a):
     dev = torch.device("cuda", local)
 
     from paper_2103_16063_b200 import _lib
-    from paper_2103_16063_b200.search import (_pack, call_weight, decide, enumerate_calls,
+    from paper_2103_16063_b200.search import (device_weights, _pack, call_weight, decide, enumerate_calls,
                                               exchange, form_stage_sharded, lpt_shard,
                                               run_calls)
     from paper_2103_16063_b200.stages import bind_problem
@@ -239,7 +239,8 @@ def run_ours(a):
     nb = len(bs)
     calls, levels = enumerate_calls(nodes, dpn, BS, nb)
     unpruned = unpruned_visits(nb, calls)
-    owner = lpt_shard(nb, calls, world)
+    bind_problem(ctx, bs)
+    owner = lpt_shard(nb, calls, world, device_weights(ctx, calls, BS) if world > 1 else None)
     local_idx = [i for i in range(len(calls)) if owner[i] == rank]
     my_calls = [calls[i] for i in local_idx]
     n_levels = max(levels) + 1

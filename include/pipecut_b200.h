@@ -216,6 +216,13 @@ int pc_simulate(pc_ctx *ctx, const pc_plan *plan, int64_t batch_size, int32_t ev
                 int32_t *lane_off, int32_t *ev_mb, int8_t *ev_phase, double *ev_start,
                 double *ev_end, double *summary);
 
+/* Sharding weights for n calls (the LPT key of form_stage_sharded): per call
+ * S * sum_b sum_dev (B - dev + 1) * #{lo < b : span (lo, b) fits at the share
+ * of dev devices}, from the key tables (built for every call's shares).
+ * Exact integers: every rank computes the same assignment. */
+int pc_call_weights(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
+                    int64_t *weights);
+
 /* CostModel.profile over block spans: n queries (lo, hi, m, ckpt). */
 int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const int32_t *hi,
                      const int64_t *m, const int32_t *ckpt,

@@ -74,6 +74,7 @@ def load():
                                       C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_double)]
         lib.pc_simulate.argtypes = [C.c_void_p, P(PcPlan), C.c_int64, C.c_int32, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.pc_call_weights.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]
         lib.pc_reset_cache.argtypes = [C.c_void_p]
         lib.pc_timer_start.argtypes = [C.c_void_p]
         lib.pc_timer_stop.argtypes = [C.c_void_p, P(C.c_double)]
@@ -82,7 +83,7 @@ def load():
                      "pc_form_stage_dp", "pc_run_calls", "pc_last_crossing", "pc_form_stage",
                      "pc_reset_cache", "pc_timer_start", "pc_timer_stop",
                      "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides",
-                     "pc_brute_force", "pc_check_plan", "pc_simulate"):
+                     "pc_brute_force", "pc_check_plan", "pc_simulate", "pc_call_weights"):
             getattr(lib, name).restype = C.c_int
         _lib = lib
         return lib
@@ -92,7 +93,7 @@ EXPORTS = ("pc_ctx_create", "pc_ctx_destroy", "pc_last_error", "pc_device_info",
            "pc_set_problem", "pc_profile_spans", "pc_form_stage_dp", "pc_run_calls",
            "pc_last_crossing", "pc_form_stage", "pc_reset_cache", "pc_timer_start",
            "pc_timer_stop", "pc_measure_fp64_peak", "pc_partition_blocks", "pc_set_overrides",
-           "pc_brute_force", "pc_check_plan", "pc_simulate")
+           "pc_brute_force", "pc_check_plan", "pc_simulate", "pc_call_weights")
 
 
 class Context:

@@ -1362,6 +1362,59 @@ extern "C" int pc_simulate(pc_ctx *ctx, const pc_plan *plan, int64_t batch_size,
     return PC_OK;
 }
 
+// Sharding weights: per call, a feasible-pair count from the key tables,
+// S * sum_b sum_dev (B - dev + 1) * #{lo < b : span (lo, b) fits at share(dev)}
+// (the first feasible lo per (key, hi) is already in the table).  Exact
+// integers, so every rank derives the same assignment.
+extern "C" int pc_call_weights(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
+                               int64_t *weights) {
+    if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
+    cudaSetDevice(ctx->device);
+    if (n <= 0) return PC_OK;
+    const DevProblem &P = ctx->P;
+    std::vector<std::pair<int64_t, int>> want;
+    std::vector<int32_t> koff(n + 1, 0);
+    std::vector<std::pair<int64_t, int>> flat_keys;
+    for (int i = 0; i < n; ++i) {
+        if (int rc = validate_call(ctx, calls[i], batch_size)) return rc;
+        const int ckpt = P.checkpointing && calls[i].S > 1;
+        const int B = calls[i].D - calls[i].S + 1;
+        koff[i + 1] = koff[i] + B + 1;
+        for (int dev = 0; dev <= B; ++dev) {
+            const int64_t m = dev >= 1 ? batch_size / ((int64_t)calls[i].MB * calls[i].R * dev) : 0;
+            flat_keys.push_back(m >= 1 ? std::make_pair(m, ckpt) : std::make_pair((int64_t)0, -1));
+            if (m >= 1) want.push_back({m, ckpt});
+        }
+    }
+    std::sort(want.begin(), want.end());
+    want.erase(std::unique(want.begin(), want.end()), want.end());
+    if (int rc = ensure_keys(ctx, want)) return rc;
+    std::vector<int16_t> keyidx(flat_keys.size(), -1);
+    for (size_t q = 0; q < flat_keys.size(); ++q)
+        if (flat_keys[q].second >= 0) keyidx[q] = (int16_t)ctx->key_map[flat_keys[q]];
+    const size_t c_bytes = sizeof(pc_call) * (size_t)n, o_bytes = 4 * (size_t)(n + 1);
+    const size_t k_bytes = 2 * keyidx.size(), w_bytes = 8 * (size_t)n;
+    const size_t off_o = (c_bytes + 255) & ~size_t(255);
+    const size_t off_k = (off_o + o_bytes + 255) & ~size_t(255);
+    const size_t off_w = (off_k + k_bytes + 255) & ~size_t(255);
+    CUDA_TRY(ctx, ctx->bf_d.ensure(off_w + w_bytes + 64));
+    char *base = ctx->bf_d.as<char>();
+    CUDA_TRY(ctx, cudaMemcpyAsync(base, calls, c_bytes, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(base + off_o, koff.data(), o_bytes, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(base + off_k, keyidx.data(), k_bytes, cudaMemcpyHostToDevice, ctx->st));
+    CUDA_TRY(ctx, cudaMemsetAsync(base + off_w, 0, w_bytes, ctx->st));
+    const size_t nk = ctx->keys.size();
+    launch_call_weights(ctx->nb, n, (const int32_t *)base, (const int32_t *)(base + off_o),
+                        (const int16_t *)(base + off_k),
+                        ((const int32_t *const *)ctx->key_ptrs.p) + 3 * nk,
+                        (unsigned long long *)(base + off_w), ctx->st);
+    ctx->launches++;
+    if (int rc = check_launch(ctx, "call_weights")) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(weights, base + off_w, w_bytes, cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    return PC_OK;
+}
+
 extern "C" int pc_reset_cache(pc_ctx *ctx) {
     cudaSetDevice(ctx->device);
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));

@@ -221,6 +221,9 @@ void launch_first_feasible(int nb, int n_keys, const double *const *tf, int32_t 
 void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
                             const int64_t *m, const int32_t *ckpt, double *tf, double *tb,
                             int64_t *mem, cudaStream_t st);
+void launch_call_weights(int nb, int n, const int32_t *calls, const int32_t *koff,
+                         const int16_t *keyidx, const int32_t *const *ffb, unsigned long long *w,
+                         cudaStream_t st);
 // dp.cu
 void launch_cta_call(const int64_t *prefix, int n, int64_t total, int32_t *out, cudaStream_t st);
 void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool derived,

@@ -269,4 +269,33 @@ void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const
     k_profile_queries<<<(n + 127) / 128, 128, 0, st>>>(p, n, lo, hi, m, ckpt, tf, tb, mem);
 }
 
+// ---------------------------------------------------------------- sharding weights
+// Thread per (call, b): sum over device counts of the feasible predecessor
+// count b - ffb(key(dev))[b], weighted by the (d, d') pairs with that count.
+__global__ void k_call_weights(int nb, int n, const int32_t *calls, const int32_t *koff,
+                               const int16_t *keyidx, const int32_t *const *ffb,
+                               unsigned long long *w) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)n * nb) return;
+    const int c = (int)(g / nb);
+    const int b = 1 + (int)(g % nb);
+    const int S = calls[4 * c], D = calls[4 * c + 1];
+    const int B = D - S + 1;
+    unsigned long long acc = 0;
+    for (int dev = 1; dev <= B; ++dev) {
+        const int kk = keyidx[koff[c] + dev];
+        if (kk < 0) continue;
+        const int f = b - ffb[kk][b];
+        if (f > 0) acc += (unsigned long long)(B - dev + 1) * (unsigned long long)f;
+    }
+    if (acc) atomicAdd(&w[c], acc * (unsigned long long)S);
+}
+
+void launch_call_weights(int nb, int n, const int32_t *calls, const int32_t *koff,
+                         const int16_t *keyidx, const int32_t *const *ffb, unsigned long long *w,
+                         cudaStream_t st) {
+    const int64_t t = (int64_t)n * nb;
+    if (t > 0) k_call_weights<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(nb, n, calls, koff, keyidx, ffb, w);
+}
+
 }  // namespace pcb

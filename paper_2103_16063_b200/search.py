@@ -56,16 +56,32 @@ def call_weight(nb: int, call) -> int:
     return S * (A * (A + 1) // 2) * (B * (B + 1) // 2)
 
 
-def lpt_shard(nb: int, calls, world: int):
-    """Owner rank per call: longest-processing-time first, deterministic."""
-    order = sorted(range(len(calls)), key=lambda i: (-call_weight(nb, calls[i]), i))
+def lpt_shard(nb: int, calls, world: int, weights=None):
+    """Owner rank per call: longest-processing-time first, deterministic.
+    ``weights`` (device_weights) default to the closed-form visit count."""
+    w = list(weights) if weights is not None else [call_weight(nb, c) for c in calls]
+    order = sorted(range(len(calls)), key=lambda i: (-w[i], i))
     heap = [(0, r) for r in range(world)]
     owner = [0] * len(calls)
     for i in order:
         load, r = heapq.heappop(heap)
         owner[i] = r
-        heapq.heappush(heap, (load + call_weight(nb, calls[i]) + 1, r))
+        heapq.heappush(heap, (load + int(w[i]) + 1, r))
     return owner
+
+
+def device_weights(ctx: _lib.Context, calls, batch_size: int):
+    """Feasible-pair sharding weights from the device key tables
+    (pc_call_weights); identical on every rank."""
+    n = len(calls)
+    if ctx.problem_flat is not None:
+        bind_overrides(ctx, ctx.problem_flat, call_shares(calls, batch_size))
+    out = np.zeros(max(n, 1), np.int64)
+    if n:
+        arr = np.ascontiguousarray(np.asarray(calls, np.int32).reshape(n, 4))
+        ctx.check(ctx.lib.pc_call_weights(ctx.h, n, arr.ctypes.data, batch_size, out.ctypes.data),
+                  "pc_call_weights")
+    return out[:n].tolist()
 
 
 class BatchResult:
@@ -261,7 +277,8 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
     nb = len(blocks)
     calls, levels = enumerate_calls(num_nodes, devices_per_node, batch_size, nb)
     n_levels = (max(levels) + 1) if levels else 0
-    owner = lpt_shard(nb, calls, world)
+    owner = lpt_shard(nb, calls, world,
+                      device_weights(ctx, calls, batch_size) if world > 1 else None)
     local_idx = [i for i in range(len(calls)) if owner[i] == rank]
     batch = run_calls(ctx, [calls[i] for i in local_idx], batch_size,
                       opts.disable_pruning, True)
