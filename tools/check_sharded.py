@@ -50,6 +50,21 @@ for budget in (2, 20, 45, 80):
             return ("budget", e.visits)
     same = run(form_stage_sharded) == run(pc.form_stage)
     ok &= same
+# measured cost tables: golden form_stage of the reference (tests/golden/cost_tables.json)
+import random  # noqa: E402
+
+rng = random.Random(4242)
+n_ct = 0
+for rec in json.load(open(os.path.join(ROOT, "tests", "golden", "cost_tables.json"))):
+    part, model, k, (nodes, dpn, S, D, BS, R, MB) = cases.cost_table_instance(rng)
+    if "error" in rec:
+        continue
+    bs = partition_blocks(part, model, k)
+    same = result_doc(form_stage_sharded(nodes, dpn, BS, bs)) == rec["form_stage"]
+    ok &= same
+    n_ct += same
+if rank == 0:
+    print(f"cost tables: {n_ct} sharded searches == golden", flush=True)
 t = torch.tensor([1 if ok else 0], device="cuda")
 dist.all_reduce(t, op=dist.ReduceOp.MIN)
 if rank == 0:
