@@ -26,6 +26,8 @@ import subprocess
 import sys
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -115,14 +117,14 @@ def _ref_worker_init(nb, D):
 
 class _Deadline:
     """SearchOptions-compatible options for the unmodified reference: pruning
-    off, and `visit_budget` None until the deadline, then -1 -- the reference's
-    own per-cell check (stages.py:214-216) then raises SearchBudgetExceeded
-    carrying the exact visit count reached."""
+    off (the metric's unit) or on (its stock default), and `visit_budget` None
+    until the deadline, then -1 -- the reference's own per-cell check
+    (stages.py:214-216) then raises SearchBudgetExceeded carrying the exact
+    visit count reached."""
 
-    disable_pruning = True
-
-    def __init__(self, seconds):
+    def __init__(self, seconds, disable_pruning=True):
         self._end = time.perf_counter() + seconds
+        self.disable_pruning = disable_pruning
 
     @property
     def visit_budget(self):
@@ -133,10 +135,11 @@ def _ref_run(args):
     """The reference's own form_stage_dp on one call of the workload for about
     `seconds` of wall time; returns (visits, seconds)."""
     import pipecut
-    (S, D, R, MB), bs_batch, seconds = args
+    (S, D, R, MB), bs_batch, seconds = args[:3]
+    unpruned = args[3] if len(args) > 3 else True
     t0 = time.perf_counter()
     try:
-        res = pipecut.form_stage_dp(_REF_BS, S, D, bs_batch, R, MB, _Deadline(seconds))
+        res = pipecut.form_stage_dp(_REF_BS, S, D, bs_batch, R, MB, _Deadline(seconds, unpruned))
         visits = res.stats.visits
     except pipecut.SearchBudgetExceeded as exc:
         visits = exc.visits
@@ -152,11 +155,11 @@ class RefSampler:
     """Reference visits/s on `cores` host processes, each running one call of
     the workload (calls spread over the enumeration) for `seconds`."""
 
-    def __init__(self, nb, D, calls, seconds, cores):
+    def __init__(self, nb, D, calls, seconds, cores, unpruned=True):
         import multiprocessing as mp
         self.cores = cores
         self.calls = sample_calls(calls, cores)
-        self.work = [(c, 8 * D, seconds) for c in self.calls]
+        self.work = [(c, 8 * D, seconds, unpruned) for c in self.calls]
         if cores == 1:
             _ref_worker_init(nb, D)
             self.pool = None
@@ -193,6 +196,9 @@ def run_reference_arm(a):
             rates.append(r)
     sampler.close()
     value = sorted(rates)[len(rates) // 2]
+    stock_sampler = RefSampler(a.nb, a.D, calls, per_step, cores, unpruned=False)
+    stock = stock_sampler.rate()
+    stock_sampler.close()
     sample = (f"{cores} processes x one call of the workload each (calls spread over the "
               f"enumeration), the reference's pipecut.form_stage_dp with pruning off, each "
               f"stopped after ~{per_step:.0f} s by its own visit-budget check; "
@@ -204,7 +210,12 @@ def run_reference_arm(a):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(a.nb, a.D, calls, unpruned_visits(a.nb, calls)),
         "cpu_baseline": {"value": value, "unit": "visits/s", "cores": cores,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample,
+                         "stock_path": {"pruned_visits_per_sec": stock,
+                                        "note": "same workers, the reference's default options "
+                                                "(pruning on); rate in its own pruned visits. "
+                                                "Bounded samples start at level 1 (O(1) per cell, "
+                                                "up to b*d visits), which favours the reference"}},
         "e2e": {"value": value, "unit": "visits/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -281,7 +292,7 @@ def run_ours(a):
         allrec = exchange(rec, None, dev)
         out = decide(allrec, calls, levels, owner, plan_w, None, BS)
         ms = stop()
-        last.update(stats=batch.stats, result=out[1])
+        last.update(stats=batch.stats, result=out[1], stats_visits=batch.results["visits"].copy())
         return max_over_ranks(ms)
 
     for _ in range(a.warmup):
@@ -383,11 +394,26 @@ def run_ours(a):
     if world == 1 and not a.no_cpu_baseline:
         sampler = RefSampler(nb, a.D, calls, a.cpu_sample_sec, 1)
         rate = sampler.rate()
+        # the reference's stock path (pruning on, its default) on the same call:
+        # its own pruned visits/s, and the time-to-solution equivalent in the
+        # metric's unit via this workload's exact unpruned/pruned ratio (the
+        # pruned count per call is the reference's, reproduced bit-exactly)
+        stock = RefSampler(nb, a.D, calls, a.cpu_sample_sec / 2, 1, unpruned=False).rate()
+        pruned_total = int(np.asarray(last["stats_visits"]).sum())
+        ratio = unpruned / pruned_total if pruned_total else None
         line["cpu_baseline"] = {
             "value": rate, "unit": "visits/s", "cores": 1, "kind": "reference",
             "sample": f"reference pipecut.form_stage_dp (baseline/_ref, unmodified) on one call "
                       f"{sampler.calls[0]} of the workload with pruning off, stopped after "
-                      f"~{a.cpu_sample_sec:.0f} s by its own visit-budget check; single thread"}
+                      f"~{a.cpu_sample_sec:.0f} s by its own visit-budget check; single thread",
+            "stock_path": {
+                "pruned_visits_per_sec": stock, "unpruned_per_pruned": ratio,
+                "equivalent_visits_per_sec": stock * ratio if ratio else None,
+                "note": "reference default options (pruning on), same call, "
+                        f"~{a.cpu_sample_sec / 2:.0f} s; equivalent = pruned rate x the "
+                        "workload's unpruned/pruned visit ratio. Bounded samples start at "
+                        "level 1, where a cell costs O(1) but counts up to b*d visits, so "
+                        "sampled CPU rates favour the reference"}}
     if not a.no_latency and world == 1:
         line["latency_ms"] = config_latencies(ctx)
     print(json.dumps(line), flush=True)
