@@ -1,0 +1,77 @@
+"""Edge cases of the stage search on the device, checked against the C oracle
+(pinned to the reference in test_oracle.py): a single block, zero-share
+calls, budgets nothing fits, one device per stage, very wide device ranges,
+and capacity limits that must raise rather than truncate."""
+
+import pytest
+
+import cases
+from oracle.oracle import OracleProblem, PC_OK
+from paper_2103_16063_b200 import brute_force_partition, form_stage, form_stage_dp
+from paper_2103_16063_b200._host import pipecut as pc
+from paper_2103_16063_b200._lib import DeviceError
+from paper_2103_16063_b200.flatten import flatten_blockset
+
+pytestmark = pytest.mark.gpu
+
+
+def _dp_matches_oracle(bs, S, D, BS, R, MB):
+    op = OracleProblem(flatten_blockset(bs))
+    for prune in (True, False):
+        res = form_stage_dp(bs, S, D, BS, R, MB, pc.SearchOptions(disable_pruning=not prune))
+        rc, stages, obj, visits = op.form_stage_dp(S, D, BS, R, MB, disable_pruning=not prune)
+        assert res.stats.visits == visits, (S, D, BS, R, MB, prune)
+        if rc == PC_OK:
+            got = [(s.blocks[0], s.blocks[1], s.devices, s.t_fwd, s.t_bwd, s.mem)
+                   for s in res.plan.stages]
+            assert got == stages and res.plan.objective == obj
+        else:
+            assert res.plan is None
+
+
+def test_single_block(gpu):
+    bs = cases.one_block_per_task(cases.chain([2.0], params=[512]), dpn=4)
+    assert len(bs) == 1
+    for D in (1, 2, 4):
+        for R, MB in ((1, 1), (2, 1), (1, 8)):
+            _dp_matches_oracle(bs, 1, D, 16, R, MB)
+    res = form_stage(1, 4, 16, bs)
+    rc, want, visits, calls = OracleProblem(flatten_blockset(bs)).form_stage(1, 4, 16)
+    assert res.plan.objective == want["objective"] and res.stats.visits == visits
+    assert brute_force_partition(bs, 1, 4, 16, 1, 1).plan.objective == \
+        form_stage_dp(bs, 1, 4, 16, 1, 1).plan.objective
+
+
+def test_zero_share_calls(gpu):
+    # MB * R * dev > batch: every (or every wide) stage gets m == 0 (stages.py:224-228)
+    bs = cases.one_block_per_task(cases.chain([1.0, 2.0, 1.5, 1.0], sizes=[64] * 4), dpn=6)
+    for S, D, BS, R, MB in ((2, 6, 4, 1, 4), (2, 6, 4, 2, 2), (1, 6, 2, 1, 4), (3, 6, 6, 1, 2),
+                            (2, 6, 1, 1, 1), (4, 6, 8, 2, 1)):
+        _dp_matches_oracle(bs, S, D, BS, R, MB)
+
+
+def test_budget_nothing_fits(gpu):
+    g = cases.chain([1.0, 1.0, 1.0], sizes=[4096] * 3, params=[1 << 20] * 3)
+    for mem in (1 << 22, 5 << 20, 9 << 20):
+        try:
+            bs = cases.one_block_per_task(g, mem=mem, dpn=4, ckpt=True)
+        except pc.InfeasibleAtom:
+            continue
+        for S in (1, 2, 3):
+            _dp_matches_oracle(bs, S, 4, 64, 1, 2)
+            _dp_matches_oracle(bs, S, 4, 64, 2, 8)
+
+
+def test_one_device_per_stage_and_wide_ranges(gpu):
+    bs = cases.c5_blockset(12, 8, jitter_seed=4)
+    for S in (1, 6, 8):
+        _dp_matches_oracle(bs, S, S, 8 * S, 1, 1)           # D == S: one device each
+    wide = cases.c5_blockset(6, 512, jitter_seed=5)
+    for S, D in ((2, 300), (3, 512), (6, 512)):
+        _dp_matches_oracle(wide, S, D, 8 * D, 1, 4)
+
+
+def test_capacity_limits_raise(gpu):
+    bs = cases.c5_blockset(4, 8)
+    with pytest.raises(DeviceError):
+        form_stage_dp(bs, 2, 4096, 8 * 4096, 1, 1)           # D beyond the packed key range
