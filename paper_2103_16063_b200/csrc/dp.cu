@@ -324,21 +324,52 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                         }
                     }
                 }
-                const int rounds = (int)__reduce_max_sync(0xffffffffu, (unsigned)(whi - wlo + 1));
+                // Candidate work items (lane, window entry) compacted over the
+                // warp: 32 per round whatever the lanes' window sizes (an
+                // exclusive prefix over the lanes, then a 5-step shuffle search
+                // for each item's owner).  The frontier does not depend on the
+                // order candidates arrive in.
+                const int cntw = whi - wlo + 1;
+                int incl = cntw;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                const int excl = incl - cntw;
+                const uint32_t pb32 = (uint32_t)pbase;           // pool offsets < 2^31
+                const int spill = etf == stf ? 1 : 0;
                 if (PC_DP_DIAG) {
-                    n_win += whi - wlo + 1;
-                    n_rounds += rounds;
+                    n_win += cntw;
+                    n_rounds += (total + 31) / 32;
                     ++n_iters;
                 }
-                for (int r = 0; r < rounds; ++r) {
-                    const int i = wlo + r;
+                for (int q0 = 0; q0 < total; q0 += 32) {
+                    const int q = q0 + lane;
+                    int ow = 0;                                  // lanes with incl <= q
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) {
+                        const int v = __shfl_sync(0xffffffffu, incl, ow + st - 1);
+                        if (v <= q) ow += st;
+                    }
+                    const int o_excl = __shfl_sync(0xffffffffu, excl, ow);
+                    const int o_wlo = __shfl_sync(0xffffffffu, wlo, ow);
+                    const double o_tfc = __shfl_sync(0xffffffffu, tfc, ow);
+                    const double o_tbc = __shfl_sync(0xffffffffu, tbc, ow);
+                    const uint32_t o_pb = __shfl_sync(0xffffffffu, pb32, ow);
+                    const int o_sp = __shfl_sync(0xffffffffu, spill, ow);
+                    const int o_bp = __shfl_sync(0xffffffffu, bp, ow);
                     double cx = 0.0, cy = 0.0;
                     uint32_t ck = 0;
                     bool surv = false;
-                    if (i <= whi) {
-                        cx = dmax_ref(etf[pbase + i], tfc);
-                        cy = dmax_ref(etb[pbase + i], tbc);
-                        ck = pack_key(bp, dp, i);
+                    if (q < total) {
+                        const int i = o_wlo + (q - o_excl);
+                        const double *xt = o_sp ? stf : qtf;
+                        const double *yt = o_sp ? stb : qtb;
+                        cx = dmax_ref(xt[o_pb + i], o_tfc);
+                        cy = dmax_ref(yt[o_pb + i], o_tbc);
+                        ck = pack_key(o_bp, dp, i);
                         surv = n == 0 || !front_dominated(F, n, cx, cy, ck);
                     }
                     while (__any_sync(0xffffffffu, surv)) {
