@@ -314,11 +314,14 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                         else {
                             // exact window: entries with ptf <= tfc collapse onto the
                             // last of them, entries with ptb <= tbc onto the first
-                            int i0 = -1, i1 = cnt;
-                            for (int i = 0; i < cnt; ++i) {
-                                if (etf[pbase + i] <= tfc) i0 = i;
-                                if (i1 == cnt && etb[pbase + i] <= tbc) i1 = i;
+                            // (ptf strictly ascending, ptb strictly descending:
+                            // two branch-free binary searches)
+                            int c0 = 0, c1 = 0;   // #{ptf <= tfc}, #{ptb > tbc}
+                            for (int st = 1 << (log2_steps(cnt) - 1); st > 0; st >>= 1) {
+                                if (c0 + st <= cnt && etf[pbase + c0 + st - 1] <= tfc) c0 += st;
+                                if (c1 + st <= cnt && etb[pbase + c1 + st - 1] > tbc) c1 += st;
                             }
+                            const int i0 = c0 - 1, i1 = c1;
                             if (i1 <= i0) { wlo = i1; whi = i1; }
                             else { wlo = i0 < 0 ? 0 : i0; whi = i1 < cnt ? i1 : cnt - 1; }
                         }
