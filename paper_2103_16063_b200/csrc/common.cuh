@@ -139,9 +139,10 @@ struct CallDesc {
     int32_t pad;
 };
 
-// Warps (cells) per CTA of the level kernel: 4 warps x 10 CTAs per SM
-// (48 registers) measured 11% faster than 8 x 4 on the C5 bench -- small CTAs
-// free their slot as soon as their few cells finish, and more of them fit
+// Warps (cells) per CTA of the level kernel: 4 warps x 8 CTAs per SM (64
+// registers, DP_MIN_BLOCKS in dp.cu) -- small CTAs free their slot as soon as
+// their few cells finish; the occupancy/register split is re-measured whenever
+// the kernel changes (tuning log)
 #ifndef PC_DP_WARPS
 #define PC_DP_WARPS 4
 #endif
