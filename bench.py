@@ -292,16 +292,19 @@ def run_ours(a):
         allrec = exchange(rec, None, dev)
         out = decide(allrec, calls, levels, owner, plan_w, None, BS)
         ms = stop()
-        last.update(stats=batch.stats, result=out[1], stats_visits=batch.results["visits"].copy())
+        last.update(stats=batch.stats, result=out[1], stats_visits=batch.results["visits"].copy(),
+                    own_ms=ms)
         return max_over_ranks(ms)
 
     for _ in range(a.warmup):
         step_resident()
     times = []
     pairs = cands = dp_ms = span_ms = launches = dp_launches = 0
+    own_ms = 0.0
     with Clocks(local) as clk:
         for _ in range(a.steps):
             times.append(step_resident())
+            own_ms += last["own_ms"]
             st = last["stats"]
             pairs += st.pairs
             cands += st.candidates
@@ -310,6 +313,10 @@ def run_ours(a):
             launches += st.kernel_launches
             dp_launches += st.dp_launches
     ms_per_step = sum(times) / len(times)
+    if os.environ.get("PIPECUT_BENCH_VERBOSE"):
+        print(f"[rank {rank}] own step ms {own_ms / a.steps:.1f}, max-over-ranks {ms_per_step:.1f}, "
+              f"dp {dp_ms / a.steps:.1f}, span {span_ms / a.steps:.1f}, calls {len(my_calls)}",
+              file=sys.stderr, flush=True)
     value = unpruned / (ms_per_step / 1e3)
     result = last["result"]
 
