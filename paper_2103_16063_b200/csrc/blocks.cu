@@ -298,10 +298,27 @@ struct Coarsener {
     const pc_atoms *H;
     DevAtoms A{};
     int n;
-    DBuf atoms_d, lev_grp, lev_off, lev_at, sets_d, scratch_d, out_d, comp_d, mv_d;
-    int lev_cap = 0;
+    // device buffers and pinned level staging live in the context (cb)
+    DBuf &atoms_d, &lev_grp, &lev_off, &lev_at, &sets_d, &scratch_d, &out_d, &comp_d, &mv_d;
+    int &lev_cap;
+    int32_t *&pin;                    // [lev_cap][3n + 1] (grp | off | at)
+    std::vector<char> dirty;          // host level differs from its device copy
     std::vector<std::vector<std::vector<int>>> levels;
     std::vector<double> atom_comp;
+
+    Coarsener(pc_ctx *c, const pc_atoms *h)
+        : ctx(c), H(h), n(h->n), atoms_d(c->cb.atoms_d), lev_grp(c->cb.lev_grp),
+          lev_off(c->cb.lev_off), lev_at(c->cb.lev_at), sets_d(c->cb.sets_d),
+          scratch_d(c->cb.scratch_d), out_d(c->cb.out_d), comp_d(c->cb.comp_d), mv_d(c->cb.mv_d),
+          lev_cap(c->cb.lev_cap), pin(c->cb.pin) {
+        if (c->cb.lev_n != n) {          // slot layout depends on n
+            cudaStreamSynchronize(c->st);
+            lev_cap = 0;
+            if (pin) cudaFreeHost(pin);
+            pin = nullptr;
+            c->cb.lev_n = n;
+        }
+    }
 
     int upload_atoms() {
         struct Part { const void *src; size_t bytes; size_t off; };
@@ -378,38 +395,50 @@ struct Coarsener {
         return DevLevels{lev_grp.as<int32_t>(), lev_off.as<int32_t>(), lev_at.as<int32_t>(), n};
     }
 
-    // copy level `l` (list of ascending atom groups) into device slot l
+    // copy level `l` (list of ascending atom groups) into device slot l: the
+    // level's pinned staging slot is only rewritten after a later sync, so the
+    // copies stay asynchronous
     int upload_level(int l, const std::vector<std::vector<int>> &groups) {
+        const size_t per = 3 * (size_t)n + 1;
         if (l >= lev_cap) {
+            CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
             int cap = std::max(16, 2 * (l + 1));
             DBuf g2, o2, a2;
             CUDA_TRY(ctx, g2.ensure(sizeof(int32_t) * (size_t)cap * n));
             CUDA_TRY(ctx, o2.ensure(sizeof(int32_t) * (size_t)cap * (n + 1)));
             CUDA_TRY(ctx, a2.ensure(sizeof(int32_t) * (size_t)cap * n));
+            int32_t *p2 = nullptr;
+            CUDA_TRY(ctx, cudaMallocHost(&p2, sizeof(int32_t) * per * cap));
             if (lev_cap) {
                 CUDA_TRY(ctx, cudaMemcpy(g2.p, lev_grp.p, sizeof(int32_t) * (size_t)lev_cap * n, cudaMemcpyDeviceToDevice));
                 CUDA_TRY(ctx, cudaMemcpy(o2.p, lev_off.p, sizeof(int32_t) * (size_t)lev_cap * (n + 1), cudaMemcpyDeviceToDevice));
                 CUDA_TRY(ctx, cudaMemcpy(a2.p, lev_at.p, sizeof(int32_t) * (size_t)lev_cap * n, cudaMemcpyDeviceToDevice));
             }
+            if (pin) cudaFreeHost(pin);
+            pin = p2;
             std::swap(lev_grp.p, g2.p); std::swap(lev_grp.n, g2.n);
             std::swap(lev_off.p, o2.p); std::swap(lev_off.n, o2.n);
             std::swap(lev_at.p, a2.p); std::swap(lev_at.n, a2.n);
             lev_cap = cap;
         }
-        std::vector<int32_t> grp(n, -1), off(n + 1, 0), at;
-        at.reserve(n);
+        int32_t *grp = pin + per * l, *off = grp + n, *at = off + n + 1;
+        std::fill(grp, grp + n, -1);
+        off[0] = 0;
+        int32_t pos = 0;
         for (size_t g = 0; g < groups.size(); ++g) {
             for (int x : groups[g]) {
                 grp[x] = (int32_t)g;
-                at.push_back(x);
+                at[pos++] = x;
             }
-            off[g + 1] = (int32_t)at.size();
+            off[g + 1] = pos;
         }
-        for (size_t g = groups.size(); g < (size_t)n; ++g) off[g + 1] = off[groups.size()];
-        at.resize(n, 0);
-        CUDA_TRY(ctx, cudaMemcpy(lev_grp.as<int32_t>() + (size_t)l * n, grp.data(), 4 * (size_t)n, cudaMemcpyHostToDevice));
-        CUDA_TRY(ctx, cudaMemcpy(lev_off.as<int32_t>() + (size_t)l * (n + 1), off.data(), 4 * (size_t)(n + 1), cudaMemcpyHostToDevice));
-        CUDA_TRY(ctx, cudaMemcpy(lev_at.as<int32_t>() + (size_t)l * n, at.data(), 4 * (size_t)n, cudaMemcpyHostToDevice));
+        for (size_t g = groups.size(); g < (size_t)n; ++g) off[g + 1] = pos;
+        for (int32_t q = pos; q < n; ++q) at[q] = 0;
+        CUDA_TRY(ctx, cudaMemcpyAsync(lev_grp.as<int32_t>() + (size_t)l * n, grp, 4 * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(lev_off.as<int32_t>() + (size_t)l * (n + 1), off, 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
+        CUDA_TRY(ctx, cudaMemcpyAsync(lev_at.as<int32_t>() + (size_t)l * n, at, 4 * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
+        if ((int)dirty.size() <= l) dirty.resize(l + 1, 0);
+        dirty[l] = 0;
         return PC_OK;
     }
 
@@ -455,6 +484,14 @@ struct Coarsener {
         const int nm = (int)mv.size();
         out.assign(nm, 0);
         if (!nm) return PC_OK;
+        if (int rc = savings_async(mv, out)) return rc;
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        return PC_OK;
+    }
+
+    // launch + async read-back into out (sized by the caller); no sync
+    int savings_async(const std::vector<MoveDesc> &mv, std::vector<int64_t> &out) {
+        const int nm = (int)mv.size();
         CUDA_TRY(ctx, mv_d.ensure(sizeof(MoveDesc) * nm + 8 * (size_t)nm + 64));
         MoveDesc *dm = mv_d.as<MoveDesc>();
         int64_t *ds = (int64_t *)(((uintptr_t)(dm + nm) + 15) & ~uintptr_t(15));
@@ -463,8 +500,17 @@ struct Coarsener {
         ctx->launches++;
         if (int rc = check_launch(ctx, "move_savings")) return rc;
         CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), ds, 8 * (size_t)nm, cudaMemcpyDeviceToHost, ctx->st));
-        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
         return PC_OK;
+    }
+
+    // k_eval_sets and k_move_savings of one speculative round, one sync
+    int eval_moves(const std::vector<SetDesc> &sets, const std::vector<MoveDesc> &mv,
+                   std::vector<int64_t> &mem, std::vector<int32_t> &count,
+                   std::vector<uint8_t> &convex, std::vector<int64_t> &sav) {
+        sav.assign(mv.size(), 0);
+        if (!mv.empty())
+            if (int rc = savings_async(mv, sav)) return rc;
+        return eval(sets, mem, count, convex);      // synchronises the stream
     }
 
     int profiles(int l, int ngroups, bool single, std::vector<double> &tf, std::vector<double> &tb,
@@ -512,10 +558,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
     if (k < 1) return fail(ctx, PC_ERR_INVALID, "k must be at least 1");
     if (H->n < 1) return fail(ctx, PC_ERR_INVALID, "no atoms");
     cudaSetDevice(ctx->device);
-    Coarsener co;
-    co.ctx = ctx;
-    co.H = H;
-    co.n = H->n;
+    Coarsener co(ctx, H);
     const int n = H->n;
     const int64_t budget = H->budget;
     if (int rc = co.upload_atoms()) return rc;
@@ -632,7 +675,8 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         size_t p = 0;
         while (p < pairs.size()) {
             for (int l = li; l <= top; ++l)
-                if (int rc = co.upload_level(l, co.levels[l])) return rc;
+                if (co.dirty[l])
+                    if (int rc = co.upload_level(l, co.levels[l])) return rc;
             std::vector<std::vector<int>> maps(top + 1);
             for (int l = li; l <= top; ++l) maps[l] = member_map(n, co.levels[l]);
             struct Tri { int q, mi, ti, mv; int64_t set0; };
@@ -665,8 +709,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
             std::vector<int64_t> smem, sav;
             std::vector<int32_t> scount;
             std::vector<uint8_t> sconv;
-            if (int rc = co.eval(sets, smem, scount, sconv)) return rc;
-            if (int rc = co.savings(moves, sav)) return rc;
+            if (int rc = co.eval_moves(sets, moves, smem, scount, sconv, sav)) return rc;
             const int nlev = top - li;
             bool applied = false;
             size_t ti_ptr = 0;
@@ -709,6 +752,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
                         std::sort(gr.begin(), gr.end());
                         lev[di] = gr;
                         sort_by_first(lev);
+                        co.dirty[ell] = 1;
                     }
                     applied = true;
                     p = q + 1;

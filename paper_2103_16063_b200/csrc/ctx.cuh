@@ -36,6 +36,18 @@ struct DBuf {
     T *as() const { return (T *)p; }
 };
 
+// partition_blocks' device buffers, kept across calls (allocation and the
+// pinned staging would otherwise cost more than a small coarsening)
+struct CoarsenBufs {
+    DBuf atoms_d, lev_grp, lev_off, lev_at, sets_d, scratch_d, out_d, comp_d, mv_d;
+    int lev_cap = 0;          // level slots valid for lev_n atoms
+    int lev_n = -1;
+    int32_t *pin = nullptr;   // pinned level staging [lev_cap][3 * lev_n + 1]
+    ~CoarsenBufs() {
+        if (pin) cudaFreeHost(pin);
+    }
+};
+
 struct CachedKey {
     int64_t m;
     int ckpt;
@@ -90,6 +102,7 @@ struct pc_ctx {
     DBuf plan_off_d, seg_d, objective_d, feasible_d;
     DBuf q_d, q_out_d, sim_d;
     DBuf raw_d, keys_m_d, keys_ckpt_d, colb_d;
+    pcb::CoarsenBufs cb;  // partition_blocks
     DBuf bf_d;       // brute force: binomials, keys, per-block winners
     DBuf cut_d;      // pruning cut (cost tables): row/column prefixes, row_e
     // last batch (for budget crossing queries)
