@@ -536,9 +536,9 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.hspill_used = used + 3 * (size_t)n + 2;
         bt.hist_cells = hist_cells;
         CUDA_TRY(ctx, cudaMemsetAsync(ob, 0, 64 + 3 * sizeof(unsigned long long) * (size_t)n + 64, ctx->st));
-        CUDA_TRY(ctx, ctx->counters_d.ensure((8 + FMAX) * sizeof(unsigned long long)));
+        CUDA_TRY(ctx, ctx->counters_d.ensure((8 + FMAX + 3 * WORK_SLOTS) * sizeof(unsigned long long)));
         bt.counters = ctx->counters_d.as<unsigned long long>();
-        CUDA_TRY(ctx, cudaMemsetAsync(bt.counters, 0, (8 + FMAX) * sizeof(unsigned long long), ctx->st));
+        CUDA_TRY(ctx, cudaMemsetAsync(bt.counters, 0, (8 + FMAX + 3 * WORK_SLOTS) * sizeof(unsigned long long), ctx->st));
         int64_t launches = 0;
         // the reference's pruning break drops cells only when a cost table can
         // make memory non-monotone in the share (dp.cu: pruning cut)
@@ -572,10 +572,12 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         if (int rc = check_launch(ctx, "dp_level")) return rc;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev2, ctx->st));
         int ovf = 0;
-        unsigned long long cnt[8 + FMAX] = {0};
+        unsigned long long cnt[8 + FMAX + 3 * WORK_SLOTS] = {0};
         CUDA_TRY(ctx, cudaMemcpyAsync(&ovf, bt.overflow, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaMemcpyAsync(cnt, bt.counters, sizeof(cnt), cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        for (int q = 0; q < WORK_SLOTS; ++q)
+            for (int j = 0; j < 3; ++j) cnt[j] += cnt[8 + FMAX + 3 * q + j];
         ctx->last_pairs += (int64_t)cnt[0];
         ctx->last_cands += (int64_t)cnt[1];
         ctx->last_inserts += (int64_t)cnt[2];

@@ -147,6 +147,7 @@ struct CallDesc {
 #define PC_DP_WARPS 4
 #endif
 constexpr int DP_WARPS = PC_DP_WARPS;
+constexpr int WORK_SLOTS = 64;  // work counters spread over slots (no same-address atomics)
 constexpr int FMAX = 64;       // Pareto frontier capacity per cell (two slots per lane)
 
 struct DPBatch {

@@ -433,9 +433,10 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         n_cands += __shfl_xor_sync(0xffffffffu, n_cands, o);
     }
     if (lane == 0) {
-        atomicAdd(&B.counters[0], (unsigned long long)n_pairs);
-        atomicAdd(&B.counters[1], (unsigned long long)n_cands);
-        atomicAdd(&B.counters[2], (unsigned long long)n_ins);
+        unsigned long long *wk = B.counters + 8 + FMAX + 3 * (blockIdx.x & (WORK_SLOTS - 1));
+        atomicAdd(&wk[0], (unsigned long long)n_pairs);
+        atomicAdd(&wk[1], (unsigned long long)n_cands);
+        atomicAdd(&wk[2], (unsigned long long)n_ins);
         if (PC_DP_DIAG) {
             atomicAdd(&B.counters[3 + min(n, FMAX)], 1ull);     // frontier-size histogram
             atomicAdd(&B.counters[4 + FMAX + 0], (unsigned long long)n_rounds);
