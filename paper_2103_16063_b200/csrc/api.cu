@@ -555,6 +555,14 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             CUDA_TRY(ctx, cudaMemcpyAsync(cut_rows, row_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
             CUDA_TRY(ctx, cudaMemcpyAsync(cut_cols, col_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
         }
+        // PIPECUT_B200_LEVELS: per-level kernel time (debug; one event pair per level)
+        const bool level_times = getenv("PIPECUT_B200_LEVELS") != nullptr;
+        std::vector<cudaEvent_t> lev_ev;
+        if (level_times) {
+            lev_ev.resize(maxS + 1);
+            for (auto &e : lev_ev) cudaEventCreate(&e);
+            cudaEventRecord(lev_ev[0], ctx->st);
+        }
         for (int s = 1; s <= maxS; ++s) {
             int n_active = 0;
             while (n_active < n && cds[n_active].S >= s) ++n_active;
@@ -568,6 +576,24 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             if (cut)
                 ctx->launches += launch_prune_cut(bt, s, n_active, row_prefix[n_active], col_prefix[n_active],
                                                   cut_rows, cut_cols, row_e, ctx->st);
+            if (level_times) cudaEventRecord(lev_ev[s], ctx->st);
+        }
+        if (level_times) {
+            cudaEventSynchronize(lev_ev[maxS]);
+            const int edges[] = {1, 2, 9, 33, 65, 129, 249, maxS + 1};
+            fprintf(stderr, "[pipecut_b200] level times:");
+            for (int e = 0; e + 1 < 8; ++e) {
+                float tot = 0;
+                int s0 = edges[e], s1 = std::min(edges[e + 1], maxS + 1);
+                for (int s = s0; s < s1; ++s) {
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, lev_ev[s - 1], lev_ev[s]);
+                    tot += ms;
+                }
+                if (s1 > s0) fprintf(stderr, " s%d-%d %.1fms", s0, s1 - 1, tot);
+            }
+            fprintf(stderr, "\n");
+            for (auto &e : lev_ev) cudaEventDestroy(e);
         }
         if (int rc = check_launch(ctx, "dp_level")) return rc;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev2, ctx->st));
