@@ -77,5 +77,25 @@ def main():
         fh.write("\n")
 
 
+def criterion8():
+    """The acceptance gate's criterion-8 sweep (test_acceptance.py:324-353) with
+    the reference CLI -> golden/sweep_c8.csv."""
+    with tempfile.TemporaryDirectory() as wd:
+        with open(os.path.join(wd, "cluster.json"), "w") as fh:
+            json.dump({"num_nodes": 2, "devices_per_node": 2, "device_memory_bytes": 32 * 10 ** 9,
+                       "bw_intra": 50e9, "bw_inter": 10e9, "link_latency_sec": 0.0}, fh)
+        env = dict(os.environ, PYTHONPATH=REF)
+        subprocess.run([sys.executable, "-c",
+                        "import sys; from pipecut.cli import main; sys.exit(main(sys.argv[1:]))",
+                        "sweep", "--cluster", "cluster.json", "--hidden", "2048",
+                        "--layers", "24,48,96,192", "--batch-size", "32", "--out", "."],
+                       cwd=wd, env=env, check=True)
+        with open(os.path.join(wd, "sweep.csv")) as src, \
+                open(os.path.join(HERE, "sweep_c8.csv"), "w") as dst:
+            dst.write(src.read())
+
+
 if __name__ == "__main__":
     main()
+    if "c8" in sys.argv[1:]:
+        criterion8()
