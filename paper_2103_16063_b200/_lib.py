@@ -7,6 +7,8 @@ every entry point raises ``DeviceUnavailable``.
 from __future__ import annotations
 
 import ctypes as C
+import functools
+import threading
 import os
 import threading
 
@@ -137,11 +139,27 @@ class Context:
 _contexts: dict[int, Context] = {}
 
 
+# The library is not re-entrant and a context (device memory, stream, key
+# cache) is shared by every thread of the process: the drop-ins serialise on
+# one re-entrant lock (the reference itself is single-threaded).
+_call_lock = threading.RLock()
+
+
+def serialized(fn):
+    """Run a drop-in entry point under the process-wide library lock."""
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        with _call_lock:
+            return fn(*args, **kwargs)
+    return wrapper
+
+
 def context(device: int | None = None) -> Context:
     if device is None:
         device = int(os.environ.get("PIPECUT_B200_DEVICE", os.environ.get("LOCAL_RANK", "0")))
-    ctx = _contexts.get(device)
-    if ctx is None:
-        ctx = Context(device)
-        _contexts[device] = ctx
-    return ctx
+    with _call_lock:
+        ctx = _contexts.get(device)
+        if ctx is None:
+            ctx = Context(device)
+            _contexts[device] = ctx
+        return ctx

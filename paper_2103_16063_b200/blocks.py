@@ -24,6 +24,7 @@ CompactionStuck = _pc.blocks.CompactionStuck
 CostRecord = _pc.costs.CostRecord
 
 
+@_lib.serialized
 def partition_blocks(partition, model, k: int = 32):
     """Group atoms into at most k convex, memory-feasible blocks (GPU)."""
     if k < 1:

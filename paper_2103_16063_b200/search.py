@@ -258,6 +258,7 @@ def decide(allrec: np.ndarray, calls, levels, owner, plan_w: int, budget, batch_
     return ("plan", SearchResult(plan, stats))
 
 
+@_lib.serialized
 def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
                        options=None, *, group=None, timings: dict | None = None):
     """form_stage with its DP calls spread over every rank of a

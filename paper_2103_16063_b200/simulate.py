@@ -86,6 +86,7 @@ def _close(a, b):
     return math.isclose(a, b, rel_tol=1e-9, abs_tol=1e-15)
 
 
+@_lib.serialized
 def validate_plan(plan, blocks):
     """Recheck a plan from scratch; empty list iff it is sound (GPU records)."""
     out = _structure(plan, len(blocks))
@@ -125,6 +126,7 @@ def validate_plan(plan, blocks):
     return out
 
 
+@_lib.serialized
 def simulate(plan, blocks):
     """Event-level replay of one iteration of the plan (GPU), as the
     reference's Schedule."""

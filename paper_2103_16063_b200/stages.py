@@ -98,6 +98,7 @@ def _budget(opts) -> int:
     return -1 if opts.visit_budget is None else int(opts.visit_budget)
 
 
+@_lib.serialized
 def form_stage_dp(blocks, S: int, D: int, batch_size: int, replica_factor: int,
                   microbatches: int, options=None):
     """Optimal S-stage assignment of the block list onto D devices (GPU)."""
@@ -119,6 +120,7 @@ def form_stage_dp(blocks, S: int, D: int, batch_size: int, replica_factor: int,
     return SearchResult(plan, stats)
 
 
+@_lib.serialized
 def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
                options=None, *, speculative: bool = True, last_stats: dict | None = None):
     """Search replica factor, stage count and microbatch count together (GPU).
@@ -153,6 +155,7 @@ def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
     return SearchResult(plan, stats)
 
 
+@_lib.serialized
 def brute_force_partition(blocks, S: int, D: int, batch_size: int, replica_factor: int,
                           microbatches: int, options=None, *, guard: bool = True):
     """Exhaustive search over every (cut combination, device composition)

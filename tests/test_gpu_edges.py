@@ -75,3 +75,28 @@ def test_capacity_limits_raise(gpu):
     bs = cases.c5_blockset(4, 8)
     with pytest.raises(DeviceError):
         form_stage_dp(bs, 2, 4096, 8 * 4096, 1, 1)           # D beyond the packed key range
+
+
+def test_concurrent_callers(gpu):
+    """Threads sharing the process's context get the sequential results (the
+    drop-ins serialise on the library lock; SURVEY.md §8b threading)."""
+    import random
+    import threading
+
+    from plans import result_doc
+
+    rng = random.Random(11)
+    inst = [cases.stages_random_instance(rng) for _ in range(8)]
+    want = [result_doc(form_stage_dp(*x)) for x in inst]
+    got = [None] * len(inst)
+
+    def work(i):
+        for _ in range(3):
+            got[i] = result_doc(form_stage_dp(*inst[i]))
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(inst))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert got == want
