@@ -129,7 +129,8 @@ __device__ __forceinline__ int front_insert(const WarpFront &f, int n, int lane,
     uint32_t k0 = 0;
     if (h0) { x0 = f.x(lane); y0 = f.y(lane); k0 = f.k(lane); }
     if (n <= 32) {
-        if (__any_sync(0xffffffffu, h0 && dominates(x0, y0, k0, cx, cy, ck))) return n;
+        // c is not dominated here: it passed front_dominated against the
+        // round's frontier, and every insert since was checked against it
         const bool keep0 = h0 && !dominates(cx, cy, ck, x0, y0, k0);
         const uint32_t m0 = __ballot_sync(0xffffffffu, keep0);
         const bool lt0 = keep0 && x0 < cx;
@@ -147,9 +148,6 @@ __device__ __forceinline__ int front_insert(const WarpFront &f, int n, int lane,
     double x1 = 0, y1 = 0;
     uint32_t k1 = 0;
     if (h1) { x1 = f.x(lane + 32); y1 = f.y(lane + 32); k1 = f.k(lane + 32); }
-    if (__any_sync(0xffffffffu, (h0 && dominates(x0, y0, k0, cx, cy, ck)) ||
-                                    (h1 && dominates(x1, y1, k1, cx, cy, ck))))
-        return n;
     const bool keep0 = h0 && !dominates(cx, cy, ck, x0, y0, k0);
     const bool keep1 = h1 && !dominates(cx, cy, ck, x1, y1, k1);
     const uint32_t m0 = __ballot_sync(0xffffffffu, keep0);
