@@ -14,6 +14,9 @@
 // pair against the current state, accept the first pair with a move, re-run
 // from the next pair (accepted moves are rare: 62 on BERT, 0 on ResNet).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -561,7 +564,19 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
     Coarsener co(ctx, H);
     const int n = H->n;
     const int64_t budget = H->budget;
+    // PIPECUT_B200_BLOCKS_TIMES: host wall time per phase (debug)
+    const bool phase_times = getenv("PIPECUT_B200_BLOCKS_TIMES") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto phase = [&](const char *what) {
+        if (!phase_times) return;
+        cudaStreamSynchronize(ctx->st);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[pipecut_b200] blocks %-12s %8.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t_prev).count());
+        t_prev = now;
+    };
     if (int rc = co.upload_atoms()) return rc;
+    phase("upload");
 
     // ---- level 0 and the atoms' own profiles (blocks.py:89-94, 366-369)
     std::vector<std::vector<int>> l0(n);
@@ -583,6 +598,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
     }
     const int32_t *nbr_off = H->nbr_off, *nbr = H->nbr;
 
+    phase("level0");
     // ---- coarsening passes (blocks.py:127-166, 371-378)
     std::vector<std::vector<std::pair<std::vector<int>, std::vector<int>>>> transitions;
     while ((int)co.levels.back().size() > k) {
@@ -668,8 +684,11 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         if (int rc = co.upload_level(L + 1, co.levels.back())) return rc;
     }
 
+    phase("coarsen");
     // ---- refinement: speculative rounds over the recorded merges (blocks.py:173-232)
     const int top = (int)co.levels.size() - 1;
+    long long n_rounds = 0, n_sets = 0, n_moves = 0;
+    double t_dev = 0.0;
     for (int li = (int)transitions.size() - 1; li >= 0; --li) {
         const auto &pairs = transitions[li];
         size_t p = 0;
@@ -709,7 +728,12 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
             std::vector<int64_t> smem, sav;
             std::vector<int32_t> scount;
             std::vector<uint8_t> sconv;
+            const auto td0 = std::chrono::steady_clock::now();
             if (int rc = co.eval_moves(sets, moves, smem, scount, sconv, sav)) return rc;
+            t_dev += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count();
+            ++n_rounds;
+            n_sets += (long long)sets.size();
+            n_moves += (long long)moves.size();
             const int nlev = top - li;
             bool applied = false;
             size_t ti_ptr = 0;
@@ -762,6 +786,10 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         }
     }
 
+    if (phase_times)
+        fprintf(stderr, "[pipecut_b200] refine: %lld rounds, %lld sets, %lld moves, %.2f ms in eval (device + sync)\n",
+                n_rounds, n_sets, n_moves, t_dev);
+    phase("refine");
     // ---- dependency order (blocks.py:235-255) and compaction (267-292)
     auto topo = [&](const std::vector<std::vector<int>> &groups) {
         const int m = (int)groups.size();
@@ -838,6 +866,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         glist = topo(glist);
     }
 
+    phase("compact");
     // ---- outputs: blocks and their profiles (blocks.py:387-397)
     const int nbk = (int)glist.size();
     const int fin = (int)co.levels.size();
@@ -853,5 +882,6 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         out_tb[b] = tb[b];
         out_mem[b] = mem[b];
     }
+    phase("outputs");
     return PC_OK;
 }
