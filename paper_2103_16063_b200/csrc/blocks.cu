@@ -139,56 +139,155 @@ __device__ int64_t set_mem(const DevAtoms &A, const DevLevels &L, const SetDesc 
     return (int64_t)memd;
 }
 
-// is_convex (blocks.py:45-70) as one sweep in index order: atom indices are
-// a topological order, so "reached" (the reference's DFS set) is
-// x in (lo, hi), not a member, with a member or reached predecessor; the set
-// is non-convex iff a member has a reached predecessor.
-__device__ bool set_convex(const DevAtoms &A, const DevLevels &L, const SetDesc &s, int lo, int hi,
-                           int count, uint32_t *bits) {
-    if (hi - lo + 1 == count) return true;
-    const int span = hi - lo + 1;
-    for (int w = 0; w < (span + 31) / 32; ++w) bits[w] = 0u;
-    for (int x = lo + 1; x <= hi; ++x) {
-        if (in_set(L, s, x)) {
-            for (int q = A.pred_off[x]; q < A.pred_off[x + 1]; ++q) {
-                const int p = A.pred[q];
-                if (p > lo && p < hi && ((bits[(p - lo) >> 5] >> ((p - lo) & 31)) & 1u)) return false;
-            }
-        } else if (x < hi) {
-            for (int q = A.pred_off[x]; q < A.pred_off[x + 1]; ++q) {
-                const int p = A.pred[q];
-                if (p < lo) continue;
-                const bool pm = in_set(L, s, p);
-                const bool pr = p > lo && ((bits[(p - lo) >> 5] >> ((p - lo) & 31)) & 1u);
-                if (pm || pr) {
-                    bits[(x - lo) >> 5] |= 1u << ((x - lo) & 31);
+// k_eval_sets: memory and convexity of implicit atom sets, one warp per set
+// (is_convex, blocks.py:45-70, as a sweep in index order: atom indices are a
+// topological order, so the reference's DFS "reached" set is: x in (lo, hi),
+// not a member, with a member or reached predecessor).  Memory: lanes stride over
+// the set's members and reduce exact integer partial sums (param, inputs) and
+// the footprint max, so the value is the one set_mem computes.  Convexity: the
+// same index-order sweep as set_convex, 32 consecutive atoms at a time --
+// reachability from earlier chunks comes from the bitmap, inside the chunk it
+// propagates by ballots until nothing changes (edges only go forward); a member
+// with a reached predecessor makes the set non-convex.
+__device__ __forceinline__ bool bit_at(const uint32_t *bits, int i) {
+    return (bits[i >> 5] >> (i & 31)) & 1u;
+}
+
+__global__ void k_eval_sets_warp(DevAtoms A, DevLevels L, const SetDesc *sets, int nsets,
+                                 uint32_t *scratch, int words, int64_t *out_mem,
+                                 int32_t *out_count, uint8_t *out_convex) {
+    const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= nsets) return;                                   // warp-uniform
+    const SetDesc s = sets[i];
+    const int n = L.n;
+    const int32_t *offa = L.goff + (int64_t)s.la * (n + 1);
+    const int32_t *ata = L.gat + (int64_t)s.la * n;
+    const int a0 = offa[s.ga], na = offa[s.ga + 1] - a0;
+    int b0 = 0, nbm = 0;
+    const int32_t *atb = ata;
+    if (s.mode == 0 && s.gb >= 0) {
+        const int32_t *offb = L.goff + (int64_t)s.lb * (n + 1);
+        atb = L.gat + (int64_t)s.lb * n;
+        b0 = offb[s.gb];
+        nbm = offb[s.gb + 1] - b0;
+    }
+    int lo = 0x7fffffff, hi = -1, count = 0;
+    long long param = 0, inb = 0, mfp = 0;
+    for (int j = lane; j < na + nbm; j += 32) {
+        int x;
+        if (j < na) {
+            x = ata[a0 + j];
+            if (s.mode == 1 && L.grp[(int64_t)s.lb * n + x] == s.gb) continue;
+        } else {
+            x = atb[b0 + j - na];
+            if (L.grp[(int64_t)s.la * n + x] == s.ga) continue;
+        }
+        lo = min(lo, x);
+        hi = max(hi, x);
+        ++count;
+        param += A.atom_param[x];
+        for (int q = A.atom_in_off[x]; q < A.atom_in_off[x + 1]; ++q) {
+            const int iv = A.atom_in[q];
+            const int own = A.in_owner[iv];
+            if (own >= 0 && in_set(L, s, own)) continue;          // owned inside: not an input
+            for (int r = A.in_atoms_off[iv]; r < A.in_atoms_off[iv + 1]; ++r) {
+                const int y = A.in_atoms[r];
+                if (in_set(L, s, y)) {                              // count at the first lister
+                    if (y == x) inb += A.in_size[iv];
                     break;
                 }
             }
         }
+        for (int q = A.atom_task_off[x]; q < A.atom_task_off[x + 1]; ++q) {
+            const int t = A.atom_tasks[q];
+            long long fp = A.task_fp1[t];
+            if (A.ov_has && A.ov_has[t] && A.ov_act[t] >= 0) fp += A.ov_act[t] - A.task_prod1[t];
+            for (int d = A.dep_off[t]; d < A.dep_off[t + 1]; ++d)
+                if (in_set(L, s, A.dep_owner[d])) fp += A.dep_size[d];
+            mfp = fp > mfp ? fp : mfp;
+        }
     }
-    return true;
-}
-
-__global__ void k_eval_sets(DevAtoms A, DevLevels L, const SetDesc *sets, int nsets, uint32_t *scratch,
-                            int words, int64_t *out_mem, int32_t *out_count, uint8_t *out_convex) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nsets) return;
-    const SetDesc s = sets[i];
-    int lo = 0x7fffffff, hi = -1, count = 0;
-    for_each_member(L, s, [&](int x) {
-        lo = x < lo ? x : lo;
-        hi = x > hi ? x : hi;
-        ++count;
-    });
-    out_count[i] = count;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        count += __shfl_xor_sync(0xffffffffu, count, o);
+        param += __shfl_xor_sync(0xffffffffu, param, o);
+        inb += __shfl_xor_sync(0xffffffffu, inb, o);
+        const long long m2 = __shfl_xor_sync(0xffffffffu, mfp, o);
+        mfp = m2 > mfp ? m2 : mfp;
+    }
     if (count == 0) {
-        out_mem[i] = 0;
-        out_convex[i] = 1;
+        if (lane == 0) {
+            out_count[i] = 0;
+            out_mem[i] = 0;
+            out_convex[i] = 1;
+        }
         return;
     }
-    out_mem[i] = set_mem(A, L, s);
-    out_convex[i] = set_convex(A, L, s, lo, hi, count, scratch + (int64_t)i * words) ? 1 : 0;
+    bool convex = true;
+    if (hi - lo + 1 != count) {
+        const int span = hi - lo + 1;
+        uint32_t *bits = scratch + (int64_t)i * words;
+        for (int w = lane; w < (span + 31) / 32; w += 32) bits[w] = 0u;
+        __syncwarp();
+        for (int base = lo + 1; base <= hi; base += 32) {
+            const int x = base + lane;
+            const bool valid = x <= hi;
+            const bool mem = valid && in_set(L, s, x);
+            const bool open = valid && !mem && x < hi;           // may become reached
+            bool reached = false, bad = false;
+            if (mem) {
+                for (int q = A.pred_off[x]; q < A.pred_off[x + 1]; ++q) {
+                    const int p = A.pred[q];
+                    if (p > lo && p < base && bit_at(bits, p - lo)) bad = true;
+                }
+            } else if (open) {
+                for (int q = A.pred_off[x]; q < A.pred_off[x + 1]; ++q) {
+                    const int p = A.pred[q];
+                    if (p < lo) continue;
+                    if (in_set(L, s, p) || (p > lo && p < base && bit_at(bits, p - lo))) {
+                        reached = true;
+                        break;
+                    }
+                }
+            }
+            uint32_t rmask = __ballot_sync(0xffffffffu, reached);
+            for (;;) {                                          // in-chunk propagation
+                bool nr = reached;
+                if (open && !reached)
+                    for (int q = A.pred_off[x]; q < A.pred_off[x + 1]; ++q) {
+                        const int p = A.pred[q];
+                        if (p >= base && p < x && ((rmask >> (p - base)) & 1u)) {
+                            nr = true;
+                            break;
+                        }
+                    }
+                const uint32_t nm = __ballot_sync(0xffffffffu, nr);
+                reached = nr;
+                if (nm == rmask) break;
+                rmask = nm;
+            }
+            if (mem)
+                for (int q = A.pred_off[x]; q < A.pred_off[x + 1]; ++q) {
+                    const int p = A.pred[q];
+                    if (p >= base && p < x && ((rmask >> (p - base)) & 1u)) bad = true;
+                }
+            if (__any_sync(0xffffffffu, bad)) {
+                convex = false;
+                break;
+            }
+            if (reached) atomicOr(&bits[(x - lo) >> 5], 1u << ((x - lo) & 31));
+            __syncwarp();
+        }
+    }
+    if (lane == 0) {
+        out_count[i] = count;
+        const double memd = __dadd_rn(__dmul_rn((double)param, A.factor), (double)(inb + mfp));
+        out_mem[i] = (int64_t)memd;
+        out_convex[i] = convex ? 1 : 0;
+    }
 }
 
 // sum(atom_comp[i] for i in group) with CPython 3.12's float sum: the first
@@ -472,8 +571,8 @@ struct Coarsener {
         int64_t *om = out_d.as<int64_t>();
         int32_t *oc = (int32_t *)(om + ns);
         uint8_t *ov = (uint8_t *)(oc + ns);
-        k_eval_sets<<<(ns + 127) / 128, 128, 0, ctx->st>>>(A, dev_levels(), sets_d.as<SetDesc>(), ns,
-                                                           scratch_d.as<uint32_t>(), words, om, oc, ov);
+        k_eval_sets_warp<<<(unsigned)(((int64_t)ns * 32 + 127) / 128), 128, 0, ctx->st>>>(
+            A, dev_levels(), sets_d.as<SetDesc>(), ns, scratch_d.as<uint32_t>(), words, om, oc, ov);
         ctx->launches++;
         if (int rc = check_launch(ctx, "eval_sets")) return rc;
         CUDA_TRY(ctx, cudaMemcpyAsync(mem.data(), om, 8 * (size_t)ns, cudaMemcpyDeviceToHost, ctx->st));
