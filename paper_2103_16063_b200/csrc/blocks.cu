@@ -145,7 +145,7 @@ __device__ int64_t set_mem(const DevAtoms &A, const DevLevels &L, const SetDesc 
 // not a member, with a member or reached predecessor).  Memory: lanes stride over
 // the set's members and reduce exact integer partial sums (param, inputs) and
 // the footprint max, so the value is the one set_mem computes.  Convexity: the
-// same index-order sweep as set_convex, 32 consecutive atoms at a time --
+// index-order sweep, 32 consecutive atoms at a time --
 // reachability from earlier chunks comes from the bitmap, inside the chunk it
 // propagates by ballots until nothing changes (edges only go forward); a member
 // with a reached predecessor makes the set non-convex.
