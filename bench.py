@@ -20,6 +20,7 @@ e2e:   the public API form_stage_sharded() per step, including host
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -445,6 +446,7 @@ def config_latencies(ctx):
             _flat._ATOM_CACHE.clear()
             ctx.problem_owner = None
             ctx.lib.pc_reset_cache(ctx.h)
+            gc.collect()          # the CPU-baseline sampler leaves large garbage behind
             t0 = time.perf_counter()
             bs = partition_blocks(part, model, k)
             t1 = time.perf_counter()

@@ -234,12 +234,11 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
     for (int attempt = 0; attempt < 2; ++attempt) {
         const size_t raw_key = sizeof(double) * ((ctx->derived ? 1 : 2) * (size_t)tri + 2 * (size_t)(P.nb + 1)) + sizeof(int32_t) * (size_t)(P.nb + 1);
         const size_t per_key = (raw_key + 255) & ~size_t(255);
-        if (per_key != ctx->key_slot) {          // new layout (nb or derived changed)
-            free_keys(ctx);
-            ctx->key_arena.release();
+        if (per_key != ctx->key_slot) {          // new layout (nb or derived changed):
+            free_keys(ctx);                       // re-slice the arena, keep the memory
             ctx->key_slot = per_key;
-            ctx->key_cap = 0;
-            ctx->slot_used.clear();
+            ctx->key_cap = (int)(ctx->key_arena.n / per_key);
+            ctx->slot_used.assign(ctx->key_cap, 0);
             fresh = want;
         }
         if (ctx->keys.size() + fresh.size() > (size_t)ctx->key_cap) {
