@@ -100,3 +100,32 @@ def test_concurrent_callers(gpu):
     for t in ts:
         t.join()
     assert got == want
+
+
+@pytest.mark.parametrize("beta", [3.0, 1.5, 0.7, 4.0])
+def test_backward_ratio_not_two(gpu, beta):
+    """t_bwd = beta * t_fwd per task (costs.py:138-140): with beta not a power of
+    two the span tables store t_bwd (no derivation), and the -fmad=false folds
+    must still match the oracle bit for bit (test_costs.py uses beta = 3)."""
+    import random
+
+    rng = random.Random(int(beta * 10))
+    for _ in range(6):
+        n = rng.randint(3, 8)
+        g = cases.chain([round(rng.uniform(0.5, 4.0), 3) for _ in range(n)],
+                        sizes=[rng.choice([0, 64, 256]) for _ in range(n)],
+                        params=[rng.choice([0, 512]) for _ in range(n)])
+        cl = pc.ClusterSpec(num_nodes=2, devices_per_node=3, device_memory_bytes=2 ** 40,
+                            bw_intra=1e3, bw_inter=5e2, link_latency_sec=0.01)
+        part = pc.build_atomic_subcomponents(g)
+        cfg = pc.CostModelConfig(device_flops_per_sec=1.0, bwd_fwd_ratio=beta,
+                                 checkpointing=rng.random() < 0.5)
+        bs = pc.partition_blocks(part, pc.CostModel(part.graph, cfg, cl), k=10 ** 6)
+        S = rng.randint(1, min(3, n))
+        _dp_matches_oracle(bs, S, 6, 24, 1, 2)
+        res = form_stage(2, 3, 24, bs)
+        rc, want, visits, calls = OracleProblem(flatten_blockset(bs)).form_stage(2, 3, 24)
+        assert res.stats.visits == visits and res.stats.dp_calls == calls
+        assert (res.plan is None) == (want is None)
+        if want is not None:
+            assert res.plan.objective == want["objective"]

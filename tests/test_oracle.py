@@ -73,6 +73,23 @@ def test_span_profile_matches_reference_model_graphs(kind):
                     assert op.span(lo, hi, m, ck) == (r.t_fwd_sec, r.t_bwd_sec, r.mem_bytes)
 
 
+@pytest.mark.parametrize("beta", [3.0, 1.5, 0.7, 4.0])
+def test_span_profile_matches_reference_backward_ratio(beta):
+    """beta * x per task folded without FMA (costs.py:138-140; test_costs.py
+    uses beta = 3): the oracle's t_bwd equals CostModel.profile's bit for bit."""
+    g = pc.gen_bert_like(64, 3, 16, 100)
+    cl = pc.ClusterSpec(2, 2, 2 ** 40, 50e9, 10e9)
+    part = pc.build_atomic_subcomponents(g)
+    model = pc.CostModel(part.graph, pc.CostModelConfig(bwd_fwd_ratio=beta), cl)
+    bs = pc.partition_blocks(part, model, 12)
+    op = OracleProblem(flatten_blockset(bs))
+    for lo in range(len(bs)):
+        for hi in range(lo + 1, len(bs) + 1):
+            for m in (1, 5):
+                r = model.profile(bs.span(lo, hi), m, checkpointing=True)
+                assert op.span(lo, hi, m, True) == (r.t_fwd_sec, r.t_bwd_sec, r.mem_bytes)
+
+
 def test_cut_time_matches_reference():
     rng = random.Random(11)
     for _ in range(10):
