@@ -17,7 +17,17 @@
  *                       simulate()-based ranking keys (stages.py:389-411,
  *                       simulate.py:79-165) -- the unit sharded across GPUs
  *   pc_form_stage       form_stage (stages.py:372-413), single GPU
+ *   pc_last_crossing    the SearchBudgetExceeded visit count (stages.py:214-216)
  *   pc_partition_blocks partition_blocks (blocks.py:361-397)
+ *   pc_set_overrides    measured cost-table entries (costs.py:43-80, 130-148)
+ *   pc_brute_force      brute_force_partition (stages.py:304-369)
+ *   pc_check_plan       validate_plan's fresh records (stages.py:416-492)
+ *   pc_simulate         simulate (simulate.py:79-179)
+ *   pc_call_weights     sharding weights of form_stage's call enumeration
+ *                       (stages.py:389-403); no reference counterpart
+ *   pc_ctx_*, pc_device_info, pc_reset_cache, pc_timer_*, pc_measure_fp64_peak
+ *                       library plumbing and measurement; no reference
+ *                       counterpart
  *
  * Conventions: plain pointers and sizes, caller-owned host buffers, valid for
  * the duration of the call; the library owns device memory behind an opaque
@@ -223,25 +233,28 @@ int pc_simulate(pc_ctx *ctx, const pc_plan *plan, int64_t batch_size, int32_t ev
 int pc_call_weights(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
                     int64_t *weights);
 
-/* CostModel.profile over block spans: n queries (lo, hi, m, ckpt). */
+/* CostModel.profile over block spans (costs.py:97-160 via stages.py:138-145):
+ * n queries (lo, hi, m, ckpt). */
 int pc_profile_spans(pc_ctx *ctx, int32_t n, const int32_t *lo, const int32_t *hi,
                      const int64_t *m, const int32_t *ckpt,
                      double *t_fwd, double *t_bwd, int64_t *mem);
 
-/* form_stage_dp: one DP call.  visit_budget < 0 means none.  Returns PC_OK,
+/* form_stage_dp (stages.py:282-291 -> _run_dp 188-279): one DP call.
+ * visit_budget < 0 means none.  Returns PC_OK,
  * PC_INFEASIBLE, PC_ERR_BUDGET (stats->visits = visits at the crossing). */
 int pc_form_stage_dp(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_size,
                      int32_t R, int32_t MB, int32_t disable_pruning,
                      int64_t visit_budget, pc_plan *plan, pc_stats *stats);
 
-/* Batch of independent DP calls (the sharded unit of form_stage).  Every
+/* Batch of independent DP calls (the sharded unit of form_stage,
+ * stages.py:389-411).  Every
  * call's plan is simulated for its ranking key when want_iteration != 0.
  * plans may be NULL (results only); otherwise n entries. */
 int pc_run_calls(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
                  int32_t disable_pruning, int32_t want_iteration,
                  pc_call_result *results, pc_plan *plans, pc_stats *stats);
 
-/* form_stage on one GPU.  speculative != 0 evaluates every widening level in
+/* form_stage (stages.py:372-413) on one GPU.  speculative != 0 evaluates every widening level in
  * one batch and then applies the reference's first-feasible-level rule;
  * results and stats are identical either way. */
 int pc_form_stage(pc_ctx *ctx, int32_t num_nodes, int32_t devices_per_node,
