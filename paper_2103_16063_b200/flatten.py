@@ -384,33 +384,45 @@ def _flatten_atoms(partition, model) -> FlatAtoms:
     pg = partition.graph
     n = len(partition.atoms)
     atom_of = atom_node_tables(partition)
+    atom_get = atom_of.get
     graph_inputs = g.inputs
+    nodes = g.nodes
+    succ_of, pred_of = g.succ, g.pred
+    sizes = {}                                   # value id -> exact bytes at m = 1
 
-    def size1(info, what):
-        return _as_int(info.fixed_bytes, what) + _as_int(info.bytes_per_sample, what)
+    def size1(info, vid):
+        sz = sizes.get(vid)
+        if sz is None:
+            sz = sizes[vid] = _as_int(info.fixed_bytes, vid) + _as_int(info.bytes_per_sample, vid)
+        return sz
 
     inputs_of_atom = [frozenset(a.input_values) for a in partition.atoms]
-    in_ids = sorted({v for ins in inputs_of_atom for v in ins})
-    in_index = {v: i for i, v in enumerate(in_ids)}
-    in_owner, in_size, in_atoms = [], [], []
-    listing = {v: [] for v in in_ids}
+    listing = {}
     for a, ins in enumerate(inputs_of_atom):
         for v in ins:
-            listing[v].append(a)
+            lst = listing.get(v)
+            if lst is None:
+                listing[v] = [a]
+            else:
+                lst.append(a)
+    in_ids = sorted(listing)
+    in_index = {v: i for i, v in enumerate(in_ids)}
+    in_owner, in_size, in_atoms = [], [], []
     for v in in_ids:
-        node = g.nodes[v]
+        node = nodes[v]
         if not node.is_value:
             raise UnsupportedGraph(f"atom input {v!r} is not a value")
-        own = atom_of.get(v)
+        own = atom_get(v)
         in_owner.append(-1 if (v in graph_inputs or own is None) else own)
         in_size.append(size1(node.value, v))
-        in_atoms.append(sorted(listing[v]))
+        in_atoms.append(listing[v])              # ascending: atoms visited in order
 
     atom_param = [0] * n
-    task_atom, task_flops, task_fp1, deps, task_prod1, tnodes = [], [], [], [], [], []
+    task_atom, task_flops, task_fp1, task_prod1, tnodes = [], [], [], [], []
+    dep_owner_l, dep_size_l, dep_off = [], [], [0]
     atom_tasks = [[] for _ in range(n)]
-    for nid, node in g.nodes.items():           # sorted id order (graph.py:90-93)
-        a = atom_of.get(nid)
+    for nid, node in nodes.items():             # sorted id order (graph.py:90-93)
+        a = atom_get(nid)
         if a is None:
             continue
         if node.is_value:
@@ -418,56 +430,57 @@ def _flatten_atoms(partition, model) -> FlatAtoms:
                 atom_param[a] += _as_int(node.value.fixed_bytes, nid)
             continue
         fp = 0
-        for vid in g.succ(nid):
-            info = g.nodes[vid].value
+        for vid in succ_of(nid):
+            info = nodes[vid].value
             if info is not None and not info.is_param:
                 fp += size1(info, vid)
         task_prod1.append(fp)
         tnodes.append(node.task)
-        dl = []
-        for vid in g.pred(nid):
-            info = g.nodes[vid].value
+        ins = inputs_of_atom[a]
+        for vid in pred_of(nid):
+            info = nodes[vid].value
             if info is None or info.is_param:
                 continue
-            if vid in inputs_of_atom[a]:
+            if vid in ins:
                 own = in_owner[in_index[vid]]
                 if own >= 0:
-                    dl.append((own, size1(info, vid)))
+                    dep_owner_l.append(own)
+                    dep_size_l.append(size1(info, vid))
                 # model input / unowned: always an input of G, never counted
             else:
-                if atom_of.get(vid) != a:
+                if atom_get(vid) != a:
                     raise UnsupportedGraph(f"task {nid!r} reads {vid!r} across atoms "
                                            f"without listing it as an input")
                 fp += size1(info, vid)
+        dep_off.append(len(dep_owner_l))
         atom_tasks[a].append(len(task_atom))
         task_atom.append(a)
         task_flops.append(float(node.task.flops_per_sample))
         task_fp1.append(fp)
-        deps.append(dl)
 
     succ = [[] for _ in range(n)]
     pred = [[] for _ in range(n)]
     for a, b in _dependencies(partition, n):   # sorted unique pairs
         succ[a].append(b)
         pred[b].append(a)
-    nbr = [sorted(set(succ[i]) | set(pred[i])) for i in range(n)]
+    nbr = [sorted(set(succ[i]).union(pred[i])) for i in range(n)]
 
     tr_owner, tr_size, tr_cons = [], [], []
     atom_tr = [[] for _ in range(n)]
+    consumer_atoms, owner_of = partition.consumer_atoms, partition.owner_of_value
     for vid in pg.value_ids():                   # blocks.py:96-102
-        consumers = partition.consumer_atoms(vid)
-        owner = partition.owner_of_value(vid)
-        foreign = tuple(sorted(consumers - {owner}))
+        owner = owner_of(vid)
+        foreign = sorted(consumer_atoms(vid) - {owner})
         if foreign:
             e = len(tr_owner)
             tr_owner.append(owner)
             tr_size.append(_as_int(pg.value_size(vid, 1), vid))
-            tr_cons.append(list(foreign))
+            tr_cons.append(foreign)
             for x in sorted({owner, *foreign}):
                 atom_tr[x].append(e)
 
-    d_off, d_flat = _csr([[o for o, _ in dl] for dl in deps])
-    ds = [s for dl in deps for _, s in dl]
+    d_off, d_flat = _i32(dep_off), _i32(dep_owner_l)
+    ds = dep_size_l
     at_off, at = _csr(atom_tasks)
     ai_off, ai = _csr([[in_index[v] for v in sorted(ins)] for ins in inputs_of_atom])
     ia_off, ia = _csr(in_atoms)
