@@ -237,7 +237,7 @@ def run_ours(a):
     dev = torch.device("cuda", local)
 
     from paper_2103_16063_b200 import _lib
-    from paper_2103_16063_b200.search import (device_weights, _pack, call_weight, decide, enumerate_calls,
+    from paper_2103_16063_b200.search import (device_weights, _pack, decide, enumerate_calls,
                                               exchange, form_stage_sharded, lpt_shard,
                                               run_calls)
     from paper_2103_16063_b200.stages import bind_problem

@@ -9,8 +9,6 @@ The configs C1-C5 follow SURVEY.md §8(d) / BASELINE.md §2.
 
 from __future__ import annotations
 
-import random
-
 from paper_2103_16063_b200._host import pipecut as pc
 
 Node, TaskGraph, TaskInfo, ValueInfo = pc.graph.Node, pc.TaskGraph, pc.graph.TaskInfo, pc.graph.ValueInfo

@@ -12,9 +12,8 @@ import cases
 from oracle.oracle import OracleProblem, PC_OK
 from paper_2103_16063_b200 import abi, form_stage, form_stage_dp
 from paper_2103_16063_b200._host import pipecut as pc
-from paper_2103_16063_b200.flatten import flatten_blockset
 from paper_2103_16063_b200.stages import bind_problem
-from plans import plan_doc, result_doc
+from plans import result_doc
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")

@@ -6,8 +6,7 @@ import torch
 from paper_2103_16063_b200 import _lib
 from paper_2103_16063_b200 import flatten as F
 from paper_2103_16063_b200 import abi
-from paper_2103_16063_b200.search import device_weights, enumerate_calls, form_stage_sharded, run_calls
-from paper_2103_16063_b200.stages import bind_problem
+from paper_2103_16063_b200.search import device_weights, enumerate_calls, form_stage_sharded
 from paper_2103_16063_b200.workloads import c5_blockset
 import ctypes as C
 
