@@ -8,6 +8,13 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
     if p not in sys.path:
         sys.path.insert(0, p)
 
+# the host API is the unmodified reference installed in baseline/_ref (git-ignored);
+# on a fresh checkout create it the way build() does (offline pip install)
+if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "pipecut")):
+    import __graft_entry__
+
+    __graft_entry__._ensure_reference_install()
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and libpipecut_b200.so")
