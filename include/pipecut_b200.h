@@ -254,9 +254,10 @@ int pc_run_calls(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_siz
                  int32_t disable_pruning, int32_t want_iteration,
                  pc_call_result *results, pc_plan *plans, pc_stats *stats);
 
-/* form_stage (stages.py:372-413) on one GPU.  speculative != 0 evaluates every widening level in
- * one batch and then applies the reference's first-feasible-level rule;
- * results and stats are identical either way. */
+/* form_stage (stages.py:372-413) on one GPU.  Batching of the widening
+ * levels: speculative = 1 all in one batch, 0 one batch per level, 2 the first
+ * level and then the rest together.  The reference's first-feasible-level
+ * rule is applied afterwards; results and stats are identical in every mode. */
 int pc_form_stage(pc_ctx *ctx, int32_t num_nodes, int32_t devices_per_node,
                   int64_t batch_size, int32_t disable_pruning, int64_t visit_budget,
                   int32_t speculative, pc_plan *plan, pc_stats *stats);

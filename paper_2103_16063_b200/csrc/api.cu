@@ -1024,7 +1024,7 @@ extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, in
         return PC_OK;
     };
     int chunks = 0;
-    if (speculative) {
+    if (speculative == 1) {
         std::vector<CallOut> outs;
         if (int rc = run_calls_impl(ctx, calls, BS, !disable_pruning, 1, outs, &chunks)) return rc;
         if (chunks > 1 && visit_budget >= 0) {
@@ -1049,11 +1049,20 @@ extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, in
     running = calls_counted = unpruned = cells = 0;
     double dp_ms = 0, span_ms = 0;
     int64_t pairs = 0, cands = 0, launches = 0;
-    for (int lv = 0; lv < n_levels; ++lv) {
+    // batches of widening levels: one per level (0), or the first level and then
+    // all the others together (2: the first level is usually feasible)
+    std::vector<std::pair<int, int>> groups;
+    if (speculative == 2) {
+        groups.push_back({0, std::min(1, n_levels)});
+        groups.push_back({std::min(1, n_levels), n_levels});
+    } else {
+        for (int lv = 0; lv < n_levels; ++lv) groups.push_back({lv, lv + 1});
+    }
+    for (const auto &grp : groups) {
         std::vector<pc_call> sub;
         std::vector<int> map(calls.size(), -1);
         for (size_t ci = 0; ci < calls.size(); ++ci)
-            if (level_of[ci] == lv) {
+            if (level_of[ci] >= grp.first && level_of[ci] < grp.second) {
                 map[ci] = (int)sub.size();
                 sub.push_back(calls[ci]);
             }
@@ -1070,11 +1079,13 @@ extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, in
         ctx->last_pairs = pairs;
         ctx->last_cands = cands;
         ctx->last_dp_launches = launches;
-        if (int rc = process_level(lv, outs, map)) return rc;
-        if (best >= 0) {
-            fill_stats(ctx, stats, running, calls_counted, unpruned, cells);
-            if (plan) fill_plan(outs[map[best]], calls[best], plan);
-            return PC_OK;
+        for (int lv = grp.first; lv < grp.second; ++lv) {
+            if (int rc = process_level(lv, outs, map)) return rc;
+            if (best >= 0) {
+                fill_stats(ctx, stats, running, calls_counted, unpruned, cells);
+                if (plan) fill_plan(outs[map[best]], calls[best], plan);
+                return PC_OK;
+            }
         }
     }
     fill_stats(ctx, stats, running, calls_counted, unpruned, cells);

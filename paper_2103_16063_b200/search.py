@@ -224,19 +224,22 @@ def exchange(rec: np.ndarray, group=None, device=None) -> np.ndarray:
     return torch.stack(parts).numpy()
 
 
-def decide(allrec: np.ndarray, calls, levels, owner, plan_w: int, budget, batch_size: int):
-    """Apply the reference's selection to the gathered records.
+def decide(allrec: np.ndarray, calls, levels, owner, plan_w: int, budget, batch_size: int,
+           upto: int | None = None):
+    """Apply the reference's selection to the gathered records (to the first
+    `upto` calls when given: the levels evaluated so far).
 
     Returns ("plan", SearchResult) or ("budget", crossing call, visits before)."""
     n = len(calls)
+    m = n if upto is None else upto
     world = allrec.shape[0]
     per = allrec[:, :n * _REC].reshape(world, n, _REC)
-    own = np.asarray(owner, dtype=np.int64)
-    g = per[own, np.arange(n)] if n else np.zeros((0, _REC))
+    own = np.asarray(owner[:m], dtype=np.int64)
+    g = per[own, np.arange(m)] if m else np.zeros((0, _REC))
     visits = [int(v) for v in g[:, 0]]
     feasible = [bool(f) for f in g[:, 1]]
-    keys = [rank_key(float(g[i, 2]), float(g[i, 3]), calls[i][3], i) for i in range(n)]
-    best, counted, running, cross, before = select(levels, visits, feasible, keys, budget)
+    keys = [rank_key(float(g[i, 2]), float(g[i, 3]), calls[i][3], i) for i in range(m)]
+    best, counted, running, cross, before = select(levels[:m], visits, feasible, keys, budget)
     if cross >= 0:
         return ("budget", cross, before)
     stats = SearchStats(visits=running, dp_calls=counted)
@@ -260,10 +263,17 @@ def decide(allrec: np.ndarray, calls, levels, owner, plan_w: int, budget, batch_
 
 @_lib.serialized
 def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
-                       options=None, *, group=None, timings: dict | None = None):
+                       options=None, *, group=None, timings: dict | None = None,
+                       speculative: bool = True):
     """form_stage with its DP calls spread over every rank of a
     torch.distributed group (one GPU per rank, NCCL); all ranks return the
-    reference's SearchResult."""
+    reference's SearchResult.
+
+    ``speculative`` (SURVEY.md §8e schedule ii) shards every widening level's
+    calls at once and exchanges once; ``speculative=False`` (schedule i, the
+    reference's latency order) runs the levels in order, sharding each level's
+    calls and exchanging after each, and stops at the first level with a
+    feasible plan (or at a budget crossing).  Results and stats are identical."""
     import torch
     import torch.distributed as dist
 
@@ -278,14 +288,17 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
     nb = len(blocks)
     calls, levels = enumerate_calls(num_nodes, devices_per_node, batch_size, nb)
     n_levels = (max(levels) + 1) if levels else 0
-    owner = lpt_shard(nb, calls, world,
-                      device_weights(ctx, calls, batch_size) if world > 1 else None)
+    max_stages = max((c[0] for c in calls), default=1)
+    dev = torch.device("cuda", ctx.device)
+    weights = device_weights(ctx, calls, batch_size) if world > 1 else None
+    if not speculative:
+        return _sharded_by_level(ctx, calls, levels, n_levels, max_stages, nb, weights, world,
+                                 rank, group, dev, opts, batch_size)
+    owner = lpt_shard(nb, calls, world, weights)
     local_idx = [i for i in range(len(calls)) if owner[i] == rank]
     batch = run_calls(ctx, [calls[i] for i in local_idx], batch_size,
                       opts.disable_pruning, True)
-    max_stages = max((c[0] for c in calls), default=1)
     rec, plan_w = _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels, max_stages)
-    dev = torch.device("cuda", ctx.device)
     allrec = exchange(rec, group, dev)
     if timings is not None:
         timings.update(pairs=int(batch.stats.pairs), candidates=int(batch.stats.candidates),
@@ -299,6 +312,17 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
     if out[0] == "plan":
         return out[1]
     _, cross, before = out
+    _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, group, dev, opts,
+                    batch_size)
+
+
+def _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, group, dev, opts,
+                    batch_size):
+    """SearchBudgetExceeded with the exact visit count at the crossing cell,
+    computed by the rank that owns the crossing call (its last batch)."""
+    import torch
+    import torch.distributed as dist
+
     v = np.zeros(1, np.float64)
     if owner[cross] == rank:
         li = local_idx.index(cross)
@@ -315,6 +339,45 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
         dist.broadcast(t, src=owner[cross], group=group)
         v = t.cpu().numpy()
     raise SearchBudgetExceeded(int(v[0]), int(opts.visit_budget))
+
+
+def _sharded_by_level(ctx, calls, levels, n_levels, max_stages, nb, weights, world, rank, group,
+                      dev, opts, batch_size):
+    """Schedule (i): widening levels in order, each level's calls sharded
+    (LPT within the level) and one exchange per level; the reference's rule is
+    applied to the calls evaluated so far after every level."""
+    n = len(calls)
+    owner = [0] * n
+    allrec = None
+    end = 0
+    plan_w = 4 + 6 * max_stages
+    for lv in range(n_levels):
+        start = end
+        while end < n and levels[end] == lv:
+            end += 1
+        idx = list(range(start, end))
+        lv_owner = lpt_shard(nb, [calls[i] for i in idx], world,
+                             None if weights is None else [weights[i] for i in idx])
+        for i, o in zip(idx, lv_owner):
+            owner[i] = o
+        local_idx = [i for i in idx if owner[i] == rank]
+        batch = run_calls(ctx, [calls[i] for i in local_idx], batch_size,
+                          opts.disable_pruning, True)
+        rec, plan_w = _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels,
+                            max_stages)
+        got = exchange(rec, group, dev)
+        allrec = got if allrec is None else allrec + got      # disjoint slots per level
+        out = decide(allrec, calls, levels, owner, plan_w, opts.visit_budget, batch_size,
+                     upto=end)
+        if out[0] == "budget":
+            _, cross, before = out
+            _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, group,
+                            dev, opts, batch_size)
+        result = out[1]
+        if result.plan is not None or end == n:
+            return result
+    return decide(np.zeros((max(world, 1), n * _REC + n_levels * plan_w)), calls, levels,
+                  owner, plan_w, opts.visit_budget, batch_size)[1]
 
 
 def _flat_bytes(flat) -> int:

@@ -122,12 +122,15 @@ def form_stage_dp(blocks, S: int, D: int, batch_size: int, replica_factor: int,
 
 @_lib.serialized
 def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
-               options=None, *, speculative: bool = True, last_stats: dict | None = None):
+               options=None, *, speculative: bool | None = None,
+               last_stats: dict | None = None):
     """Search replica factor, stage count and microbatch count together (GPU).
 
-    ``speculative`` evaluates every widening level in one device batch and
-    then applies the reference's first-feasible-level rule; the result and
-    the stats are identical to the level-by-level order either way.
+    Batching of the widening levels: ``speculative=True`` evaluates every level
+    in one device batch, ``False`` one batch per level, and the default
+    (``None``) the first level alone and then, only if it has no feasible plan,
+    all the others in one batch.  The reference's first-feasible-level rule is
+    applied afterwards, so the result and the stats are identical either way.
     """
     if num_nodes < 1 or devices_per_node < 1 or batch_size < 1:
         raise InvalidArgs("node count, devices per node and batch size must be at least 1")
@@ -142,7 +145,8 @@ def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
     st = abi.PcStats()
     rc = ctx.lib.pc_form_stage(ctx.h, num_nodes, devices_per_node, batch_size,
                                int(bool(opts.disable_pruning)), _budget(opts),
-                               int(bool(speculative)), C.byref(buf.s), C.byref(st))
+                               2 if speculative is None else int(bool(speculative)),
+                               C.byref(buf.s), C.byref(st))
     ctx.check(rc, "form_stage")
     if last_stats is not None:
         last_stats.update(visits=int(st.visits), dp_calls=int(st.dp_calls),

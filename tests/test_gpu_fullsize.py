@@ -45,8 +45,10 @@ def test_full_size_calls_match_oracle(gpu, workload, S, R, MB, modes):
 
 def test_full_size_search_consistent(gpu, workload):
     bs, _ = workload
-    a = result_doc(form_stage(32, 8, BS, bs))
-    b = result_doc(form_stage(32, 8, BS, bs, speculative=False))
+    a = result_doc(form_stage(32, 8, BS, bs))                        # first level, then the rest
+    b = result_doc(form_stage(32, 8, BS, bs, speculative=False))     # level by level
+    assert result_doc(form_stage(32, 8, BS, bs, speculative=True)) == a   # all at once
     c = result_doc(form_stage_sharded(32, 8, BS, bs))
-    assert a == b == c
+    d = result_doc(form_stage_sharded(32, 8, BS, bs, speculative=False))
+    assert a == b == c == d
     assert a["plan"] is not None and a["dp_calls"] == 56

@@ -10,7 +10,7 @@ import pytest
 
 import cases
 from oracle.oracle import OracleProblem, PC_OK
-from paper_2103_16063_b200 import abi, form_stage, form_stage_dp
+from paper_2103_16063_b200 import abi, form_stage, form_stage_dp, form_stage_sharded
 from paper_2103_16063_b200._host import pipecut as pc
 from paper_2103_16063_b200.stages import bind_problem
 from plans import result_doc
@@ -118,7 +118,24 @@ def test_budget_semantics_match_reference(gpu):
                 return ("ok", r.stats.visits)
             except pc.SearchBudgetExceeded as e:
                 return ("budget", e.visits)
-        assert run(form_stage) == run(pc.form_stage), budget
+        want = run(pc.form_stage)
+        assert run(form_stage) == want, budget
+        for spec in (True, False):         # both sharded schedules
+            assert run(lambda *a, **k: form_stage_sharded(*a, speculative=spec, **k)) == want
+    # a multi-level search (2 nodes: widening levels n = 1, 2) with budgets that
+    # cross in either level
+    bs = cases.one_block_per_task(cases.chain([1.0, 2.0, 1.5, 1.0, 3.0]), nodes=2, dpn=2)
+    for budget in (5, 40, 120, 400, 2000, None):
+        def run2(fn):
+            try:
+                r = fn(2, 2, 8, bs, pc.SearchOptions(visit_budget=budget))
+                return ("ok", r.stats.visits, r.stats.dp_calls,
+                        None if r.plan is None else r.plan.objective)
+            except pc.SearchBudgetExceeded as e:
+                return ("budget", e.visits)
+        want = run2(pc.form_stage)
+        for spec in (True, False):
+            assert run2(lambda *a, **k: form_stage_sharded(*a, speculative=spec, **k)) == want
 
 
 def test_form_stage_small_cases(gpu):

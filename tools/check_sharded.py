@@ -30,7 +30,9 @@ for name in ("C1", "C2", "C3", "C4"):
     part, model, k, batch, cl = cases.config_partition(name)
     bs = partition_blocks(part, model, k)
     got = result_doc(form_stage_sharded(cl.num_nodes, cl.devices_per_node, batch, bs))
-    same = got == gold[name]["form_stage"]
+    lvl = result_doc(form_stage_sharded(cl.num_nodes, cl.devices_per_node, batch, bs,
+                                        speculative=False))
+    same = got == gold[name]["form_stage"] == lvl
     ok &= same
     if rank == 0:
         print(f"{name}: sharded over {world} == golden: {same}", flush=True)
@@ -48,7 +50,8 @@ for budget in (2, 20, 45, 80):
             return ("ok", r.stats.visits)
         except pc.SearchBudgetExceeded as e:
             return ("budget", e.visits)
-    same = run(form_stage_sharded) == run(pc.form_stage)
+    same = (run(form_stage_sharded) == run(pc.form_stage)
+            == run(lambda *a, **k: form_stage_sharded(*a, speculative=False, **k)))
     ok &= same
 # measured cost tables: golden form_stage of the reference (tests/golden/cost_tables.json)
 import random  # noqa: E402
