@@ -1,0 +1,291 @@
+// Host-side flattening of an AtomicPartition + CostModel into the atom-level
+// arrays of partition_blocks (paper_2103_16063_b200/flatten.py:
+// _flatten_atoms, blocks.py:73-124), natively: the same traversal of the
+// reference's graph objects without the interpreter loop.  It covers the
+// common case -- every byte count an exact integer that fits int64, no
+// structural violation; anything else raises Fallback and the Python
+// implementation runs (and raises the reference's errors).
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cmath>
+#include <vector>
+
+namespace py = pybind11;
+
+namespace {
+
+struct Fallback {};
+
+// attribute names interned once; ga() = getattr with a new reference
+struct Names {
+    py::str value{"value"}, is_param{"is_param"}, fixed_bytes{"fixed_bytes"},
+        bytes_per_sample{"bytes_per_sample"}, task{"task"}, flops_per_sample{"flops_per_sample"};
+};
+const Names &names() {
+    static Names *n = new Names();
+    return *n;
+}
+inline py::object ga(py::handle o, const py::str &name) {
+    PyObject *r = PyObject_GetAttr(o.ptr(), name.ptr());
+    if (!r) throw py::error_already_set();
+    return py::reinterpret_steal<py::object>(r);
+}
+inline py::handle dget(py::handle dict, py::handle key) {   // borrowed
+    PyObject *r = PyDict_GetItem(dict.ptr(), key.ptr());
+    if (!r) throw Fallback();
+    return r;
+}
+
+// an exact integer byte count (flatten.py: _as_int), else Fallback
+int64_t as_int(PyObject *x) {
+    if (PyLong_CheckExact(x)) {
+        int overflow = 0;
+        const long long v = PyLong_AsLongLongAndOverflow(x, &overflow);
+        if (overflow) throw Fallback();
+        return v;
+    }
+    if (PyFloat_Check(x)) {
+        const double d = PyFloat_AS_DOUBLE(x);
+        if (!(d == std::floor(d)) || std::fabs(d) >= 9007199254740992.0) throw Fallback();
+        return (int64_t)d;
+    }
+    throw Fallback();
+}
+
+int64_t size1(const py::handle &info) {
+    return as_int(ga(info, names().fixed_bytes).ptr()) + as_int(ga(info, names().bytes_per_sample).ptr());
+}
+
+template <class T>
+py::array_t<T> arr(const std::vector<T> &v) {
+    py::array_t<T> a(v.size());
+    if (!v.empty()) std::copy(v.begin(), v.end(), a.mutable_data());
+    return a;
+}
+
+void csr(const std::vector<std::vector<int32_t>> &lists, std::vector<int32_t> &off,
+         std::vector<int32_t> &flat) {
+    off.assign(lists.size() + 1, 0);
+    flat.clear();
+    for (size_t i = 0; i < lists.size(); ++i) {
+        flat.insert(flat.end(), lists[i].begin(), lists[i].end());
+        off[i + 1] = (int32_t)flat.size();
+    }
+}
+
+py::dict flatten(py::object partition, py::object model) {
+    py::object g = model.attr("graph");
+    py::object pg = partition.attr("graph");
+    py::list atoms = partition.attr("atoms");
+    const int n = (int)py::len(atoms);
+    py::dict nodes = g.attr("nodes");
+    // the graph's adjacency dicts (graph.py:56-57: node id -> sorted tuple); a
+    // different reference layout falls back to the Python path
+    py::dict succ_d = g.attr("_succ"), pred_d = g.attr("_pred");
+    py::object graph_inputs = g.attr("inputs");
+    py::object none = py::none();
+
+    // node id -> atom (atoms.py:259-305); duplicates are the Python path's error
+    py::dict atom_of;
+    for (int i = 0; i < n; ++i)
+        for (py::handle nid : py::reinterpret_borrow<py::object>(atoms[i].attr("node_ids"))) {
+            if (atom_of.contains(nid)) throw Fallback();
+            atom_of[nid] = py::int_(i);
+        }
+    auto atom_get = [&](py::handle k) -> int {
+        PyObject *v = PyDict_GetItem(atom_of.ptr(), k.ptr());
+        return v ? (int)PyLong_AsLong(v) : -1;
+    };
+
+    std::vector<py::object> inputs_of_atom(n);
+    py::dict listing;
+    for (int a = 0; a < n; ++a) {
+        inputs_of_atom[a] = py::reinterpret_steal<py::object>(
+            PyFrozenSet_New(atoms[a].attr("input_values").ptr()));
+        for (py::handle v : inputs_of_atom[a]) {
+            PyObject *lst = PyDict_GetItem(listing.ptr(), v.ptr());
+            if (!lst) {
+                py::list l;
+                l.append(a);
+                listing[v] = l;
+            } else {
+                PyList_Append(lst, py::int_(a).ptr());
+            }
+        }
+    }
+    py::list in_ids = py::module_::import("builtins").attr("sorted")(listing);
+    py::dict in_index;
+    std::vector<int32_t> in_owner, in_atoms_off{0}, in_atoms;
+    std::vector<int64_t> in_size;
+    for (size_t i = 0; i < py::len(in_ids); ++i) {
+        py::handle v = in_ids[i];
+        in_index[v] = py::int_(i);
+        py::object node = nodes[v];
+        if (!node.attr("is_value").cast<bool>()) throw Fallback();
+        const int own = atom_get(v);
+        const bool is_input = PySequence_Contains(graph_inputs.ptr(), v.ptr()) == 1;
+        in_owner.push_back((is_input || own < 0) ? -1 : own);
+        in_size.push_back(size1(node.attr("value")));
+        for (py::handle a : py::reinterpret_borrow<py::list>(listing[v]))
+            in_atoms.push_back(a.cast<int32_t>());
+        in_atoms_off.push_back((int32_t)in_atoms.size());
+    }
+    auto in_index_of = [&](py::handle v) -> int {
+        PyObject *x = PyDict_GetItem(in_index.ptr(), v.ptr());
+        return x ? (int)PyLong_AsLong(x) : -1;
+    };
+
+    std::vector<int64_t> atom_param(n, 0), task_fp1, task_prod1, dep_size;
+    std::vector<int32_t> task_atom, dep_off{0}, dep_owner;
+    std::vector<double> task_flops;
+    std::vector<std::vector<int32_t>> atom_tasks(n);
+    py::list tnodes;
+    for (auto item : nodes) {                       // sorted id order (graph.py:90-93)
+        py::handle nid = item.first, node = item.second;
+        const int a = atom_get(nid);
+        if (a < 0) continue;
+        const Names &N = names();
+        py::object value = ga(node, N.value);
+        if (!value.is_none()) {
+            if (PyObject_IsTrue(ga(value, N.is_param).ptr()))
+                atom_param[a] += as_int(ga(value, N.fixed_bytes).ptr());
+            continue;
+        }
+        int64_t fp = 0;
+        for (py::handle vid : dget(succ_d, nid)) {
+            py::object info = ga(dget(nodes, vid), N.value);
+            if (!info.is_none() && !PyObject_IsTrue(ga(info, N.is_param).ptr())) fp += size1(info);
+        }
+        task_prod1.push_back(fp);
+        py::object task = ga(node, N.task);
+        tnodes.append(task);
+        const py::object &ins = inputs_of_atom[a];
+        for (py::handle vid : dget(pred_d, nid)) {
+            py::object info = ga(dget(nodes, vid), N.value);
+            if (info.is_none() || PyObject_IsTrue(ga(info, N.is_param).ptr())) continue;
+            if (PySet_Contains(ins.ptr(), vid.ptr()) == 1) {
+                const int own = in_owner[in_index_of(vid)];
+                if (own >= 0) {
+                    dep_owner.push_back(own);
+                    dep_size.push_back(size1(info));
+                }
+            } else {
+                if (atom_get(vid) != a) throw Fallback();     // cross-atom read: Python raises
+                fp += size1(info);
+            }
+        }
+        dep_off.push_back((int32_t)dep_owner.size());
+        atom_tasks[a].push_back((int32_t)task_atom.size());
+        task_atom.push_back(a);
+        task_flops.push_back(PyFloat_AsDouble(ga(task, N.flops_per_sample).ptr()));
+        task_fp1.push_back(fp);
+    }
+
+    // atom dependencies (atoms.py:115-125) and traffic entries (blocks.py:96-102)
+    // atoms.py:93-106: value id -> owner atom / frozenset of consumer atoms
+    py::dict owner_d = partition.attr("_value_owner");
+    py::dict cons_d = partition.attr("_consumer_atoms");
+    py::dict ppred_d = pg.attr("_pred");
+    py::object value_size = pg.attr("value_size");
+    std::vector<int64_t> dep_keys;
+    std::vector<int32_t> tr_owner;
+    std::vector<int64_t> tr_size;
+    std::vector<std::vector<int32_t>> tr_cons, atom_tr(n);
+    py::object one = py::int_(1);
+    for (py::handle vid : pg.attr("value_ids")()) {
+        const int owner = (int)PyLong_AsLong(dget(owner_d, vid).ptr());
+        std::vector<int32_t> cons;
+        for (py::handle c : dget(cons_d, vid)) cons.push_back((int32_t)PyLong_AsLong(c.ptr()));
+        std::sort(cons.begin(), cons.end());
+        if (PyTuple_GET_SIZE(dget(ppred_d, vid).ptr()) > 0)     // graph.py:84-88: a producer
+            for (int c : cons)
+                if (c != owner) dep_keys.push_back((int64_t)owner * n + c);
+        std::vector<int32_t> foreign;
+        for (int c : cons)
+            if (c != owner) foreign.push_back(c);
+        if (!foreign.empty()) {
+            const int e = (int)tr_owner.size();
+            tr_owner.push_back(owner);
+            py::object sz = value_size(vid, one);
+            tr_size.push_back(as_int(sz.ptr()));
+            std::vector<int32_t> members(foreign);
+            members.push_back(owner);
+            std::sort(members.begin(), members.end());
+            members.erase(std::unique(members.begin(), members.end()), members.end());
+            for (int x : members) atom_tr[x].push_back(e);
+            tr_cons.push_back(std::move(foreign));
+        }
+    }
+    std::sort(dep_keys.begin(), dep_keys.end());
+    dep_keys.erase(std::unique(dep_keys.begin(), dep_keys.end()), dep_keys.end());
+    std::vector<std::vector<int32_t>> succ(n), pred(n), nbr(n);
+    for (int64_t k : dep_keys) {
+        const int a = (int)(k / n), b = (int)(k % n);
+        succ[a].push_back(b);
+        pred[b].push_back(a);
+    }
+    for (int i = 0; i < n; ++i) {
+        std::vector<int32_t> u(succ[i]);
+        u.insert(u.end(), pred[i].begin(), pred[i].end());
+        std::sort(u.begin(), u.end());
+        u.erase(std::unique(u.begin(), u.end()), u.end());
+        nbr[i] = std::move(u);
+    }
+
+    // inputs of each atom by in_ids index, ascending (sorted(ins) then index)
+    std::vector<std::vector<int32_t>> atom_in(n);
+    for (int a = 0; a < n; ++a) {
+        for (py::handle v : inputs_of_atom[a]) atom_in[a].push_back(in_index_of(v));
+        std::sort(atom_in[a].begin(), atom_in[a].end());
+    }
+
+    py::dict out;
+    std::vector<int32_t> off, flat;
+    auto put_csr = [&](const char *o, const char *f, const std::vector<std::vector<int32_t>> &l) {
+        csr(l, off, flat);
+        out[o] = arr(off);
+        out[f] = arr(flat);
+    };
+    out["n"] = n;
+    out["atom_param"] = arr(atom_param);
+    out["task_atom"] = arr(task_atom);
+    out["task_flops"] = arr(task_flops);
+    out["task_fp1"] = arr(task_fp1);
+    out["task_prod1"] = arr(task_prod1);
+    out["dep_off"] = arr(dep_off);
+    out["dep_owner"] = arr(dep_owner);
+    out["dep_size"] = arr(dep_size);
+    put_csr("atom_task_off", "atom_tasks", atom_tasks);
+    put_csr("atom_in_off", "atom_in", atom_in);
+    out["in_owner"] = arr(in_owner);
+    out["in_size"] = arr(in_size);
+    out["in_atoms_off"] = arr(in_atoms_off);
+    out["in_atoms"] = arr(in_atoms);
+    put_csr("succ_off", "succ", succ);
+    put_csr("pred_off", "pred", pred);
+    put_csr("nbr_off", "nbr", nbr);
+    out["tr_owner"] = arr(tr_owner);
+    out["tr_size"] = arr(tr_size);
+    put_csr("tr_cons_off", "tr_cons", tr_cons);
+    put_csr("atom_tr_off", "atom_tr", atom_tr);
+    out["tnodes"] = tnodes;
+    return out;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_flatten_native, m) {
+    static py::exception<Fallback> fallback(m, "Fallback");
+    py::register_exception_translator([](std::exception_ptr p) {
+        try {
+            if (p) std::rethrow_exception(p);
+        } catch (const Fallback &) {
+            PyErr_SetString(fallback.ptr(), "outside the native path's common case");
+        }
+    });
+    m.def("flatten_atoms", &flatten, "atom-level arrays of partition_blocks (flatten.py)");
+}

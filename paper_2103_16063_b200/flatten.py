@@ -378,7 +378,49 @@ def flatten_atoms(partition, model) -> FlatAtoms:
     return fa
 
 
+try:                                         # C++ traversal (csrc/flatten_native.cpp)
+    from . import _flatten_native
+except ImportError:                          # pragma: no cover - built by build()
+    _flatten_native = None
+
+
 def _flatten_atoms(partition, model) -> FlatAtoms:
+    """Native flattening for the common case; anything it does not cover
+    (non-integer byte counts, structural violations) runs the Python
+    restatement below, which raises the reference-facing errors."""
+    if _flatten_native is not None:
+        try:
+            d = _flatten_native.flatten_atoms(partition, model)
+        except Exception:
+            d = None
+        if d is not None:
+            return _atoms_from_arrays(d, model)
+    return _flatten_atoms_py(partition, model)
+
+
+def _atoms_from_arrays(d, model) -> FlatAtoms:
+    cfg = model.config
+    ov = resolve_overrides(cfg, d["tnodes"], [1]) if cfg.cost_table is not None else None
+    return FlatAtoms(
+        n=int(d["n"]), atom_param=d["atom_param"], task_atom=d["task_atom"],
+        task_flops=d["task_flops"], task_fp1=d["task_fp1"], task_prod1=d["task_prod1"],
+        ov_has=None if ov is None else ov[1][0], ov_tf=None if ov is None else ov[2][0],
+        ov_tb=None if ov is None else ov[3][0], ov_act=None if ov is None else ov[4][0],
+        dep_off=d["dep_off"], dep_owner=d["dep_owner"], dep_size=d["dep_size"],
+        atom_task_off=d["atom_task_off"], atom_tasks=d["atom_tasks"],
+        atom_in_off=d["atom_in_off"], atom_in=d["atom_in"],
+        in_owner=d["in_owner"], in_size=d["in_size"], in_atoms_off=d["in_atoms_off"],
+        in_atoms=d["in_atoms"], succ_off=d["succ_off"], succ=d["succ"],
+        pred_off=d["pred_off"], pred=d["pred"], nbr_off=d["nbr_off"], nbr=d["nbr"],
+        tr_owner=d["tr_owner"], tr_size=d["tr_size"], tr_cons_off=d["tr_cons_off"],
+        tr_cons=d["tr_cons"], atom_tr_off=d["atom_tr_off"], atom_tr=d["atom_tr"],
+        budget=_as_int(model.cluster.device_memory_bytes, "device_memory_bytes"),
+        flops_per_sec=float(cfg.device_flops_per_sec), bwd_fwd_ratio=float(cfg.bwd_fwd_ratio),
+        factor_g=float(cfg.grad_factor), factor_o=float(cfg.optimizer_state_factor),
+    )
+
+
+def _flatten_atoms_py(partition, model) -> FlatAtoms:
     cfg = model.config
     g = model.graph
     pg = partition.graph
