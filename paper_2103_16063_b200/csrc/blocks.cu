@@ -787,6 +787,8 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
     // ---- refinement: speculative rounds over the recorded merges (blocks.py:173-232)
     const int top = (int)co.levels.size() - 1;
     long long n_rounds = 0, n_sets = 0, n_moves = 0;
+    std::vector<std::vector<int>> map_cache(co.levels.size());
+    std::vector<char> map_valid(co.levels.size(), 0);
     double t_dev = 0.0;
     for (int li = (int)transitions.size() - 1; li >= 0; --li) {
         const auto &pairs = transitions[li];
@@ -795,8 +797,13 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
             for (int l = li; l <= top; ++l)
                 if (co.dirty[l])
                     if (int rc = co.upload_level(l, co.levels[l])) return rc;
-            std::vector<std::vector<int>> maps(top + 1);
-            for (int l = li; l <= top; ++l) maps[l] = member_map(n, co.levels[l]);
+            // atom -> group maps, rebuilt only for levels a move changed
+            for (int l = li; l <= top; ++l)
+                if (!map_valid[l]) {
+                    map_cache[l] = member_map(n, co.levels[l]);
+                    map_valid[l] = 1;
+                }
+            const std::vector<std::vector<int>> &maps = map_cache;
             struct Tri { int q, mi, ti, mv; int64_t set0; };
             std::vector<Tri> tris;
             std::vector<SetDesc> sets;
@@ -864,7 +871,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
                     for (int a : mover) in_mover[a] = 1;
                     for (int ell = li + 1; ell <= top; ++ell) {
                         auto &lev = co.levels[ell];
-                        const std::vector<int> mm = member_map(n, lev);
+                        const std::vector<int> &mm = map_cache[ell];   // current until changed below
                         const int si = mm[mover[0]], di = mm[target[0]];
                         std::vector<int> shr;
                         for (int a : lev[si])
@@ -876,6 +883,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
                         lev[di] = gr;
                         sort_by_first(lev);
                         co.dirty[ell] = 1;
+                        map_valid[ell] = 0;
                     }
                     applied = true;
                     p = q + 1;
