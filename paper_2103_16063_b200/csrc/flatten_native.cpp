@@ -276,6 +276,195 @@ py::dict flatten(py::object partition, py::object model) {
     return out;
 }
 
+// Block-level arrays of the span profile (flatten.py: flatten_blockset,
+// costs.py:97-160 over BlockSet spans).  Same conventions: the common case
+// natively, every structural violation -> Fallback (the Python restatement
+// raises UnsupportedGraph with its message).
+py::dict flatten_blocks(py::object bs) {
+    const Names &N = names();
+    py::object model = bs.attr("model");
+    py::object g = model.attr("graph");
+    py::object part = bs.attr("partition");
+    py::list atoms = part.attr("atoms");
+    const int n_atoms = (int)py::len(atoms);
+    py::tuple block_atoms = bs.attr("block_atoms");
+    const int nb = (int)py::len(block_atoms);
+    py::dict nodes = g.attr("nodes");
+    py::dict succ_d = g.attr("_succ"), pred_d = g.attr("_pred");
+    py::object graph_inputs = g.attr("inputs");
+
+    py::dict atom_of;
+    for (int i = 0; i < n_atoms; ++i)
+        for (py::handle nid : py::reinterpret_borrow<py::object>(atoms[i].attr("node_ids"))) {
+            if (atom_of.contains(nid)) throw Fallback();
+            atom_of[nid] = py::int_(i);
+        }
+    std::vector<int> block_of_atom(n_atoms, -1);
+    int covered = 0;
+    for (int bi = 0; bi < nb; ++bi)
+        for (py::handle a : py::reinterpret_borrow<py::object>(block_atoms[bi])) {
+            const long ai = PyLong_AsLong(a.ptr());
+            if (ai < 0 || ai >= n_atoms) throw Fallback();
+            if (block_of_atom[ai] < 0) ++covered;
+            block_of_atom[ai] = bi;
+        }
+    if (covered != n_atoms) throw Fallback();
+    auto atom_get = [&](py::handle k) -> int {
+        PyObject *v = PyDict_GetItem(atom_of.ptr(), k.ptr());
+        return v ? (int)PyLong_AsLong(v) : -1;
+    };
+    auto blk_of = [&](py::handle k) -> int {
+        const int a = atom_get(k);
+        return a < 0 ? -1 : block_of_atom[a];
+    };
+
+    // values in some atom's input_values and their consumer blocks
+    std::vector<py::object> inputs_of_atom(n_atoms);
+    py::dict cons_of;                             // vid -> index into cons_sets
+    std::vector<std::vector<int32_t>> cons_sets;
+    for (int a = 0; a < n_atoms; ++a) {
+        inputs_of_atom[a] = py::reinterpret_steal<py::object>(
+            PyFrozenSet_New(atoms[a].attr("input_values").ptr()));
+        for (py::handle v : inputs_of_atom[a]) {
+            PyObject *k = PyDict_GetItem(cons_of.ptr(), v.ptr());
+            int ci;
+            if (!k) {
+                ci = (int)cons_sets.size();
+                cons_sets.emplace_back();
+                cons_of[v] = py::int_(ci);
+            } else {
+                ci = (int)PyLong_AsLong(k);
+            }
+            cons_sets[ci].push_back(block_of_atom[a]);
+        }
+    }
+    py::list in_ids = py::module_::import("builtins").attr("sorted")(cons_of);
+    py::dict in_index;
+    std::vector<int32_t> in_ob, in_off{0}, in_cons;
+    std::vector<int64_t> in_fix, in_ps;
+    for (size_t i = 0; i < py::len(in_ids); ++i) {
+        py::handle vid = in_ids[i];
+        in_index[vid] = py::int_(i);
+        py::handle node = dget(nodes, vid);
+        py::object info = ga(node, N.value);
+        if (info.is_none()) throw Fallback();                 // not a value
+        std::vector<int32_t> cb = cons_sets[PyLong_AsLong(dget(cons_of, vid).ptr())];
+        std::sort(cb.begin(), cb.end());
+        cb.erase(std::unique(cb.begin(), cb.end()), cb.end());
+        int ob;
+        if (PySequence_Contains(graph_inputs.ptr(), vid.ptr()) == 1) {
+            ob = -1;
+            const int own = blk_of(vid);
+            if (own >= 0 && !std::binary_search(cb.begin(), cb.end(), own)) throw Fallback();
+        } else {
+            ob = blk_of(vid);
+            if (ob > cb[0]) throw Fallback();
+        }
+        in_ob.push_back(ob);
+        in_cons.insert(in_cons.end(), cb.begin(), cb.end());
+        in_off.push_back((int32_t)in_cons.size());
+        in_fix.push_back(as_int(ga(info, N.fixed_bytes).ptr()));
+        in_ps.push_back(as_int(ga(info, N.bytes_per_sample).ptr()));
+    }
+    auto in_index_of = [&](py::handle v) -> int {
+        PyObject *x = PyDict_GetItem(in_index.ptr(), v.ptr());
+        return x ? (int)PyLong_AsLong(x) : -1;
+    };
+
+    std::vector<int64_t> blk_param(nb, 0), blk_res_fix(nb, 0), blk_res_ps(nb, 0);
+    std::vector<int32_t> task_block, dep_off{0}, dep_ob;
+    std::vector<double> task_flops;
+    std::vector<int64_t> fp_fix, fp_ps, dep_fix, dep_ps, prod_fix, prod_ps;
+    py::list task_nodes;
+    for (auto kv : nodes) {                       // sorted id order (graph.py:90-93)
+        py::handle nid = kv.first, node = kv.second;
+        const int b = blk_of(nid);
+        if (b < 0) continue;
+        py::object info = ga(node, N.value);
+        if (!info.is_none()) {
+            if (PyObject_IsTrue(ga(info, N.is_param).ptr())) {
+                blk_param[b] += as_int(ga(info, N.fixed_bytes).ptr());
+            } else if (PyTuple_GET_SIZE(dget(pred_d, nid).ptr()) == 0) {     // no producer
+                const bool span_input = PySequence_Contains(graph_inputs.ptr(), nid.ptr()) == 1 &&
+                                        in_index_of(nid) >= 0;
+                if (!span_input) {
+                    blk_res_fix[b] += as_int(ga(info, N.fixed_bytes).ptr());
+                    blk_res_ps[b] += as_int(ga(info, N.bytes_per_sample).ptr());
+                }
+            }
+            continue;
+        }
+        py::object task = ga(node, N.task);
+        const int a = atom_get(nid);
+        int64_t pf = 0, pp = 0;
+        for (py::handle vid : dget(succ_d, nid)) {
+            py::object vi = ga(dget(nodes, vid), N.value);
+            if (!vi.is_none() && !PyObject_IsTrue(ga(vi, N.is_param).ptr())) {
+                pf += as_int(ga(vi, N.fixed_bytes).ptr());
+                pp += as_int(ga(vi, N.bytes_per_sample).ptr());
+            }
+        }
+        blk_res_fix[b] += pf;
+        blk_res_ps[b] += pp;
+        int64_t bf = pf, bp = pp;
+        const py::object &ins = inputs_of_atom[a];
+        for (py::handle vid : dget(pred_d, nid)) {
+            py::object vi = ga(dget(nodes, vid), N.value);
+            if (vi.is_none() || PyObject_IsTrue(ga(vi, N.is_param).ptr())) continue;
+            const int64_t vf = as_int(ga(vi, N.fixed_bytes).ptr());
+            const int64_t vp = as_int(ga(vi, N.bytes_per_sample).ptr());
+            const int i = in_index_of(vid);
+            if (i < 0) {
+                bf += vf;
+                bp += vp;
+                continue;
+            }
+            const int ob = in_ob[i];
+            if (PySet_Contains(ins.ptr(), vid.ptr()) != 1) {
+                if (ob != b) throw Fallback();       // cross-atom read: Python raises
+                bf += vf;
+                bp += vp;
+                continue;
+            }
+            if (ob < 0) continue;                    // model input / unowned
+            dep_ob.push_back(ob);
+            dep_fix.push_back(vf);
+            dep_ps.push_back(vp);
+        }
+        task_block.push_back(b);
+        task_flops.push_back(PyFloat_AsDouble(ga(task, N.flops_per_sample).ptr()));
+        task_nodes.append(task);
+        fp_fix.push_back(bf);
+        fp_ps.push_back(bp);
+        prod_fix.push_back(pf);
+        prod_ps.push_back(pp);
+        dep_off.push_back((int32_t)dep_ob.size());
+    }
+    if (PyErr_Occurred()) throw py::error_already_set();
+
+    py::dict out;
+    out["task_block"] = arr(task_block);
+    out["task_flops"] = arr(task_flops);
+    out["task_fp_fix"] = arr(fp_fix);
+    out["task_fp_ps"] = arr(fp_ps);
+    out["task_prod_fix"] = arr(prod_fix);
+    out["task_prod_ps"] = arr(prod_ps);
+    out["task_dep_off"] = arr(dep_off);
+    out["dep_ob"] = arr(dep_ob);
+    out["dep_fix"] = arr(dep_fix);
+    out["dep_ps"] = arr(dep_ps);
+    out["in_ob"] = arr(in_ob);
+    out["in_cons_off"] = arr(in_off);
+    out["in_cons"] = arr(in_cons);
+    out["in_fix"] = arr(in_fix);
+    out["in_ps"] = arr(in_ps);
+    out["blk_param"] = arr(blk_param);
+    out["blk_res_fix"] = arr(blk_res_fix);
+    out["blk_res_ps"] = arr(blk_res_ps);
+    out["task_nodes"] = task_nodes;
+    return out;
+}
+
 }  // namespace
 
 PYBIND11_MODULE(_flatten_native, m) {
@@ -288,4 +477,5 @@ PYBIND11_MODULE(_flatten_native, m) {
         }
     });
     m.def("flatten_atoms", &flatten, "atom-level arrays of partition_blocks (flatten.py)");
+    m.def("flatten_blocks", &flatten_blocks, "block-level span-profile arrays (flatten.py)");
 }

@@ -130,6 +130,53 @@ def atom_node_tables(partition):
 
 
 def flatten_blockset(bs) -> FlatProblem:
+    """Native traversal for the common case (csrc/flatten_native.cpp), the
+    Python restatement below otherwise (it raises UnsupportedGraph)."""
+    if _flatten_native is not None:
+        try:
+            d = _flatten_native.flatten_blocks(bs)
+        except Exception:
+            d = None
+        if d is not None:
+            return _problem_from_arrays(d, bs)
+    return _flatten_blockset_py(bs)
+
+
+def _problem_from_arrays(d, bs) -> FlatProblem:
+    model = bs.model
+    cfg = model.config
+    cl = model.cluster
+    tb = d["task_block"]
+    monotone = bool(np.all(tb[1:] >= tb[:-1])) if tb.size else True
+    return FlatProblem(
+        nb=len(bs.block_atoms),
+        task_block=tb, task_flops=d["task_flops"],
+        task_fp_fix=d["task_fp_fix"], task_fp_ps=d["task_fp_ps"],
+        task_prod_fix=d["task_prod_fix"], task_prod_ps=d["task_prod_ps"],
+        task_dep_off=d["task_dep_off"], dep_ob=d["dep_ob"],
+        dep_fix=d["dep_fix"], dep_ps=d["dep_ps"],
+        in_ob=d["in_ob"], in_cons_off=d["in_cons_off"], in_cons=d["in_cons"],
+        in_fix=d["in_fix"], in_ps=d["in_ps"],
+        blk_param=d["blk_param"], blk_res_fix=d["blk_res_fix"], blk_res_ps=d["blk_res_ps"],
+        cut_fixed=_i64([_as_int(x, "cut_fixed") for x in bs._cut_fixed]),
+        cut_ps=_f64([float(x) for x in bs._cut_per_sample]),
+        flops_per_sec=float(cfg.device_flops_per_sec),
+        bwd_fwd_ratio=float(cfg.bwd_fwd_ratio),
+        grad_factor=float(cfg.grad_factor),
+        opt_factor=float(cfg.optimizer_state_factor),
+        checkpointing=bool(cfg.checkpointing),
+        num_nodes=int(cl.num_nodes), devices_per_node=int(cl.devices_per_node),
+        mem_budget=_as_int(cl.device_memory_bytes, "device_memory_bytes"),
+        bw_intra=float(cl.bw_intra), bw_inter=float(cl.bw_inter),
+        latency=float(cl.link_latency_sec),
+        monotone=monotone,
+        has_cost_table=cfg.cost_table is not None,
+        task_nodes=list(d["task_nodes"]),
+        cost_config=cfg,
+    )
+
+
+def _flatten_blockset_py(bs) -> FlatProblem:
     model = bs.model
     cfg = model.config
     cl = model.cluster
