@@ -413,11 +413,13 @@ struct Coarsener {
           lev_off(c->cb.lev_off), lev_at(c->cb.lev_at), sets_d(c->cb.sets_d),
           scratch_d(c->cb.scratch_d), out_d(c->cb.out_d), comp_d(c->cb.comp_d), mv_d(c->cb.mv_d),
           lev_cap(c->cb.lev_cap), pin(c->cb.pin) {
-        if (c->cb.lev_n != n) {          // slot layout depends on n
+        if (c->cb.lev_n != n) {          // slot layout depends on n: re-slice, keep the memory
             cudaStreamSynchronize(c->st);
-            lev_cap = 0;
-            if (pin) cudaFreeHost(pin);
-            pin = nullptr;
+            const size_t fit_g = c->cb.lev_grp.n / (sizeof(int32_t) * (size_t)std::max(n, 1));
+            const size_t fit_o = c->cb.lev_off.n / (sizeof(int32_t) * (size_t)(n + 1));
+            const size_t fit_a = c->cb.lev_at.n / (sizeof(int32_t) * (size_t)std::max(n, 1));
+            const size_t fit_p = c->cb.pin_bytes / (sizeof(int32_t) * (3 * (size_t)n + 1));
+            lev_cap = (int)std::min(std::min(fit_g, fit_o), std::min(fit_a, fit_p));
             c->cb.lev_n = n;
         }
     }
@@ -511,6 +513,7 @@ struct Coarsener {
             CUDA_TRY(ctx, a2.ensure(sizeof(int32_t) * (size_t)cap * n));
             int32_t *p2 = nullptr;
             CUDA_TRY(ctx, cudaMallocHost(&p2, sizeof(int32_t) * per * cap));
+            ctx->cb.pin_bytes = sizeof(int32_t) * per * cap;
             if (lev_cap) {
                 CUDA_TRY(ctx, cudaMemcpy(g2.p, lev_grp.p, sizeof(int32_t) * (size_t)lev_cap * n, cudaMemcpyDeviceToDevice));
                 CUDA_TRY(ctx, cudaMemcpy(o2.p, lev_off.p, sizeof(int32_t) * (size_t)lev_cap * (n + 1), cudaMemcpyDeviceToDevice));

@@ -43,6 +43,7 @@ struct CoarsenBufs {
     int lev_cap = 0;          // level slots valid for lev_n atoms
     int lev_n = -1;
     int32_t *pin = nullptr;   // pinned level staging [lev_cap][3 * lev_n + 1]
+    size_t pin_bytes = 0;
     ~CoarsenBufs() {
         if (pin) cudaFreeHost(pin);
     }
