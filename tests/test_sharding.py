@@ -1,5 +1,5 @@
 """CPU: the multi-GPU host logic of form_stage_sharded -- enumeration order,
-LPT sharding, record packing, the all-gather exchange (gloo, world_size 2)
+LPT sharding, record packing, the all-gather exchange (gloo, world_size 2 and 4)
 and the reference's selection / budget rule -- against the reference."""
 
 import os
@@ -171,13 +171,13 @@ def _worker(rank, world, port, seed, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("seed", [0, 3])
-def test_two_rank_gloo_exchange_matches_single_rank(seed):
+@pytest.mark.parametrize("seed,world", [(0, 2), (3, 2), (5, 4)])
+def test_gloo_exchange_matches_single_rank(seed, world):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, seed, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, seed, q)) for r in range(world)]
     for p in procs:
         p.start()
     outs = [q.get(timeout=120) for _ in procs]
@@ -194,7 +194,7 @@ def test_two_rank_gloo_exchange_matches_single_rank(seed):
         else:
             assert plan["microbatches"] == calls[want[1]][3]
             assert plan["objective"] == recs[want[1]][0].objective
-    assert outs[0][1:] == outs[1][1:]
+    assert all(o[1:] == outs[0][1:] for o in outs)
 
 
 def test_select_matches_reference_form_stage_semantics_live():
