@@ -585,15 +585,6 @@ struct Coarsener {
         return PC_OK;
     }
 
-    int savings(const std::vector<MoveDesc> &mv, std::vector<int64_t> &out) {
-        const int nm = (int)mv.size();
-        out.assign(nm, 0);
-        if (!nm) return PC_OK;
-        if (int rc = savings_async(mv, out)) return rc;
-        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
-        return PC_OK;
-    }
-
     // launch + async read-back into out (sized by the caller); no sync
     int savings_async(const std::vector<MoveDesc> &mv, std::vector<int64_t> &out) {
         const int nm = (int)mv.size();
