@@ -3,18 +3,28 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, NCCL)
 
-Workload (config.workload): the C5 DP scaling sweep point of BASELINE.json
-configs[4] -- an enlarged-BERT layer chain (one BERT-1024 layer per block,
-+-10% seeded FLOP jitter), nb blocks on D devices (D/8 nodes x 8), batch 8*D,
-every (n, S, MB) call of form_stage evaluated (full enumeration), the plan
-chosen by the reference's first-feasible-level rule.  A step is one complete
-search.  DP cells/s = the reference's unpruned SearchStats.visits unit
- / step time.  Multi-GPU: the calls are sharded (LPT) over the
-ranks, one NCCL all-gather of fixed-size records per step: strong scaling.
+Workload (config.workload): the largest point of BASELINE.json configs[4],
+the C5 DP scaling sweep -- an enlarged-BERT layer chain (one BERT-1024 layer
+per block, +-10% seeded FLOP jitter), nb = 4096 blocks on D = 1024 devices
+(128 nodes x 8), batch 8*D, every (n, S, MB) call of form_stage evaluated
+(full enumeration, 672 calls), the plan chosen by the reference's
+first-feasible-level rule.  A step is one complete search.  DP cells/s = the
+reference's unpruned SearchStats.visits unit / step time.
+Multi-GPU: the calls are sharded (LPT) over the ranks, one NCCL all-gather
+of fixed-size records per step: strong scaling.
 
-value: problem resident on the device, span/cut tables rebuilt every step.
-e2e:   the public API form_stage_sharded() per step, including host
-       flattening, host->device upload of the problem and device->host results.
+Every timed step is one call of the public API, form_stage_sharded(), from
+the host BlockSet: host flattening, host->device upload, span/cut tables, the
+DP, backtrack, simulate, exchange and the result objects.
+  e2e   = unpruned visits / wall time of that call (max over ranks)
+  value = unpruned visits / its device-resident part (CUDA events on the
+          library stream from after the upload to the result; max over ranks)
+A 512 MiB L2 flush precedes every step.  At N = 1 the line adds the 16-point
+sweep, the C1-C4 latencies with a phase breakdown and the reference's own
+C1-C4 times from this run, and a single-core reference sample.
+
+--impl reference: the unmodified reference (baseline/_ref) on all host cores
+through its own form_stage_dp (baseline/ref_arm.py; no repo code loaded).
 """
 
 from __future__ import annotations
@@ -27,14 +37,14 @@ import subprocess
 import sys
 import time
 
-import numpy as np
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DEFAULT_NB = 1024
-DEFAULT_D = 256
+DEFAULT_NB = 4096
+DEFAULT_D = 1024
 JITTER_SEED = 0
+SWEEP_NB = (64, 256, 1024, 4096)
+SWEEP_D = (8, 64, 256, 1024)
 
 
 def parse():
@@ -45,13 +55,23 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nb", type=int, default=DEFAULT_NB)
     ap.add_argument("--D", type=int, default=DEFAULT_D)
-    ap.add_argument("--cpu-sample-sec", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=int, default=3 * 10 ** 6,
+                    help="visits per reference worker per step (deterministic prefix)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     return ap.parse_args()
 
 
-def workload_config(nb, D, calls, unpruned):
+def call_list(nb, D):
+    sys.path.insert(0, os.path.join(ROOT, "baseline"))
+    from ref_arm import enumerate_calls, unpruned      # no repo package: shared by both arms
+    calls = enumerate_calls(max(1, D // 8), min(8, D), 8 * D, nb)
+    return calls, sum(unpruned(nb, c) for c in calls)
+
+
+def workload_config(nb, D):
+    calls, unpruned = call_list(nb, D)
     nodes, dpn = max(1, D // 8), min(8, D)
     return {
         "workload": f"C5 enlarged-BERT layer chain: nb={nb} blocks, D={D} devices "
@@ -59,7 +79,7 @@ def workload_config(nb, D, calls, unpruned):
         "nb": nb, "devices": D, "batch": 8 * D, "calls": len(calls),
         "unpruned_visits_per_step": unpruned, "jitter_seed": JITTER_SEED,
         "parallelism": "calls sharded over GPUs (LPT), one NCCL all-gather",
-        "l2": "span/cut tables rebuilt each step (> L2); 512 MiB L2 flush between steps",
+        "l2": "span/cut tables rebuilt each step; 512 MiB L2 flush before every step",
     }
 
 
@@ -67,7 +87,7 @@ def workload_config(nb, D, calls, unpruned):
 class Clocks:
     def __init__(self, index):
         self.proc = None
-        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}_{index}.csv")
         self.index = index
 
     def __enter__(self):
@@ -109,376 +129,352 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
-# --------------------------------------------------------------------------- CPU legs
-def _ref_worker_init(nb, D):
-    global _REF_BS
-    from paper_2103_16063_b200.workloads import c5_blockset
-    _REF_BS = c5_blockset(nb, D, jitter_seed=JITTER_SEED)
-
-
-class _Deadline:
-    """SearchOptions-compatible options for the unmodified reference: pruning
-    off (the metric's unit) or on (its stock default), and `visit_budget` None
-    until the deadline, then -1 -- the reference's own per-cell check
-    (stages.py:214-216) then raises SearchBudgetExceeded carrying the exact
-    visit count reached."""
-
-    def __init__(self, seconds, disable_pruning=True):
-        self._end = time.perf_counter() + seconds
-        self.disable_pruning = disable_pruning
-
-    @property
-    def visit_budget(self):
-        return None if time.perf_counter() < self._end else -1
-
-
-def _ref_run(args):
-    """The reference's own form_stage_dp on one call of the workload for about
-    `seconds` of wall time; returns (visits, seconds)."""
-    import pipecut
-    (S, D, R, MB), bs_batch, seconds = args[:3]
-    unpruned = args[3] if len(args) > 3 else True
-    t0 = time.perf_counter()
-    try:
-        res = pipecut.form_stage_dp(_REF_BS, S, D, bs_batch, R, MB, _Deadline(seconds, unpruned))
-        visits = res.stats.visits
-    except pipecut.SearchBudgetExceeded as exc:
-        visits = exc.visits
-    return visits, time.perf_counter() - t0
-
-
-def sample_calls(calls, k):
-    step = max(1, len(calls) // k)
-    return [calls[(i * step) % len(calls)] for i in range(k)]
-
-
-class RefSampler:
-    """Reference visits/s on `cores` host processes, each running one call of
-    the workload (calls spread over the enumeration) for `seconds`."""
-
-    def __init__(self, nb, D, calls, seconds, cores, unpruned=True):
-        import multiprocessing as mp
-        self.cores = cores
-        self.calls = sample_calls(calls, cores)
-        self.work = [(c, 8 * D, seconds, unpruned) for c in self.calls]
-        if cores == 1:
-            _ref_worker_init(nb, D)
-            self.pool = None
-        else:
-            self.pool = mp.get_context("fork").Pool(cores, initializer=_ref_worker_init,
-                                                    initargs=(nb, D))
-
-    def rate(self):
-        out = self.pool.map(_ref_run, self.work) if self.pool else [_ref_run(w) for w in self.work]
-        return sum(o[0] for o in out) / max(o[1] for o in out)
-
-    def close(self):
-        if self.pool:
-            self.pool.close()
-            self.pool.join()
-
-
+# --------------------------------------------------------------------------- reference arm
 def run_reference_arm(a):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """The unmodified reference on all host cores (rank 0 only; baseline/ref_arm.py)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    from paper_2103_16063_b200._host import pipecut  # noqa: F401  (baseline/_ref)
-    from paper_2103_16063_b200.search import enumerate_calls
-    from paper_2103_16063_b200.workloads import unpruned_visits
-    nodes, dpn = max(1, a.D // 8), min(8, a.D)
-    calls, _ = enumerate_calls(nodes, dpn, 8 * a.D, a.nb)
+    sys.path.insert(0, os.path.join(ROOT, "baseline"))
+    import ref_arm
     cores = os.cpu_count() or 1
-    per_step = max(2.0, min(a.cpu_sample_sec, 120.0 / max(1, a.steps + a.warmup)))
-    sampler = RefSampler(a.nb, a.D, calls, per_step, cores)
-    rates = []
+    pool = ref_arm.make_pool(a.nb, a.D, cores, JITTER_SEED)
+    vals, last = [], None
     for i in range(a.warmup + a.steps):
-        r = sampler.rate()
+        last = ref_arm.sample(a.nb, a.D, cores, a.ref_budget, JITTER_SEED, pool)
         if i >= a.warmup:
-            rates.append(r)
-    sampler.close()
-    value = sorted(rates)[len(rates) // 2]
-    stock_sampler = RefSampler(a.nb, a.D, calls, per_step, cores, unpruned=False)
-    stock = stock_sampler.rate()
-    stock_sampler.close()
+            vals.append(last["value"])
+    pool.close()
+    pool.join()
+    value = sorted(vals)[len(vals) // 2]
     sample = (f"{cores} processes x one call of the workload each (calls spread over the "
-              f"enumeration), the reference's pipecut.form_stage_dp with pruning off, each "
-              f"stopped after ~{per_step:.0f} s by its own visit-budget check; "
-              f"value = total visits / slowest worker")
+              f"enumeration), the reference's pipecut.form_stage_dp with pruning off, stopped "
+              f"by its own visit-budget check after exactly {a.ref_budget} visits (a "
+              f"deterministic prefix: the same work every step); value = total visits / "
+              f"slowest worker, median over steps. Prefixes lie in level 1 where a cell "
+              f"costs O(1) but counts up to b*d visits: favours the reference")
     line = {
         "impl": "reference", "metric": "dp_cells_per_sec", "value": value,
         "unit": "visits/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": last["seconds"] * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(a.nb, a.D, calls, unpruned_visits(a.nb, calls)),
+        "config": workload_config(a.nb, a.D),
         "cpu_baseline": {"value": value, "unit": "visits/s", "cores": cores,
-                         "kind": "reference", "sample": sample,
-                         "stock_path": {"pruned_visits_per_sec": stock,
-                                        "note": "same workers, the reference's default options "
-                                                "(pruning on); rate in its own pruned visits. "
-                                                "Bounded samples start at level 1 (O(1) per cell, "
-                                                "up to b*d visits), which favours the reference"}},
+                         "kind": "reference", "sample": sample, "calls": last["calls"],
+                         "per_step": vals},
         "e2e": {"value": value, "unit": "visits/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def ref_subprocess(*args, timeout=900):
+    """Run baseline/ref_arm.py in a fresh interpreter (no repo code loaded)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "baseline", "ref_arm.py"), *args],
+                         capture_output=True, text=True, timeout=timeout)
+    if out.returncode != 0:
+        return {"error": out.stderr.strip().splitlines()[-1:] or ["failed"]}
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
 # --------------------------------------------------------------------------- GPU arm
+class Arm:
+    """One process per GPU: the library context, the L2 flush buffer and the
+    max-over-ranks helpers."""
+
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+        self.dev = torch.device("cuda", self.local)
+        from paper_2103_16063_b200 import _lib
+        self.ctx = _lib.context(self.local)
+        self.flush_buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=self.dev)
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, xs):
+        if self.world == 1:
+            return list(xs)
+        t = self.torch.tensor(list(xs), dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.cpu().tolist()
+
+    def fresh(self):
+        """Forget the bound problem and the span tables: the next call flattens,
+        uploads and rebuilds everything."""
+        self.ctx.problem_owner = None
+        self.ctx.check(self.ctx.lib.pc_reset_cache(self.ctx.h), "reset")
+        self.flush_buf.zero_()
+
+    def step(self, nodes, dpn, BS, bs, **kw):
+        """One public-API search; returns (result, timings, e2e_ms, resident_ms),
+        times max over ranks."""
+        from paper_2103_16063_b200.search import form_stage_sharded
+        self.fresh()
+        self.barrier()
+        tim = {}
+        t0 = time.perf_counter()
+        res = form_stage_sharded(nodes, dpn, BS, bs, timings=tim, **kw)
+        self.torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        e2e_ms, res_ms = self.max_over_ranks([wall, tim.get("resident_ms", wall)])
+        return res, tim, e2e_ms, res_ms
+
+
+PHASES = ("flatten_ms", "upload_ms", "weights_ms", "span_ms", "dp_ms", "post_ms",
+          "run_calls_ms", "pack_ms", "exchange_ms", "decide_ms")
+
+
+def roofline(nb, calls_local, tims, dadd_peak, mix_peak, steps):
+    """Dominant kernel k_dp_level: SURVEY §8(d) algorithmic fp64 work over its
+    measured launch time, against the measured pure-DADD rate."""
+    from paper_2103_16063_b200.workloads import unpruned_visits
+    pairs = sum(t["pairs"] for t in tims)
+    cands = sum(t["candidates"] for t in tims)
+    dp_ms = sum(t["dp_ms"] for t in tims)
+    launches = sum(t["dp_launches"] for t in tims)
+    f_bar = cands / pairs if pairs else 0.0
+    ops = unpruned_visits(nb, calls_local) * steps * (2.0 + 4.0 * f_bar)
+    achieved = ops / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
+    ops_exec = 2.0 * pairs + 4.0 * cands
+    exec_rate = ops_exec / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
+    out = {"bound": "fp64", "achieved": achieved, "peak": dadd_peak, "unit": "Gop/s",
+           "frac": achieved / dadd_peak if dadd_peak else None, "traffic": None,
+           "kernel": "k_dp_level", "avg_launch_ms": dp_ms / max(1, launches),
+           "launches_per_step": launches / max(1, steps),
+           "ops_per_step": ops / steps, "f_bar": f_bar,
+           "basis": "SURVEY 8(d): (2 + 4*F_bar) fp64 ops per unpruned visit, this rank's "
+                    "calls, over this rank's k_dp_level time (CUDA events)",
+           "peak_source": "measured on this GPU: pc_measure_dadd_peak (pure DADD chains, "
+                          "full occupancy)",
+           "mix_peak": {"peak": mix_peak, "frac": achieved / mix_peak if mix_peak else None,
+                        "source": "pc_measure_fp64_peak: DADD + fp64 max + DSETP mix"},
+           "executed": {"achieved": exec_rate, "frac": exec_rate / dadd_peak if dadd_peak else None,
+                        "ops_per_step": ops_exec / steps,
+                        "note": "fp64 ops the kernel actually runs after its exact pruning"}}
+    prof = os.path.join(ROOT, "profiles", "dp_level_profile.json")
+    if os.path.exists(prof):
+        try:
+            p = json.load(open(prof))
+            out["traffic"] = p.get("dram_bytes_per_launch")
+            if "issue_slot_busy_pct" in p:
+                out["ncu"] = {k: p[k] for k in p if k != "dram_bytes_per_launch"}
+        except Exception:
+            pass
+    return out
+
+
 def run_ours(a):
-    import torch
-    import torch.distributed as dist
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-
-    from paper_2103_16063_b200 import _lib
-    from paper_2103_16063_b200.search import (device_weights, _pack, decide, enumerate_calls,
-                                              exchange, form_stage_sharded, lpt_shard,
-                                              run_calls)
+    arm = Arm()
+    import ctypes as C
+    from paper_2103_16063_b200.search import device_weights, enumerate_calls, lpt_shard
     from paper_2103_16063_b200.stages import bind_problem
     from paper_2103_16063_b200.workloads import c5_blockset, unpruned_visits
-    import ctypes as C
 
-    ctx = _lib.context(local)
+    ctx, world, rank = arm.ctx, arm.world, arm.rank
     nodes, dpn = max(1, a.D // 8), min(8, a.D)
     BS = 8 * a.D
     bs = c5_blockset(a.nb, a.D, jitter_seed=JITTER_SEED)
     nb = len(bs)
-    calls, levels = enumerate_calls(nodes, dpn, BS, nb)
+    calls, _ = enumerate_calls(nodes, dpn, BS, nb)
     unpruned = unpruned_visits(nb, calls)
     bind_problem(ctx, bs)
     owner = lpt_shard(nb, calls, world, device_weights(ctx, calls, BS) if world > 1 else None)
-    local_idx = [i for i in range(len(calls)) if owner[i] == rank]
-    my_calls = [calls[i] for i in local_idx]
-    n_levels = max(levels) + 1
-    max_stages = max(c[0] for c in calls)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    my_calls = [calls[i] for i in range(len(calls)) if owner[i] == rank]
+    dadd, mix = C.c_double(), C.c_double()
+    ctx.check(ctx.lib.pc_measure_dadd_peak(ctx.h, C.byref(dadd)), "peak")
+    ctx.check(ctx.lib.pc_measure_fp64_peak(ctx.h, C.byref(mix)), "peak")
 
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def timer():
-        ctx.check(ctx.lib.pc_timer_start(ctx.h), "timer")
-
-    def stop():
-        ms = C.c_double()
-        ctx.check(ctx.lib.pc_timer_stop(ctx.h, C.byref(ms)), "timer")
-        return ms.value
-
-    # ---- device-resident step: span tables + DP + backtrack + simulate + exchange + select
-    bind_problem(ctx, bs)
-    last = {}
-
-    def step_resident():
-        ctx.check(ctx.lib.pc_reset_cache(ctx.h), "reset")
-        flush.zero_()
-        barrier()
-        timer()
-        batch = run_calls(ctx, my_calls, BS, False, True)
-        rec, plan_w = _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels, max_stages)
-        allrec = exchange(rec, None, dev)
-        out = decide(allrec, calls, levels, owner, plan_w, None, BS)
-        ms = stop()
-        last.update(stats=batch.stats, result=out[1], stats_visits=batch.results["visits"].copy(),
-                    own_ms=ms)
-        return max_over_ranks(ms)
-
+    # ---- headline: warm-up, then K timed public-API steps
+    result = None
     for _ in range(a.warmup):
-        step_resident()
-    times = []
-    pairs = cands = dp_ms = span_ms = launches = dp_launches = 0
-    own_ms = 0.0
-    with Clocks(local) as clk:
+        result = arm.step(nodes, dpn, BS, bs)[0]
+    e2e, resident, tims = [], [], []
+    with Clocks(arm.local) as clk:
         for _ in range(a.steps):
-            times.append(step_resident())
-            own_ms += last["own_ms"]
-            st = last["stats"]
-            pairs += st.pairs
-            cands += st.candidates
-            dp_ms += st.device_ms
-            span_ms += st.span_ms
-            launches += st.kernel_launches
-            dp_launches += st.dp_launches
-    ms_per_step = sum(times) / len(times)
-    if os.environ.get("PIPECUT_BENCH_VERBOSE"):
-        print(f"[rank {rank}] own step ms {own_ms / a.steps:.1f}, max-over-ranks {ms_per_step:.1f}, "
-              f"dp {dp_ms / a.steps:.1f}, span {span_ms / a.steps:.1f}, calls {len(my_calls)}",
-              file=sys.stderr, flush=True)
-    value = unpruned / (ms_per_step / 1e3)
-    result = last["result"]
-
-    # ---- e2e: public API from host objects every step
-    e2e_times = []
-    tim = {}
-    for i in range(a.warmup + a.steps):
-        ctx.problem_owner = None            # force flatten + H2D upload
-        ctx.check(ctx.lib.pc_reset_cache(ctx.h), "reset")
-        flush.zero_()
-        barrier()
-        timer()
-        res = form_stage_sharded(nodes, dpn, BS, bs, timings=tim)
-        ms = stop()
-        if i >= a.warmup:
-            e2e_times.append(max_over_ranks(ms))
-        assert res.plan == result.plan and res.stats == result.stats
-    e2e_ms = sum(e2e_times) / len(e2e_times)
-    # schedule (i) (SURVEY.md §8e): widening levels in order, stop at the first
-    # feasible level -- the time to the same answer under the reference's order
-    lvl_times = []
-    for i in range(a.warmup + a.steps):
-        ctx.problem_owner = None
-        ctx.check(ctx.lib.pc_reset_cache(ctx.h), "reset")
-        flush.zero_()
-        barrier()
-        timer()
-        res_l = form_stage_sharded(nodes, dpn, BS, bs, speculative=False)
-        ms = stop()
-        if i >= a.warmup:
-            lvl_times.append(max_over_ranks(ms))
-        assert res_l.plan == result.plan and res_l.stats == result.stats
-    lvl_ms = sum(lvl_times) / len(lvl_times)
+            res, tim, e_ms, r_ms = arm.step(nodes, dpn, BS, bs)
+            e2e.append(e_ms)
+            resident.append(r_ms)
+            tims.append(tim)
+            if result is not None:
+                assert res.plan == result.plan and res.stats == result.stats
+            result = res
+    ms_per_step = sum(resident) / len(resident)
+    e2e_ms = sum(e2e) / len(e2e)
+    phases = {k: sum(t.get(k, 0.0) for t in tims) / len(tims) for k in PHASES}
+    rl = roofline(nb, my_calls, tims, dadd.value, mix.value, a.steps)
+    # schedule (i), SURVEY §8e: widening levels in order, stop at the first
+    # feasible one -- the reference's own order, same answer
+    lvl = []
+    for i in range(4):
+        arm.fresh()
+        arm.barrier()
+        t0 = time.perf_counter()
+        from paper_2103_16063_b200.search import form_stage_sharded
+        r_l = form_stage_sharded(nodes, dpn, BS, bs, speculative=False)
+        arm.torch.cuda.synchronize()
+        if i:
+            lvl.append(arm.max_over_ranks([(time.perf_counter() - t0) * 1e3])[0])
+        assert r_l.plan == result.plan and r_l.stats == result.stats
     plan_bytes = 0 if result.plan is None else 48 * len(result.plan.stages)
 
-    # ---- roofline of the dominant kernel (DP level kernel)
-    peak = C.c_double()
-    ctx.check(ctx.lib.pc_measure_fp64_peak(ctx.h, C.byref(peak)), "peak")
-    # Algorithmic fp64 work per SURVEY §8(d): 2 + 4*F ops per visit (2 comm
-    # adds, stages.py:232-237, then per predecessor frontier entry 2 max,
-    # stages.py:239, and 2 compares, _pareto) over the step's unpruned visits;
-    # F = mean predecessor frontier size over the feasible pairs (cands/pairs).
-    f_bar = cands / pairs if pairs else 0.0
-    # per GPU: this rank's calls over this rank's DP time (rank 0 reports)
-    local_unpruned = unpruned_visits(nb, my_calls)
-    ops = local_unpruned * a.steps * (2.0 + 4.0 * f_bar)
-    achieved = ops / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
-    # what the kernel executes after its exact pruning (corner, window, prefix skip)
-    ops_exec = 2.0 * pairs + 4.0 * cands
-    achieved_exec = ops_exec / (dp_ms / 1e3) / 1e9 if dp_ms > 0 else 0.0
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "dp_level_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-
-    if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
-
-    line = {
-        "metric": "dp_cells_per_sec", "value": value, "unit": "visits/s",
-        "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": workload_config(nb, a.D, calls, unpruned),
-        "e2e": {"value": unpruned / (e2e_ms / 1e3), "unit": "visits/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": int(tim.get("h2d_bytes", 0)),
-                "d2h_bytes_per_step": int(tim.get("d2h_bytes", 0)) + plan_bytes},
-        "gpu_launches": int(launches // max(1, a.steps)),
-        "schedules_ms": {"speculative": e2e_ms, "level_by_level": lvl_ms,
-                         "note": "public API, answer-equal; level by level stops at the first "
-                                 "feasible widening level (the reference's order), the "
-                                 "metric counts the full enumeration"},
-        "breakdown_ms": {"dp_levels": dp_ms / a.steps, "span_tables": span_ms / a.steps,
-                         "rest": ms_per_step - (dp_ms + span_ms) / a.steps},
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value,
-                     "unit": "Gop/s", "frac": achieved / peak.value if peak.value else None,
-                     "traffic": traffic,
-                     "kernel": "k_dp_level", "avg_launch_ms": dp_ms / max(1, dp_launches),
-                     "ops_per_step": ops / a.steps, "f_bar": f_bar,
-                     "scope": "rank 0: its own calls' unpruned visits over its own DP time",
-                     "basis": "SURVEY 8(d): (2 + 4*F_bar) fp64 ops per unpruned visit",
-                     "executed": {"achieved": achieved_exec,
-                                  "frac": achieved_exec / peak.value if peak.value else None,
-                                  "ops_per_step": ops_exec / a.steps,
-                                  "note": "ops the kernel actually runs after exact pruning; "
-                                          "ncu: issue-bound on frontier bookkeeping"},
-                     "peak_source": "measured on this GPU: pc_measure_fp64_peak "
-                                    "(DADD+DSETP.MAX+DSETP chains, full occupancy)"},
-        "plan": None if result.plan is None else {
-            "stages": len(result.plan.stages), "microbatches": result.plan.microbatches,
-            "replica_factor": result.plan.replica_factor, "objective": result.plan.objective,
-            "visits": result.stats.visits, "dp_calls": result.stats.dp_calls},
-        "clocks": clk.summary(),
-    }
-    if world == 1 and not a.no_cpu_baseline:
-        sampler = RefSampler(nb, a.D, calls, a.cpu_sample_sec, 1)
-        rate = sampler.rate()
-        # the reference's stock path (pruning on, its default) on the same call:
-        # its own pruned visits/s, and the time-to-solution equivalent in the
-        # metric's unit via this workload's exact unpruned/pruned ratio (the
-        # pruned count per call is the reference's, reproduced bit-exactly)
-        stock = RefSampler(nb, a.D, calls, a.cpu_sample_sec / 2, 1, unpruned=False).rate()
-        pruned_total = int(np.asarray(last["stats_visits"]).sum())
-        ratio = unpruned / pruned_total if pruned_total else None
-        line["cpu_baseline"] = {
-            "value": rate, "unit": "visits/s", "cores": 1, "kind": "reference",
-            "sample": f"reference pipecut.form_stage_dp (baseline/_ref, unmodified) on one call "
-                      f"{sampler.calls[0]} of the workload with pruning off, stopped after "
-                      f"~{a.cpu_sample_sec:.0f} s by its own visit-budget check; single thread",
-            "stock_path": {
-                "pruned_visits_per_sec": stock, "unpruned_per_pruned": ratio,
-                "equivalent_visits_per_sec": stock * ratio if ratio else None,
-                "note": "reference default options (pruning on), same call, "
-                        f"~{a.cpu_sample_sec / 2:.0f} s; equivalent = pruned rate x the "
-                        "workload's unpruned/pruned visit ratio. Bounded samples start at "
-                        "level 1, where a cell costs O(1) but counts up to b*d visits, so "
-                        "sampled CPU rates favour the reference"}}
-    if not a.no_latency and world == 1:
-        line["latency_ms"] = config_latencies(ctx)
-    print(json.dumps(line), flush=True)
+    line = None
+    if rank == 0:
+        line = {
+            "metric": "dp_cells_per_sec", "value": unpruned / (ms_per_step / 1e3),
+            "unit": "visits/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(nb, a.D),
+            "e2e": {"value": unpruned / (e2e_ms / 1e3), "unit": "visits/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(tims[-1].get("h2d_bytes", 0)),
+                    "d2h_bytes_per_step": int(tims[-1].get("d2h_bytes", 0)) + plan_bytes,
+                    "note": "same timed steps: wall time of the public form_stage_sharded() "
+                            "call from the host BlockSet (flatten, upload, search, result "
+                            "objects), max over ranks"},
+            "gpu_launches": int(tims[-1].get("kernel_launches", 0)),
+            "breakdown_ms": dict(phases, resident=ms_per_step, e2e=e2e_ms,
+                                 note="rank 0 means over the timed steps; span/dp/post are "
+                                      "device (CUDA events): K1/K2 tables, K3 level kernels, "
+                                      "then K7 visits + K4 backtrack + stage records + K5 "
+                                      "simulate + D2H; run_calls is their host wall time"),
+            "schedules_ms": {"speculative": e2e_ms,
+                             "level_by_level": sorted(lvl)[len(lvl) // 2],
+                             "note": "public API, answer-equal; level by level stops at the "
+                                     "first feasible widening level (the reference's order), "
+                                     "the metric counts the full enumeration"},
+            "roofline": rl,
+            "plan": None if result.plan is None else {
+                "stages": len(result.plan.stages), "microbatches": result.plan.microbatches,
+                "replica_factor": result.plan.replica_factor,
+                "objective": result.plan.objective.hex(), "visits": result.stats.visits,
+                "dp_calls": result.stats.dp_calls},
+            "clocks": clk.summary(),
+        }
+    if world == 1:
+        if not a.no_sweep:
+            line["sweep"] = sweep(arm, dadd.value, (a.nb, a.D), line)
+        if not a.no_latency:
+            line["latency_ms"] = config_latencies(arm)
+        if not a.no_cpu_baseline:
+            ref = ref_subprocess("sample", "--nb", str(a.nb), "--D", str(a.D), "--cores", "1",
+                                 "--budget", str(a.ref_budget), "--seed", str(JITTER_SEED))
+            line["cpu_baseline"] = {
+                "value": ref.get("value"), "unit": "visits/s", "cores": 1, "kind": "reference",
+                "sample": f"reference pipecut.form_stage_dp (baseline/_ref, unmodified, "
+                          f"baseline/ref_arm.py in a fresh interpreter) on one call "
+                          f"{ref.get('calls')} of the workload with pruning off, stopped by "
+                          f"its own visit-budget check after exactly {a.ref_budget} visits; "
+                          f"single thread; level-1 prefix, favours the reference",
+                "seconds": ref.get("seconds")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+        arm.dist.barrier()
+        arm.dist.destroy_process_group()
 
 
-def config_latencies(ctx):
+def sweep(arm, dadd_peak, headline, line):
+    """BASELINE configs[4]: every (nb, D) point once at N = 1 through the
+    public API (one warm-up, one timed step; the headline point reuses the
+    headline's timed steps)."""
+    from paper_2103_16063_b200.search import enumerate_calls
+    from paper_2103_16063_b200.workloads import c5_blockset, unpruned_visits
+    out = []
+    for nb in SWEEP_NB:
+        for D in SWEEP_D:
+            if (nb, D) == headline:
+                out.append({"nb": nb, "D": D, "steps": line["steps"], "from": "headline",
+                            "visits_per_sec": line["value"], "e2e_visits_per_sec": line["e2e"]["value"],
+                            "ms": line["ms_per_step"], "dp_ms": line["breakdown_ms"]["dp_ms"],
+                            "roofline_frac": line["roofline"]["frac"], "clocks": line["clocks"]})
+                continue
+            nodes, dpn = max(1, D // 8), min(8, D)
+            bs = c5_blockset(nb, D, jitter_seed=JITTER_SEED)
+            calls, _ = enumerate_calls(nodes, dpn, 8 * D, nb)
+            unpruned = unpruned_visits(nb, calls)
+            arm.step(nodes, dpn, 8 * D, bs)
+            with Clocks(arm.local) as clk:
+                res, tim, e_ms, r_ms = arm.step(nodes, dpn, 8 * D, bs)
+            rl = roofline(nb, calls, [tim], dadd_peak, 0.0, 1)
+            out.append({"nb": nb, "D": D, "steps": 1, "warmup": 1, "calls": len(calls),
+                        "unpruned_visits": unpruned,
+                        "visits_per_sec": unpruned / (r_ms / 1e3),
+                        "e2e_visits_per_sec": unpruned / (e_ms / 1e3), "ms": r_ms,
+                        "dp_ms": tim["dp_ms"], "roofline_frac": rl["frac"],
+                        "f_bar": rl["f_bar"],
+                        "objective": None if res.plan is None else res.plan.objective.hex(),
+                        "clocks": clk.summary()})
+    return out
+
+
+def config_latencies(arm):
     """Reference-semantics partition search on C1-C4 through the public API:
-    partition_blocks + form_stage (median of 5 warm runs + 1 cold), beside the
-    headline; the reference's own times for the same calls are in
-    tests/golden/configs.json (ref_seconds, measured in the build container)."""
-    from paper_2103_16063_b200 import form_stage, partition_blocks
+    partition_blocks + form_stage, median of 5 warm runs + 1 cold, with the
+    phase split, beside the reference's own times measured in this run
+    (baseline/ref_arm.py configs, one process per config)."""
     from paper_2103_16063_b200 import flatten as _flat
+    from paper_2103_16063_b200 import form_stage, partition_blocks
     from paper_2103_16063_b200.workloads import config_partition
+    ctx = arm.ctx
+    ref = ref_subprocess("configs", timeout=1200)
     out = {}
     for name in ("C1", "C2", "C3", "C4"):
         part, model, k, batch, cl = config_partition(name)
-        tb, ts = [], []
+        tb, ts, pb_t, fs_t = [], [], [], []
         for i in range(6):
             _flat._ATOM_CACHE.clear()
             ctx.problem_owner = None
             ctx.lib.pc_reset_cache(ctx.h)
-            gc.collect()          # the CPU-baseline sampler leaves large garbage behind
+            gc.collect()
+            t_pb, t_fs = {}, {}
             t0 = time.perf_counter()
-            bs = partition_blocks(part, model, k)
+            bs = partition_blocks(part, model, k, timings=t_pb)
             t1 = time.perf_counter()
-            res = form_stage(cl.num_nodes, cl.devices_per_node, batch, bs)
+            res = form_stage(cl.num_nodes, cl.devices_per_node, batch, bs, last_stats=t_fs)
             t2 = time.perf_counter()
             tb.append((t1 - t0) * 1e3)
             ts.append((t2 - t1) * 1e3)
+            pb_t.append(t_pb)
+            fs_t.append(t_fs)
         med = lambda v: sorted(v[1:])[len(v[1:]) // 2]
-        out[name] = {"partition_blocks_ms": med(tb), "form_stage_ms": med(ts),
-                     "total_ms": med([a + b for a, b in zip(tb, ts)]),
-                     "cold_total_ms": tb[0] + ts[0],
-                     "visits": res.stats.visits, "dp_calls": res.stats.dp_calls,
-                     "objective": None if res.plan is None else res.plan.objective}
+        mean = lambda ds, k: sum(d.get(k, 0.0) for d in ds[1:]) / len(ds[1:])
+        r = ref.get(name, {}) if isinstance(ref, dict) else {}
+        entry = {"partition_blocks_ms": med(tb), "form_stage_ms": med(ts),
+                 "total_ms": med([x + y for x, y in zip(tb, ts)]),
+                 "cold_total_ms": tb[0] + ts[0],
+                 "phases_ms": {
+                     "partition_blocks": {k: mean(pb_t, k) for k in
+                                          ("flatten_ms", "library_ms", "build_ms")},
+                     "form_stage": {k: mean(fs_t, k) for k in
+                                    ("flatten_ms", "upload_ms", "library_ms", "span_ms",
+                                     "device_ms", "post_ms")}},
+                 "visits": res.stats.visits, "dp_calls": res.stats.dp_calls,
+                 "objective": None if res.plan is None else res.plan.objective.hex()}
+        if r:
+            entry["ref_ms"] = {k: r[k] for k in ("partition_blocks_ms", "form_stage_ms",
+                                                 "total_ms")}
+            entry["ref_same_answer"] = (r["objective"] == entry["objective"]
+                                        and r["visits"] == entry["visits"]
+                                        and r["dp_calls"] == entry["dp_calls"])
+            entry["speedup"] = r["total_ms"] / entry["total_ms"]
+        elif isinstance(ref, dict) and "error" in ref:
+            entry["ref_ms"] = {"error": ref["error"]}
+        out[name] = entry
+    out["note"] = ("phases: partition_blocks = host atom flattening / library (device "
+                   "coarsening + refinement + block profiles) / reference objects; form_stage "
+                   "= flatten / upload / pc_form_stage wall (span, device = DP levels, post = "
+                   "visits + backtrack + records + simulate, all CUDA events); ref_ms: the "
+                   "unmodified reference in this run, one process per config")
     return out
 
 

@@ -169,6 +169,8 @@ typedef struct pc_stats {
     int64_t kernel_launches;    /* all library kernel launches of the call */
     double  device_ms;          /* device time of the DP level kernels (CUDA events) */
     double  span_ms;            /* device time of span/cut table kernels */
+    double  post_ms;            /* device time after the DP levels: visit counts, backtrack,
+                                   stage records, simulate and the result copies (CUDA events) */
 } pc_stats;
 
 /* Per-call result of pc_run_calls (one record per pc_call). */
@@ -288,6 +290,10 @@ int pc_timer_stop(pc_ctx *ctx, double *ms);
 /* Measured fp64 add/max issue rate of this device (Gop/s), the roofline
  * denominator of the DP kernel (no tensor-core roof: min/max/add recurrence). */
 int pc_measure_fp64_peak(pc_ctx *ctx, double *gops);
+
+/* Measured pure-DADD rate of this device (Gop/s): the fp64 pipe's peak op rate,
+ * the denominator of the DP kernel's algorithmic-fp64 roofline. */
+int pc_measure_dadd_peak(pc_ctx *ctx, double *gops);
 
 #ifdef __cplusplus
 }

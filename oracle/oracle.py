@@ -43,6 +43,8 @@ def load():
                                         C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_int64)]
         lib.orc_span_record.restype = None
+        lib.orc_span_record_row.argtypes = lib.orc_span_record.argtypes
+        lib.orc_span_record_row.restype = None
         lib.orc_cut_time.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64]
         lib.orc_cut_time.restype = C.c_double
         lib.orc_form_stage_dp.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int,
@@ -70,6 +72,13 @@ class OracleProblem:
         tf, tb, mem = C.c_double(), C.c_double(), C.c_int64()
         load().orc_span_record(self.ref, lo, hi, m, int(ckpt),
                                C.byref(tf), C.byref(tb), C.byref(mem))
+        return tf.value, tb.value, mem.value
+
+    def span_row(self, lo, hi, m, ckpt):
+        """The memo-row path (monotone graphs only) of the same record."""
+        tf, tb, mem = C.c_double(), C.c_double(), C.c_int64()
+        load().orc_span_record_row(self.ref, lo, hi, m, int(ckpt),
+                                   C.byref(tf), C.byref(tb), C.byref(mem))
         return tf.value, tb.value, mem.value
 
     def cut_time(self, cut, m, cum):

@@ -96,14 +96,43 @@ void orc_frontier_hist(int64_t *out)
     for (int i = 0; i < 65; ++i) { out[i] = g_fhist[i]; g_fhist[i] = 0; }
 }
 
-static int cmp_entry(const void *a, const void *b)
+/* sorted(range(n), key=(tf, tb, i)) of _pareto (stages.py:177): a stable
+ * bottom-up merge sort on (tf, tb); stability keeps insertion order (ord) on
+ * equal (tf, tb), so the order equals qsort with cmp_entry. */
+static inline int entry_less(const orc_entry *x, const orc_entry *y)
 {
-    const orc_entry *x = (const orc_entry *)a, *y = (const orc_entry *)b;
-    if (x->tf < y->tf) return -1;
-    if (x->tf > y->tf) return 1;
-    if (x->tb < y->tb) return -1;
-    if (x->tb > y->tb) return 1;
-    return (x->ord > y->ord) - (x->ord < y->ord);
+    return x->tf < y->tf || (x->tf == y->tf && x->tb < y->tb);
+}
+
+static void sort_cands(orc_entry *a, size_t n, orc_entry **tmp, size_t *tmp_cap)
+{
+    if (*tmp_cap < n) {
+        *tmp_cap = n;
+        *tmp = (orc_entry *)realloc(*tmp, n * sizeof(orc_entry));
+    }
+    /* insertion sort runs of 16, then merge passes */
+    const size_t RUN = 16;
+    for (size_t lo = 0; lo < n; lo += RUN) {
+        size_t hi = lo + RUN < n ? lo + RUN : n;
+        for (size_t i = lo + 1; i < hi; ++i) {
+            orc_entry v = a[i];
+            size_t j = i;
+            while (j > lo && entry_less(&v, &a[j - 1])) { a[j] = a[j - 1]; --j; }
+            a[j] = v;
+        }
+    }
+    orc_entry *src = a, *dst = *tmp;
+    for (size_t w = RUN; w < n; w *= 2) {
+        for (size_t lo = 0; lo < n; lo += 2 * w) {
+            size_t mid = lo + w < n ? lo + w : n, hi = lo + 2 * w < n ? lo + 2 * w : n;
+            size_t i = lo, j = mid, k = lo;
+            while (i < mid && j < hi) dst[k++] = entry_less(&src[j], &src[i]) ? src[j++] : src[i++];
+            while (i < mid) dst[k++] = src[i++];
+            while (j < hi) dst[k++] = src[j++];
+        }
+        orc_entry *t = src; src = dst; dst = t;
+    }
+    if (src != a) memcpy(a, src, n * sizeof(orc_entry));
 }
 
 typedef struct {
@@ -120,6 +149,73 @@ typedef struct {
     orc_rec *memo[64];          /* [nb+1][nb+1] per key */
 } orc_prof;
 
+/* One memo row: every hi > lo of span [lo, hi) at share m in one pass.  Only
+ * for monotone task_block (non-decreasing along the sorted task list, the C5
+ * chains): the tasks of [lo, hi+1) are then those of [lo, hi) followed by the
+ * tasks of block hi, so continuing the fold of t_fwd / t_bwd over hi performs
+ * exactly the additions of orc_span_record's fold (costs.py:137-140); the
+ * byte sums are integers (order-free) and the footprint is a running max
+ * (costs.py:150-155).  Pinned against orc_span_record and CostModel.profile
+ * by tests/test_oracle.py. */
+static void span_row(const pc_problem *p, int lo, int64_t m, int ckpt, orc_rec *row)
+{
+    int nb = p->nb;
+    int64_t *in_add = (int64_t *)calloc((size_t)nb + 2, sizeof(int64_t));
+    /* inputs: v counts in [lo, hi) iff in_ob[v] < lo and its first consumer
+     * block c >= lo has c < hi, i.e. for every hi > c */
+    for (int v = 0; v < p->n_in; ++v) {
+        if (p->in_ob[v] >= lo) continue;
+        for (int k = p->in_cons_off[v]; k < p->in_cons_off[v + 1]; ++k) {
+            int c = p->in_cons[k];
+            if (c >= lo) {
+                in_add[c + 1] += p->in_fix[v] + m * p->in_ps[v];
+                break;
+            }
+        }
+    }
+    double factor = (1.0 + p->grad_factor) + p->opt_factor;
+    double tf = 0.0, tb = 0.0;
+    int64_t param = 0, res = 0, inb = 0, maxfp = 0;
+    int t = 0;
+    while (t < p->n_tasks && p->task_block[t] < lo) ++t;
+    for (int hi = lo + 1; hi <= nb; ++hi) {
+        int b = hi - 1;                       /* block joining the span */
+        for (; t < p->n_tasks && p->task_block[t] == b; ++t) {
+            double x = (p->task_flops[t] * (double)m) / p->flops_per_sec;
+            double y = p->bwd_fwd_ratio * x;
+            tf = tf + x;
+            tb = tb + y;
+            int64_t fp = p->task_fp_fix[t] + m * p->task_fp_ps[t];
+            for (int k = p->task_dep_off[t]; k < p->task_dep_off[t + 1]; ++k)
+                if (p->dep_ob[k] >= lo) fp += p->dep_fix[k] + m * p->dep_ps[k];
+            if (fp > maxfp) maxfp = fp;
+        }
+        param += p->blk_param[b];
+        res += p->blk_res_fix[b] + m * p->blk_res_ps[b];
+        inb += in_add[hi];
+        int64_t act = inb + (ckpt ? maxfp : res);
+        double memd = (double)param * factor + (double)act;
+        orc_rec *r = &row[hi];
+        r->tf = tf;
+        r->tb = tb;
+        r->mem = (int64_t)memd;
+        r->filled = 1;
+    }
+    free(in_add);
+}
+
+/* The memo row path above, exposed for the pinning test. */
+void orc_span_record_row(const pc_problem *p, int lo, int hi, int64_t m, int ckpt,
+                         double *tf_out, double *tb_out, int64_t *mem_out)
+{
+    orc_rec *row = (orc_rec *)calloc((size_t)p->nb + 1, sizeof(orc_rec));
+    span_row(p, lo, m, ckpt, row);
+    *tf_out = row[hi].tf;
+    *tb_out = row[hi].tb;
+    *mem_out = row[hi].mem;
+    free(row);
+}
+
 static const orc_rec *prof_record(orc_prof *pf, int lo, int hi, int64_t m)
 {
     int k;
@@ -133,7 +229,10 @@ static const orc_rec *prof_record(orc_prof *pf, int lo, int hi, int64_t m)
     }
     orc_rec *r = &pf->memo[k][(size_t)lo * (pf->p->nb + 1) + hi];
     if (!r->filled) {
-        orc_span_record(pf->p, lo, hi, m, pf->ckpt, &r->tf, &r->tb, &r->mem);
+        if (pf->p->monotone)
+            span_row(pf->p, lo, m, pf->ckpt, &pf->memo[k][(size_t)lo * (pf->p->nb + 1)]);
+        else
+            orc_span_record(pf->p, lo, hi, m, pf->ckpt, &r->tf, &r->tb, &r->mem);
         r->filled = 1;
     }
     return r;
@@ -237,6 +336,8 @@ int orc_run_dp(const pc_problem *p, orc_prof *pf, int S, int D, int64_t BS, int 
     lv[0][0].e[0].bp = lv[0][0].e[0].dp = lv[0][0].e[0].idx = -1;
     size_t cap = 1024;
     orc_entry *cands = (orc_entry *)malloc(cap * sizeof(orc_entry));
+    orc_entry *tmp = NULL;
+    size_t tmp_cap = 0;
     int rc = PC_OK;
     int d_min = 1;
     for (int s = 1; s <= S && rc == PC_OK; ++s) {
@@ -249,9 +350,12 @@ int orc_run_dp(const pc_problem *p, orc_prof *pf, int S, int D, int64_t BS, int 
                 if (budget >= 0 && *visits > budget) { rc = PC_ERR_BUDGET; break; }
                 size_t nc = 0;
                 int saw_zero = 0;
-                /* prev cells in sorted (bp, dp) order */
-                for (int bp = 0; bp < b; ++bp) {
-                    for (int dp = 0; dp < d; ++dp) {
+                /* prev cells in sorted (bp, dp) order (stages.py:220); level
+                 * s-1 holds cells only at bp in [s-1, nb-S+s-1], dp in
+                 * [s-1, D-S+s-1], so the scan starts and ends there */
+                int dp_end = d < D - S + s ? d : D - S + s;
+                for (int bp = s - 1; bp < b; ++bp) {
+                    for (int dp = s - 1; dp < dp_end; ++dp) {
                         orc_cell *pc = &prev[(size_t)bp * (D + 1) + dp];
                         if (pc->n == 0) continue;
                         int64_t dev = d - dp;
@@ -278,7 +382,7 @@ int orc_run_dp(const pc_problem *p, orc_prof *pf, int S, int D, int64_t BS, int 
                     }
                 }
                 if (nc) {
-                    qsort(cands, nc, sizeof(orc_entry), cmp_entry);   /* _pareto */
+                    sort_cands(cands, nc, &tmp, &tmp_cap);          /* _pareto */
                     orc_cell *cc = &cur[(size_t)b * (D + 1) + d];
                     cc->e = (orc_entry *)malloc(nc * sizeof(orc_entry));
                     double best = INFINITY;
@@ -288,6 +392,7 @@ int orc_run_dp(const pc_problem *p, orc_prof *pf, int S, int D, int64_t BS, int 
                             best = cands[i].tb;
                         }
                     }
+                    cc->e = (orc_entry *)realloc(cc->e, (size_t)cc->n * sizeof(orc_entry));
                     g_fhist[cc->n < 64 ? cc->n : 64]++;
                 } else if (!disable_pruning && !saw_zero) {   /* :242-249 */
                     if (s == 1) d_min = d + 1;
@@ -297,6 +402,7 @@ int orc_run_dp(const pc_problem *p, orc_prof *pf, int S, int D, int64_t BS, int 
         }
     }
     free(cands);
+    free(tmp);
     out->n_stages = 0;
     out->objective = NAN;
     out->iteration_time = NAN;

@@ -131,6 +131,7 @@ class PcStats(C.Structure):
         ("kernel_launches", C.c_int64),
         ("device_ms", C.c_double),
         ("span_ms", C.c_double),
+        ("post_ms", C.c_double),
     ]
 
 

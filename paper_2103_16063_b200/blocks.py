@@ -11,6 +11,7 @@ predicates and all profiles run on the GPU (csrc/blocks.cu).
 from __future__ import annotations
 
 import ctypes as C
+import time
 
 import numpy as np
 
@@ -25,11 +26,15 @@ CostRecord = _pc.costs.CostRecord
 
 
 @_lib.serialized
-def partition_blocks(partition, model, k: int = 32):
-    """Group atoms into at most k convex, memory-feasible blocks (GPU)."""
+def partition_blocks(partition, model, k: int = 32, *, timings: dict | None = None):
+    """Group atoms into at most k convex, memory-feasible blocks (GPU).
+    ``timings`` (optional) gets the host flatten, library call (coarsening,
+    refinement, block profiles) and object-build times in ms."""
     if k < 1:
         raise ValueError("k must be at least 1")
+    t0 = time.perf_counter()
     fa = flatten_atoms(partition, model)
+    t1 = time.perf_counter()
     ctx = _lib.context()
     st = abi.atoms_struct(fa)
     n = fa.n
@@ -49,11 +54,16 @@ def partition_blocks(partition, model, k: int = 32):
     if rc == abi.PC_ERR_STUCK:
         raise CompactionStuck(int(err[0]), k)
     ctx.check(rc, "partition_blocks")
+    t2 = time.perf_counter()
     nb = int(nbk.value)
     glist = tuple(tuple(int(x) for x in at[off[b]:off[b + 1]]) for b in range(nb))
     width = max(3, len(str(nb)))
     blocks = tuple(partition.merged(grp, f"B{idx:0{width}d}") for idx, grp in enumerate(glist))
     costs = tuple(CostRecord(t_fwd_sec=float(tf[b]), t_bwd_sec=float(tb[b]), mem_bytes=int(mem[b]))
                   for b in range(nb))
-    return BlockSet(partition=partition, model=model, block_atoms=glist, blocks=blocks,
-                    costs=costs)
+    out = BlockSet(partition=partition, model=model, block_atoms=glist, blocks=blocks,
+                   costs=costs)
+    if timings is not None:
+        timings.update(flatten_ms=(t1 - t0) * 1e3, library_ms=(t2 - t1) * 1e3,
+                       build_ms=(time.perf_counter() - t2) * 1e3)
+    return out

@@ -36,6 +36,7 @@ extern "C" int pc_ctx_create(int device, pc_ctx **out) {
     cudaEventCreate(&ctx->ev0);
     cudaEventCreate(&ctx->ev1);
     cudaEventCreate(&ctx->ev2);
+    cudaEventCreate(&ctx->ev3);
     cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     int major = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
@@ -63,6 +64,7 @@ extern "C" void pc_ctx_destroy(pc_ctx *ctx) {
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->ev2) cudaEventDestroy(ctx->ev2);
+    if (ctx->ev3) cudaEventDestroy(ctx->ev3);
     if (ctx->t0) cudaEventDestroy(ctx->t0);
     if (ctx->t1) cudaEventDestroy(ctx->t1);
     if (ctx->st) cudaStreamDestroy(ctx->st);
@@ -206,9 +208,14 @@ extern "C" int pc_set_problem(pc_ctx *ctx, const pc_problem *p) {
         // span times are folds of (f*m)/F: non-negative terms make them monotone
         // in the span, which the DP's prefix skip relies on
         bool nonneg = p->flops_per_sec > 0 && p->bwd_fwd_ratio >= 0;
-        for (int t = 0; t < T && nonneg; ++t) nonneg = p->task_flops[t] >= 0.0;
+        for (int t = 0; t < T; ++t) {
+            if (std::isnan(p->task_flops[t]))   // NaN is the infeasible-span marker (span_mark)
+                return fail(ctx, PC_ERR_INVALID, "NaN flops_per_sample is not supported");
+            nonneg = nonneg && p->task_flops[t] >= 0.0;
+        }
         ctx->mono_flops = nonneg;
         ctx->mono_skip = nonneg;
+        D.nonneg = nonneg ? 1 : 0;
     }
     ctx->has_cost_table = p->has_cost_table != 0;
     ctx->ov_m.clear();
@@ -322,7 +329,7 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
                               ctx->mismatch_d.as<int>(), ctx->st);
         ctx->launches++;
         if (int rc = check_launch(ctx, "span_dp_tables")) return rc;
-        launch_first_feasible(P.nb, nf, d_pf, d_pff, ctx->st);
+        launch_first_feasible(P.nb, nf, P.nonneg, d_pf, d_pff, ctx->st);
         ctx->launches++;
         if (int rc = check_launch(ctx, "first_feasible")) return rc;
         int mism = 0;
@@ -386,6 +393,12 @@ static int validate_call(pc_ctx *ctx, const pc_call &c, int64_t BS) {
 }
 
 static inline int64_t tri_sum(int64_t n) { return n * (n + 1) / 2; }
+
+// largest pool offset (entries) a 31-bit frontier offset can hold
+constexpr int64_t OFF_MAX = (int64_t)SPILL_BIT - 1;
+// history cells per chunk: the shared history spill pool is sized from them
+// (one entry per cell at first) and must stay within OFF_MAX
+constexpr int64_t CHUNK_HIST_CELLS = int64_t(1) << 30;
 
 // Runs one batch of DP calls whose buffers fit; fills outs[orig] for each.
 static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::vector<int> &idx,
@@ -469,11 +482,14 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             col_total += cds[i].B;
             col_prefix[i + 1] = col_total;
             const int64_t cells = (int64_t)cds[i].A * cds[i].B;
+            // pool offsets are stored in 31 bits (bit 31 = SPILL_BIT): every
+            // region and spill pool is capped below 2^31 entries; a cell that
+            // does not fit raises the overflow flag (never a wrapped offset)
             cds[i].vpool_base = vpool_total;
-            cds[i].vpool_cap = cells * vcap + 64;
+            cds[i].vpool_cap = std::min<int64_t>(cells * vcap + 64, OFF_MAX);
             vpool_total += cds[i].vpool_cap;
             cds[i].hpool_base = hpool_total;
-            cds[i].hpool_cap = cells * cds[i].S * hcap + 64;
+            cds[i].hpool_cap = std::min<int64_t>(cells * cds[i].S * hcap + 64, OFF_MAX);
             hpool_total += cds[i].hpool_cap;
         }
         CUDA_TRY(ctx, cudaMemcpyAsync(ctx->calls_d.p, cds.data(), sizeof(CallDesc) * n, cudaMemcpyHostToDevice, ctx->st));
@@ -483,8 +499,8 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         const size_t hmeta = ((size_t)hist_cells * 5 + a256) & ~a256;
         // shared spill pools for calls whose frontiers outgrow their region:
         // values 4 entries per cell of the batch, history 1 per cell
-        const int64_t vspill = std::max<int64_t>(1 << 20, 4 * val_cells) * vcap / 8;
-        const int64_t hspill = std::max<int64_t>(1 << 22, hist_cells) * hcap / 4;
+        const int64_t vspill = std::min<int64_t>(std::max<int64_t>(1 << 20, 4 * val_cells) * vcap / 8, OFF_MAX);
+        const int64_t hspill = std::min<int64_t>(std::max<int64_t>(1 << 22, hist_cells) * hcap / 4, OFF_MAX);
         const size_t vsp = ((size_t)vspill * 16 + a256) & ~a256;
         CUDA_TRY(ctx, ctx->val_d.ensure(2 * (vmeta + vpool + vsp) + 256));
         CUDA_TRY(ctx, ctx->hist_d.ensure(hmeta + 4 * (size_t)(hpool_total + hspill) + 512));
@@ -626,7 +642,11 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         ctx->last_dp_launches += launches;
         if (ovf & 1) return fail(ctx, PC_ERR_CAPACITY, "a Pareto frontier exceeded 64 entries");
         if (!ovf) break;
-        // a pool region ran out: grow and rerun the batch
+        // a pool region ran out: grow and rerun the batch.  With FMAX entries
+        // reserved per cell every frontier fits its region unless the 31-bit
+        // offset cap clipped it: then the batch is beyond the offset range.
+        if (vcap >= FMAX && hcap >= FMAX)
+            return fail(ctx, PC_ERR_CAPACITY, "frontier pools beyond the 31-bit offset range");
         vcap *= 2;
         hcap *= 2;
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->st));
@@ -756,6 +776,15 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
     }
 
+    // everything after the DP levels (ev2: end of the last DP pass)
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev3, ctx->st));
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev3));
+    {
+        float pms = 0;
+        cudaEventElapsedTime(&pms, ctx->ev2, ctx->ev3);
+        ctx->last_post_ms += pms;
+    }
+
     // ---- fill outputs
     std::vector<int> fpos(calls.size(), -1);
     for (int pi = 0; pi < np; ++pi) fpos[feas_orig[pi]] = pi;
@@ -803,6 +832,7 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     outs.assign(calls.size(), CallOut());
     ctx->last_dp_ms = 0;
     ctx->last_span_ms = 0;
+    ctx->last_post_ms = 0;
     ctx->last_dp_launches = 0;
     ctx->last_pairs = 0;
     ctx->last_cands = 0;
@@ -813,19 +843,23 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     const size_t cap = free_b / 2;
     std::vector<int> cur;
     size_t cur_bytes = 0;
+    int64_t cur_hist = 0;
     *n_chunks = 0;
     for (size_t i = 0; i < calls.size(); ++i) {
         const pc_call &c = calls[i];
         const int64_t A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
         const size_t bytes = (size_t)A * B * (2 * (5 + 16 * 12) + (size_t)c.S * (5 + 4 * 5));
-        if (!cur.empty() && cur_bytes + bytes > cap) {
+        const int64_t hist = A * B * c.S;
+        if (!cur.empty() && (cur_bytes + bytes > cap || cur_hist + hist > CHUNK_HIST_CELLS)) {
             if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
             ++*n_chunks;
             cur.clear();
             cur_bytes = 0;
+            cur_hist = 0;
         }
         cur.push_back((int)i);
         cur_bytes += bytes;
+        cur_hist += hist;
     }
     if (!cur.empty()) {
         if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
@@ -898,6 +932,7 @@ static void fill_stats(pc_ctx *ctx, pc_stats *stats, int64_t visits, int64_t cal
     stats->kernel_launches = ctx->launches;
     stats->device_ms = ctx->last_dp_ms;
     stats->span_ms = ctx->last_span_ms;
+    stats->post_ms = ctx->last_post_ms;
 }
 
 // =========================================================================== entry points
@@ -1047,7 +1082,7 @@ extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, in
         }
     }
     running = calls_counted = unpruned = cells = 0;
-    double dp_ms = 0, span_ms = 0;
+    double dp_ms = 0, span_ms = 0, post_ms = 0;
     int64_t pairs = 0, cands = 0, launches = 0;
     // batches of widening levels: one per level (0), or the first level and then
     // all the others together (2: the first level is usually feasible)
@@ -1071,11 +1106,13 @@ extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, in
         if (int rc = run_calls_impl(ctx, sub, BS, !disable_pruning, 1, outs, &chunks)) return rc;
         dp_ms += ctx->last_dp_ms;
         span_ms += ctx->last_span_ms;
+        post_ms += ctx->last_post_ms;
         pairs += ctx->last_pairs;
         cands += ctx->last_cands;
         launches += ctx->last_dp_launches;
         ctx->last_dp_ms = dp_ms;
         ctx->last_span_ms = span_ms;
+        ctx->last_post_ms = post_ms;
         ctx->last_pairs = pairs;
         ctx->last_cands = cands;
         ctx->last_dp_launches = launches;
@@ -1197,6 +1234,7 @@ extern "C" int pc_brute_force(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_s
     a.kcols = kcols;
     a.nb = nb; a.S = S; a.D = D;
     a.derived = ctx->derived ? 1 : 0;
+    a.nonneg = ctx->P.nonneg;
     a.num_nodes = P.num_nodes; a.dpn = P.dpn;
     a.beta = P.beta;
     a.n_comb = n_comb; a.n_comp = n_comp; a.n_chunks = n_chunks;
@@ -1480,6 +1518,13 @@ extern "C" int pc_timer_stop(pc_ctx *ctx, double *ms) {
     return PC_OK;
 }
 
+extern "C" int pc_measure_dadd_peak(pc_ctx *ctx, double *gops) {
+    cudaSetDevice(ctx->device);
+    *gops = measure_dadd_gops(ctx->st, ctx->sm_count);
+    if (*gops <= 0) return fail(ctx, PC_ERR_CUDA, "DADD peak kernel failed");
+    return PC_OK;
+}
+
 extern "C" int pc_measure_fp64_peak(pc_ctx *ctx, double *gops) {
     cudaSetDevice(ctx->device);
     *gops = measure_fp64_gops(ctx->st, ctx->sm_count);
@@ -1502,6 +1547,8 @@ extern "C" int pc_set_overrides(pc_ctx *ctx, int32_t n_m, const int64_t *m_value
         for (int t = 0; t < T; ++t) {
             const size_t q = (size_t)i * T + t;
             if (!has[q]) continue;
+            if (std::isnan(tf[q]))              // NaN is the infeasible-span marker (span_mark)
+                return fail(ctx, PC_ERR_INVALID, "NaN t_fwd in a cost-table entry is not supported");
             if (!(tf[q] >= 0.0) || (!std::isnan(tb[q]) && !(tb[q] >= 0.0))) nonneg = false;
             if (act[q] >= 0)
                 c[ctx->h_task_block[t] + 1] += act[q] - (ctx->h_prod_fix[t] + m_values[i] * ctx->h_prod_ps[t]);
@@ -1509,6 +1556,7 @@ extern "C" int pc_set_overrides(pc_ctx *ctx, int32_t n_m, const int64_t *m_value
         for (int b = 0; b < nb; ++b) c[b + 1] += c[b];
     }
     ctx->mono_skip = nonneg;
+    ctx->P.nonneg = nonneg ? 1 : 0;      // free_keys above: tables are rebuilt in this encoding
     const size_t KT = (size_t)n_m * T;
     const size_t bytes = 8 * (size_t)n_m + KT + 8 * KT * 3 + 8 * corr.size() + 256;
     CUDA_TRY(ctx, ctx->ov_d.ensure(bytes));

@@ -7,9 +7,12 @@
 // Node index = position in g.nodes, which TaskGraph builds in ascending id
 // order (graph.py:90-93), so index order is the reference's string order
 // (checked on entry; UTF-8 byte order equals code-point order).  Every error
-// the reference raises (no non-constant task, dangling outputs or constants,
-// clone-id collisions, cycles) and any unexpected shape raise Fallback: the
-// caller then runs the reference function, which raises its own error.
+// the reference raises is raised here, first one first in the reference's
+// order, with its class and message: CycleError (graph.py:170-172),
+// NoNonConstantTask and DanglingOutput (atoms.py:179-198), the clone-id
+// collision ValueError (atoms.py:209-210).  A TaskGraph whose internal layout
+// is not the reference's (non-str ids, unsorted node dict, adjacency that is
+// not id-sorted tuples) raises TypeError: there is no fallback path.
 #include <pybind11/pybind11.h>
 
 #include <algorithm>
@@ -26,17 +29,34 @@ namespace py = pybind11;
 
 namespace {
 
-struct Fallback {};
-
 inline void check(PyObject *o) {
     if (!o) throw py::error_already_set();
+}
+
+// the reference's exception classes (set by build() from its arguments)
+struct RefErrors {
+    PyObject *cycle = nullptr, *no_task = nullptr, *dangling = nullptr;
+};
+RefErrors g_err;
+
+[[noreturn]] void raise_obj(PyObject *cls, PyObject *msg) {
+    check(msg);
+    PyErr_SetObject(cls, msg);
+    Py_DECREF(msg);
+    throw py::error_already_set();
+}
+// a TaskGraph not laid out like the reference's (graph.py:82-116)
+[[noreturn]] void layout(const char *what) {
+    PyErr_Format(PyExc_TypeError, "build_atomic_subcomponents: unsupported TaskGraph layout (%s)",
+                 what);
+    throw py::error_already_set();
 }
 inline py::object steal(PyObject *o) {
     check(o);
     return py::reinterpret_steal<py::object>(o);
 }
 inline std::string_view utf8(PyObject *s) {
-    if (!PyUnicode_Check(s)) throw Fallback();
+    if (!PyUnicode_Check(s)) layout("node ids must be str");
     Py_ssize_t n = 0;
     const char *p = PyUnicode_AsUTF8AndSize(s, &n);
     check((PyObject *)p);
@@ -64,7 +84,13 @@ std::vector<int> topo_order(const Graph &G) {
         for (int v : G.succ[u])
             if (--indeg[v] == 0) ready.push(v);
     }
-    if ((int)order.size() != G.n) throw Fallback();        // CycleError
+    if ((int)order.size() != G.n) {
+        // CycleError(f"graph contains a cycle through {stuck[:8]}"), stuck sorted
+        py::list stuck;
+        for (int i = 0; i < G.n && stuck.size() < 8; ++i)
+            if (indeg[i] > 0) stuck.append(py::reinterpret_borrow<py::object>(G.id[i]));
+        raise_obj(g_err.cycle, PyUnicode_FromFormat("graph contains a cycle through %R", stuck.ptr()));
+    }
     return order;
 }
 
@@ -94,11 +120,15 @@ py::object make(const py::object &cls, std::initializer_list<py::str> names,
 }
 
 py::object build(py::object g, py::object node_cls, py::object graph_cls, py::object sub_cls,
-                 py::object part_cls) {
+                 py::object part_cls, py::object cycle_error, py::object no_task_error,
+                 py::object dangling_error) {
+    g_err.cycle = cycle_error.ptr();
+    g_err.no_task = no_task_error.ptr();
+    g_err.dangling = dangling_error.ptr();
     Graph G;
     PyObject *nodes = g.attr("nodes").ptr();
     py::object nodes_ref = g.attr("nodes");
-    if (!PyDict_Check(nodes)) throw Fallback();
+    if (!PyDict_Check(nodes)) layout("nodes is not a dict");
     G.n = (int)PyDict_Size(nodes);
     const int n = G.n;
     G.id.resize(n);
@@ -119,7 +149,7 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
         std::string_view prev;
         while (PyDict_Next(nodes, &pos, &k, &v)) {
             std::string_view cur = utf8(k);
-            if (i > 0 && !(prev < cur)) throw Fallback();   // not in sorted-id order
+            if (i > 0 && !(prev < cur)) layout("nodes not in sorted-id order");
             prev = cur;
             G.id[i] = k;
             G.node[i] = v;
@@ -137,19 +167,19 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
                 check(PyDict_SetItem(index.ptr(), G.id[i], py::int_(i).ptr()) == 0 ? Py_None
                                                                                  : nullptr);
         PyObject *r = PyDict_GetItem(index.ptr(), key);
-        if (!r) throw Fallback();
+        if (!r) layout("an edge or input/output names an unknown node");
         return (int)PyLong_AsLong(r);
     };
     py::object pred_ref = g.attr("_pred"), succ_ref = g.attr("_succ");
     for (int i = 0; i < n; ++i) {
         for (int dir = 0; dir < 2; ++dir) {
             PyObject *t = PyDict_GetItem(dir ? succ_ref.ptr() : pred_ref.ptr(), G.id[i]);
-            if (!t || !PyTuple_Check(t)) throw Fallback();
+            if (!t || !PyTuple_Check(t)) layout("adjacency is not a tuple per node");
             auto &dst = dir ? G.succ[i] : G.pred[i];
             const Py_ssize_t m = PyTuple_GET_SIZE(t);
             dst.resize((size_t)m);
             for (Py_ssize_t k = 0; k < m; ++k) dst[k] = idx_of(PyTuple_GET_ITEM(t, k));
-            if (!std::is_sorted(dst.begin(), dst.end())) throw Fallback();
+            if (!std::is_sorted(dst.begin(), dst.end())) layout("adjacency not in sorted-id order");
         }
     }
     py::object inputs = g.attr("inputs"), outputs = g.attr("outputs");
@@ -180,11 +210,17 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
         }
     }
     const int na = (int)anchors.size();
-    if (na == 0) throw Fallback();                            // NoNonConstantTask
-    for (int v = 0; v < n; ++v)                               // DanglingOutput (outputs)
+    if (na == 0)                                              // atoms.py:178-179
+        raise_obj(g_err.no_task, PyUnicode_FromString("no task depends on a model input"));
+    for (int v = 0; v < n; ++v)                               // sorted(g.outputs), atoms.py:181-187
         if (G.is_output[v]) {
             const int p = producer(v);
-            if (p < 0 ? !G.is_input[v] : constant[p]) throw Fallback();
+            if (p < 0 && !G.is_input[v])
+                raise_obj(g_err.dangling, PyUnicode_FromFormat(
+                    "output %R is not produced by any task", G.id[v]));
+            if (p >= 0 && constant[p])
+                raise_obj(g_err.dangling, PyUnicode_FromFormat(
+                    "output %R depends on no model input", G.id[v]));
         }
 
     // _constant_closure per anchor (atoms.py:62-80); owners in anchor order
@@ -218,11 +254,12 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
             for (int x : cl) owners[x].push_back(a);
         }
     }
-    for (int u = 0; u < n; ++u) {                             // DanglingOutput (constants)
-        if (G.is_task[u] && constant[u] && owners[u].empty()) throw Fallback();
+    for (int u : topo)                                        // constant.items(), atoms.py:194-196
+        if (G.is_task[u] && constant[u] && owners[u].empty())
+            raise_obj(g_err.dangling, PyUnicode_FromFormat("constant task %R feeds no atom", G.id[u]));
+    for (int u = 0; u < n; ++u)                               // g.value_ids(), atoms.py:197-199
         if (!G.is_task[u] && producer(u) < 0 && !G.is_input[u] && owners[u].empty())
-            throw Fallback();
-    }
+            raise_obj(g_err.dangling, PyUnicode_FromFormat("constant value %R feeds no atom", G.id[u]));
 
     // clone ids (atoms.py:202-215): "<id>::c<rank>" per owning atom when shared
     bool cloned = false;
@@ -264,7 +301,9 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
             for (size_t r = 0; r < owners[u].size(); ++r) {
                 py::str cid = py::reinterpret_steal<py::str>(
                     steal(PyUnicode_FromFormat("%U::c%zu", G.id[u], r)).release());
-                if (PyDict_Contains(nodes, cid.ptr())) throw Fallback();   // collision
+                if (PyDict_Contains(nodes, cid.ptr()))               // atoms.py:209-210
+                    raise_obj(PyExc_ValueError, PyUnicode_FromFormat(
+                        "clone id %R collides with a node", cid.ptr()));
                 py::object nd = node_cls(cid, task, value);
                 keep.append(cid);
                 keep.append(nd);
@@ -285,7 +324,7 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
         nnode.resize(nn);
         for (int j = 0; j < nn; ++j) {
             const Item &it = items[order[j]];
-            if (j > 0 && !(items[order[j - 1]].key < it.key)) throw Fallback();
+            if (j > 0 && !(items[order[j - 1]].key < it.key)) layout("clone ids not unique");
             item_new[order[j]] = j;
             nid[j] = it.id;
             nnode[j] = it.node;
@@ -296,7 +335,7 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
             if (owners[u].size() <= 1) return old_to_new[u];
             const auto &ow = owners[u];
             const size_t r = (size_t)(std::lower_bound(ow.begin(), ow.end(), a) - ow.begin());
-            if (r >= ow.size() || ow[r] != a) throw Fallback();
+            if (r >= ow.size() || ow[r] != a) layout("closure ownership");   // unreachable
             return item_new[clone_slot[u][r]];
         };
         for (int a = 0; a < na; ++a) {
@@ -412,7 +451,7 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
         }
         int best = -1;
         for (int t : S[un]) {                                 // min (topo_pos, id)
-            if (task_atom[t] < 0) throw Fallback();
+            if (task_atom[t] < 0) layout("input consumed by a constant task");   // unreachable
             const int ot = anchors[task_atom[t]];
             if (best < 0 || topo_pos[ot] < topo_pos[anchors[task_atom[best]]]) best = t;
         }
@@ -492,7 +531,10 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
         py::object lref = py::reinterpret_steal<py::object>(lst);
         for (size_t k = 0; k < S[j].size(); ++k) {
             const int c = member_atom[S[j][k]];
-            if (c < 0) throw Fallback();                     // KeyError in the reference
+            if (c < 0) {                                     // self._task_atom[t] (atoms.py:103)
+                PyErr_SetObject(PyExc_KeyError, nid[S[j][k]]);
+                throw py::error_already_set();
+            }
             Py_INCREF(ints[c].ptr());
             PyList_SET_ITEM(lst, (Py_ssize_t)k, ints[c].ptr());
         }
@@ -508,14 +550,6 @@ py::object build(py::object g, py::object node_cls, py::object graph_cls, py::ob
 }  // namespace
 
 PYBIND11_MODULE(_atoms_native, m) {
-    static py::exception<Fallback> fallback(m, "Fallback");
-    py::register_exception_translator([](std::exception_ptr p) {
-        try {
-            if (p) std::rethrow_exception(p);
-        } catch (const Fallback &) {
-            PyErr_SetString(fallback.ptr(), "outside the native path's common case");
-        }
-    });
     m.def("build_atomic_subcomponents", &build,
-          "atoms.py:164-222 over the reference's host objects");
+          "atoms.py:164-222 over the reference's host objects; raises the reference's errors");
 }

@@ -75,7 +75,7 @@ __global__ void k_brute(BruteArgs a) {
                 if (kk < 0) { feasible = false; break; }               // m == 0
                 const int64_t o = hm_idx(lo, hi);
                 double tf = a.key_tf[kk][o];
-                if (signbit(tf)) { feasible = false; break; }          // mem > budget
+                if (!span_ok(tf, a.nonneg)) { feasible = false; break; }  // mem > budget
                 double tb = a.derived ? __dmul_rn(a.beta, tf) : a.key_tb[kk][o];
                 const double *cut = a.key_cut[kk];
                 if (hi < nb) {

@@ -23,6 +23,7 @@ namespace pcb {
 struct DevProblem {
     int nb = 0, n_tasks = 0, n_in = 0;
     int num_nodes = 1, dpn = 1, checkpointing = 0, monotone = 0;
+    int nonneg = 1;                  // every task time >= 0 (span_mark encoding below)
     int n_inter = 1;                 // 2 when num_nodes > 1 (intra / inter cut variants)
     int64_t mem_budget = 0;
     double flops = 1, beta = 2, factor = 4, bw_intra = 1, bw_inter = 1, lat = 0;
@@ -115,8 +116,21 @@ __host__ __device__ inline int inter_of(int num_nodes, int dpn, int64_t cum) {
 }
 
 // ------------------------------------------------------------------ key tables
+// Span feasibility (mem <= budget, stages.py:230) is carried in the t_fwd
+// table itself.  With non-negative task times (the FLOP model, or cost tables
+// without negative entries) an infeasible span keeps |t_fwd| with the sign bit
+// set: the DP's prefix-skip search reads the magnitude of every span.  When
+// some time can be negative the sign is data, the skip is off, and an
+// infeasible span holds NaN instead (NaN inputs are rejected on the host).
+__device__ __forceinline__ double span_mark(double tf, bool ok, int nonneg) {
+    return ok ? tf : (nonneg ? -tf : __longlong_as_double(0x7ff8000000000000ll));
+}
+__device__ __forceinline__ bool span_ok(double tf, int nonneg) {
+    return nonneg ? !signbit(tf) : !isnan(tf);
+}
+
 // One (microbatch share m, checkpointing) key:
-//   tf[hm_idx(lo,hi)]  t_fwd of span [lo,hi) at m, sign bit set if mem > budget
+//   tf[hm_idx(lo,hi)]  t_fwd of span [lo,hi) at m, marked by span_mark
 //   tb[hm_idx(lo,hi)]  t_bwd (absent when it is derived as beta * t_fwd)
 //   cut[inter][c]      cut_time(c, m, inter) for c in [0, nb]
 
@@ -163,7 +177,8 @@ struct DPBatch {
     const int32_t *const *key_ffb;  // per key: first feasible lo for each hi
     double beta;
     int num_nodes, dpn;
-    int mono_skip;                  // t_fwd(b', b) non-increasing in b' (flops >= 0): enable skip
+    int mono_skip;                  // task times >= 0: t_fwd(b', b) non-increasing in b' (the
+                                    // prefix skip) and the span_mark sign-bit encoding
     // per level, per (call, d column): smallest / largest b of a non-empty cell
     int32_t *col_min[2];
     int32_t *col_max[2];
@@ -218,8 +233,8 @@ void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_
                            const int32_t *keys_ckpt, const double *raw_tf, const double *raw_tb,
                            double *const *tf, double *const *tb, double *const *cut,
                            int derived, int *mismatch, cudaStream_t st);
-void launch_first_feasible(int nb, int n_keys, const double *const *tf, int32_t *const *ffb,
-                           cudaStream_t st);
+void launch_first_feasible(int nb, int n_keys, int nonneg, const double *const *tf,
+                           int32_t *const *ffb, cudaStream_t st);
 void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
                             const int64_t *m, const int32_t *ckpt, double *tf, double *tb,
                             int64_t *mem, cudaStream_t st);
@@ -260,6 +275,7 @@ struct BruteArgs {
     const int64_t *binom;         // [(n_max + 1) * kcols] C(a, j), saturated
     int kcols;
     int nb, S, D, derived, num_nodes, dpn;
+    int nonneg;                   // span_mark encoding of the key tables
     double beta;
     int64_t n_comb, n_comp, n_chunks;
     unsigned long long *out_key;  // per block winner
@@ -269,6 +285,7 @@ struct BruteArgs {
 void launch_brute(const BruteArgs &a, int blocks, cudaStream_t st);
 // peak.cu
 double measure_fp64_gops(cudaStream_t st, int sm_count);
+double measure_dadd_gops(cudaStream_t st, int sm_count);
 // sim.cu
 void launch_simulate(const DevProblem &p, int n_plans, const int32_t *plan_off,
                      const int32_t *plan_S, const int32_t *plan_R, const int32_t *plan_MB,

@@ -68,7 +68,7 @@ struct pc_ctx {
     using CallDesc = pcb::CallDesc;
     int device = 0;
     cudaStream_t st = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
     std::string err;
     int sm_count = 0;
     // problem
@@ -114,7 +114,7 @@ struct pc_ctx {
     int last_FL = 4;
     DPBatch last_batch{};
     // timing of the last batch
-    double last_dp_ms = 0, last_span_ms = 0;
+    double last_dp_ms = 0, last_span_ms = 0, last_post_ms = 0;
     int64_t last_dp_launches = 0;
     int64_t last_pairs = 0, last_cands = 0, last_inserts = 0;
     int64_t launches = 0;   // all kernel launches since the last reset

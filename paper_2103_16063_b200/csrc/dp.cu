@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
             zero = true;
         } else {
             const double tf = B.key_tf[kk][row];
-            if (!signbit(tf)) {
+            if (span_ok(tf, B.mono_skip)) {
                 double tfc = tf;
                 if (b < nb) tfc = __dadd_rn(tf, B.key_cut[kk][inter_d * (nb + 1) + b]);
                 const double tbc = DERIVED ? __dmul_rn(beta, tf) : B.key_tb[kk][row];
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                 int64_t pbase = 0;
                 if (cnt > 0) {
                     const double tf = tfrow[bp];
-                    if (!signbit(tf)) {                             // mem <= budget (stages.py:230)
+                    if (span_ok(tf, B.mono_skip)) {                             // mem <= budget (stages.py:230)
                         tfc = b < nb ? __dadd_rn(tf, cutf) : tf;
                         tbc = DERIVED ? __dmul_rn(beta, tf) : tbrow[bp];
                         if (bp > 0) tbc = __dadd_rn(tbc, cutb[bp]);

@@ -170,9 +170,7 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
         const int64_t mem = (int64_t)memd;
         const bool ok = mem <= p.mem_budget;                   // stages.py:230
         const int64_t o = hm_idx(lo, hi);
-        // infeasible spans keep |t_fwd| with the sign bit set: the DP skip
-        // search needs the magnitude, the DP tests signbit for feasibility
-        out_f[o] = ok ? f : -f;
+        out_f[o] = span_mark(f, ok, p.nonneg);
         if (derived) {
             // every span, feasible or not: the DP's skip search reads
             // beta * |t_fwd| as t_bwd on infeasible spans too
@@ -201,21 +199,22 @@ void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_
 
 // First feasible lo of every hi (per key): the DP skips b' below it, which
 // are all infeasible by construction (no monotonicity assumed).
-__global__ void k_first_feasible(int nb, int n_keys, const double *const *tf, int32_t *const *ffb) {
+__global__ void k_first_feasible(int nb, int n_keys, int nonneg, const double *const *tf,
+                                 int32_t *const *ffb) {
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= (int64_t)n_keys * (nb + 1)) return;
     const int k = (int)(gid / (nb + 1));
     const int hi = (int)(gid % (nb + 1));
     const double *row = tf[k] + hm_idx(0, hi);
     int lo = 0;
-    while (lo < hi && signbit(row[lo])) ++lo;
+    while (lo < hi && !span_ok(row[lo], nonneg)) ++lo;
     ffb[k][hi] = lo;
 }
 
-void launch_first_feasible(int nb, int n_keys, const double *const *tf, int32_t *const *ffb,
-                           cudaStream_t st) {
+void launch_first_feasible(int nb, int n_keys, int nonneg, const double *const *tf,
+                           int32_t *const *ffb, cudaStream_t st) {
     const int64_t n = (int64_t)n_keys * (nb + 1);
-    k_first_feasible<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(nb, n_keys, tf, ffb);
+    k_first_feasible<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(nb, n_keys, nonneg, tf, ffb);
 }
 
 // ---------------------------------------------------------------- queries

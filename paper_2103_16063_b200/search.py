@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import heapq
+import time
 
 import numpy as np
 
@@ -284,7 +285,12 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
     world = dist.get_world_size(group) if dist_on else 1
     rank = dist.get_rank(group) if dist_on else 0
     ctx = _lib.context()
-    bind_problem(ctx, blocks)
+    tm = {} if timings is not None else None
+    bind_problem(ctx, blocks, tm)
+    if tm is not None:
+        # device-resident part of the call: CUDA events on the library stream
+        ctx.check(ctx.lib.pc_timer_start(ctx.h), "timer")
+        t_res = time.perf_counter()
     nb = len(blocks)
     calls, levels = enumerate_calls(num_nodes, devices_per_node, batch_size, nb)
     n_levels = (max(levels) + 1) if levels else 0
@@ -296,19 +302,35 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
                                  rank, group, dev, opts, batch_size)
     owner = lpt_shard(nb, calls, world, weights)
     local_idx = [i for i in range(len(calls)) if owner[i] == rank]
+    if tm is not None:
+        t_calls = time.perf_counter()
     batch = run_calls(ctx, [calls[i] for i in local_idx], batch_size,
                       opts.disable_pruning, True)
+    if tm is not None:
+        t_pack = time.perf_counter()
     rec, plan_w = _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels, max_stages)
+    if tm is not None:
+        t_ex = time.perf_counter()
     allrec = exchange(rec, group, dev)
-    if timings is not None:
-        timings.update(pairs=int(batch.stats.pairs), candidates=int(batch.stats.candidates),
-                       dp_ms=float(batch.stats.device_ms), span_ms=float(batch.stats.span_ms),
-                       dp_launches=int(batch.stats.dp_launches),
-                       kernel_launches=int(batch.stats.kernel_launches),
-                       local_unpruned=int(batch.stats.visits_unpruned),
-                       unpruned=sum(call_weight(nb, c) for c in calls),
-                       h2d_bytes=_flat_bytes(ctx.problem_flat), d2h_bytes=int(rec.nbytes))
+    if tm is not None:
+        t_dec = time.perf_counter()
     out = decide(allrec, calls, levels, owner, plan_w, opts.visit_budget, batch_size)
+    if tm is not None:
+        t_end = time.perf_counter()
+        ms = C.c_double()
+        ctx.check(ctx.lib.pc_timer_stop(ctx.h, C.byref(ms)), "timer")
+        st = batch.stats
+        timings.update(
+            tm, pairs=int(st.pairs), candidates=int(st.candidates),
+            dp_ms=float(st.device_ms), span_ms=float(st.span_ms), post_ms=float(st.post_ms),
+            dp_launches=int(st.dp_launches), kernel_launches=int(st.kernel_launches),
+            local_unpruned=int(st.visits_unpruned),
+            unpruned=sum(call_weight(nb, c) for c in calls),
+            h2d_bytes=_flat_bytes(ctx.problem_flat), d2h_bytes=int(rec.nbytes),
+            resident_ms=ms.value,
+            weights_ms=(t_calls - t_res) * 1e3, run_calls_ms=(t_pack - t_calls) * 1e3,
+            pack_ms=(t_ex - t_pack) * 1e3, exchange_ms=(t_dec - t_ex) * 1e3,
+            decide_ms=(t_end - t_dec) * 1e3)
     if out[0] == "plan":
         return out[1]
     _, cross, before = out
@@ -336,7 +358,9 @@ def _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, gr
         v[0] = at.value
     if world > 1:
         t = torch.from_numpy(v).to(dev)
-        dist.broadcast(t, src=owner[cross], group=group)
+        # owner[] holds ranks within `group`; broadcast's src is a global rank
+        src = owner[cross] if group is None else dist.get_global_rank(group, owner[cross])
+        dist.broadcast(t, src=src, group=group)
         v = t.cpu().numpy()
     raise SearchBudgetExceeded(int(v[0]), int(opts.visit_budget))
 

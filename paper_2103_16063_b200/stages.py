@@ -11,6 +11,7 @@ runs on the GPU through libpipecut_b200.so.
 from __future__ import annotations
 
 import ctypes as C
+import time
 import weakref
 
 from . import _lib, abi
@@ -28,14 +29,22 @@ StagePlan = _stages.StagePlan
 Plan = _stages.Plan
 
 
-def bind_problem(ctx: _lib.Context, blocks):
-    """Upload the flattened BlockSet once per BlockSet object."""
+def bind_problem(ctx: _lib.Context, blocks, timings: dict | None = None):
+    """Upload the flattened BlockSet once per BlockSet object.  ``timings``
+    gets flatten_ms (host) and upload_ms (pc_set_problem: host->device copy
+    of the arrays and the span-input tables)."""
     owner = ctx.problem_owner() if ctx.problem_owner is not None else None
     if owner is blocks:
+        if timings is not None:
+            timings.update(flatten_ms=0.0, upload_ms=0.0)
         return ctx.problem_flat
+    t0 = time.perf_counter()
     flat = flatten_blockset(blocks)
+    t1 = time.perf_counter()
     st = abi.problem_struct(flat)
     ctx.check(ctx.lib.pc_set_problem(ctx.h, C.byref(st)), "pc_set_problem")
+    if timings is not None:
+        timings.update(flatten_ms=(t1 - t0) * 1e3, upload_ms=(time.perf_counter() - t1) * 1e3)
     ctx.problem_owner = weakref.ref(blocks)
     ctx.problem_flat = flat
     ctx.problem_shares = frozenset()
@@ -136,22 +145,27 @@ def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
         raise InvalidArgs("node count, devices per node and batch size must be at least 1")
     opts = options or SearchOptions()
     ctx = _lib.context()
-    flat = bind_problem(ctx, blocks)
+    tm = {} if last_stats is not None else None
+    flat = bind_problem(ctx, blocks, tm)
     if flat.has_cost_table:
         from .search import enumerate_calls
         calls, _ = enumerate_calls(num_nodes, devices_per_node, batch_size, len(blocks))
         bind_overrides(ctx, flat, call_shares(calls, batch_size))
     buf = abi.PlanBuffers(max(1, len(blocks)))
     st = abi.PcStats()
+    t0 = time.perf_counter()
     rc = ctx.lib.pc_form_stage(ctx.h, num_nodes, devices_per_node, batch_size,
                                int(bool(opts.disable_pruning)), _budget(opts),
                                2 if speculative is None else int(bool(speculative)),
                                C.byref(buf.s), C.byref(st))
     ctx.check(rc, "form_stage")
     if last_stats is not None:
-        last_stats.update(visits=int(st.visits), dp_calls=int(st.dp_calls),
+        last_stats.update(tm, library_ms=(time.perf_counter() - t0) * 1e3,
+                          kernel_launches=int(st.kernel_launches),
+                          visits=int(st.visits), dp_calls=int(st.dp_calls),
                           visits_unpruned=int(st.visits_unpruned), cells=int(st.cells),
-                          device_ms=float(st.device_ms), span_ms=float(st.span_ms))
+                          device_ms=float(st.device_ms), span_ms=float(st.span_ms),
+                          post_ms=float(st.post_ms))
     if rc == abi.PC_ERR_BUDGET:
         raise SearchBudgetExceeded(int(st.visits), int(opts.visit_budget))
     stats = SearchStats(visits=int(st.visits), dp_calls=int(st.dp_calls))

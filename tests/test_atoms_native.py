@@ -13,7 +13,8 @@ import cases
 from paper_2103_16063_b200 import atoms as A
 from paper_2103_16063_b200._host import pipecut as pc
 
-pytestmark = pytest.mark.skipif(A._atoms_native is None, reason="native atoms module not built")
+# the unmodified reference function (the checker); install() may rebind the name later
+_reference = pc.atoms.build_atomic_subcomponents
 
 _val, _task, TaskGraph = cases._val, cases._task, cases.TaskGraph
 
@@ -43,7 +44,7 @@ def _outcome(fn, g):
 
 def _check(g):
     got, gerr = _outcome(A.build_atomic_subcomponents, g)
-    want, werr = _outcome(A._reference, g)
+    want, werr = _outcome(_reference, g)
     assert gerr == werr
     if werr is None:
         _same(got, want)
@@ -96,8 +97,9 @@ def test_generators():
         assert _check(g)
     g = pc.gen_bert_like(64, 2, 16, 100)                      # the native path itself, no fallback
     _same(A._atoms_native.build_atomic_subcomponents(
-        g, pc.graph.Node, pc.TaskGraph, pc.atoms.Subcomponent, pc.atoms.AtomicPartition),
-        A._reference(g))
+        g, pc.graph.Node, pc.TaskGraph, pc.atoms.Subcomponent, pc.atoms.AtomicPartition,
+        pc.graph.CycleError, pc.atoms.NoNonConstantTask, pc.atoms.DanglingOutput),
+        _reference(g))
 
 
 def test_reference_families():
@@ -155,8 +157,34 @@ def test_rejected_graphs_raise_the_reference_errors():
         TaskGraph([x, _task("a"), _val("va"), _task("b"), y],
                   [("x", "a"), ("a", "va"), ("va", "b"), ("b", "y"), ("y", "a")], ["x"], ["y"]),
     ]
+    # two dangling constant tasks whose topological order differs from id order
+    # (the reference reports the first in topological order)
+    bad.append(TaskGraph([x, _val("w", fixed=4, param=True), _task("z1"), _val("k1"),
+                          _task("a2"), _val("k2"), _task("t"), y],
+                         [("w", "z1"), ("z1", "k1"), ("k1", "a2"), ("a2", "k2"), ("x", "t"),
+                          ("t", "y")], ["x"], ["y"]))
+    # two dangling outputs: the first in sorted id order
+    bad.append(TaskGraph([x, _task("t"), y, _val("o2"), _val("o1")], [("x", "t"), ("t", "y")],
+                         ["x"], ["y", "o2", "o1"]))
+    # a long cycle: the message lists the first 8 stuck ids
+    ring = [f"r{i:02d}" for i in range(12)]
+    nodes = [x, y, _task("t")]
+    edges = [("x", "t"), ("t", "y")]
+    for i, r in enumerate(ring):
+        nodes += [_task(r), _val(r + "v")]
+        edges += [(r, r + "v"), (r + "v", ring[(i + 1) % len(ring)])]
+    bad.append(TaskGraph(nodes, edges, ["x"], ["y"]))
+    kinds = set()
     for g in bad:
         assert not _check(g)
+        kinds.add(_outcome(_reference, g)[1][0].__name__)
+    assert kinds == {"NoNonConstantTask", "DanglingOutput", "ValueError", "CycleError"}
+
+
+def test_missing_native_module_is_a_hard_error(monkeypatch):
+    monkeypatch.setattr(A, "_atoms_native", None)
+    with pytest.raises(A.NativeUnavailable):
+        A.build_atomic_subcomponents(pc.gen_bert_like(64, 2, 16, 100))
 
 
 def test_input_as_output_and_dead_inputs():
@@ -175,4 +203,4 @@ def test_install_rebinds_the_cli_name():
         assert pipecut.cli.build_atomic_subcomponents is pb.build_atomic_subcomponents
     finally:
         restore()
-    assert pipecut.cli.build_atomic_subcomponents is A._reference
+    assert pipecut.cli.build_atomic_subcomponents is _reference

@@ -157,3 +157,31 @@ def test_oracle_form_stage_matches_golden_chains():
         assert [[s[0], s[1], s[2]] for s in plan["stages"]] == [s[:3] for s in want["stages"]]
         assert plan["MB"] == want["microbatches"] and plan["R"] == want["replica_factor"]
         assert visits == doc["visits"] and calls == doc["dp_calls"]
+
+
+def test_oracle_span_row_path_matches_per_span_and_reference():
+    """The oracle's memo-row fold (monotone graphs: chains and the reference's
+    random DP families are monotone) equals its per-span fold and
+    CostModel.profile bit for bit, at every span, share and ckpt."""
+    rng = random.Random(31)
+    cases_ = [cases.c5_blockset(40, 16, jitter_seed=3)]
+    for _ in range(6):
+        cases_.append(cases.stages_random_instance(rng)[0])
+    checked = 0
+    for bs in cases_:
+        fp = flatten_blockset(bs)
+        if not fp.monotone:
+            continue
+        op = OracleProblem(fp)
+        nb = len(bs)
+        for lo in range(nb):
+            for hi in range(lo + 1, nb + 1):
+                for m in (1, 5, 64):
+                    for ck in (False, True):
+                        got = op.span_row(lo, hi, m, ck)
+                        assert got == op.span(lo, hi, m, ck)
+                        if (lo * 7 + hi) % 5 == 0:
+                            r = bs.model.profile(bs.span(lo, hi), m, checkpointing=ck)
+                            assert got == (r.t_fwd_sec, r.t_bwd_sec, r.mem_bytes)
+                        checked += 1
+    assert checked > 5000
