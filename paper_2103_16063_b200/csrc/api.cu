@@ -453,6 +453,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         cd.hist_off = hist_cells;
         cd.orig = order[i];
         cd.pad = 0;
+        cd.U = ctx->bb_U.empty() ? INFINITY : ctx->bb_U[order[i]];
         const int64_t cells = (int64_t)cd.A * cd.B;
         val_cells += cells;
         hist_cells += cells * cd.S;
@@ -864,6 +865,28 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     if (!cur.empty()) {
         if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
         ++*n_chunks;
+    }
+    // PIPECUT_B200_BB_ORACLE (measurement only): rerun the calls with each
+    // call's own optimum as the bound and report both DP times
+    if (getenv("PIPECUT_B200_BB_ORACLE") && ctx->bb_U.empty() && !ctx->has_cost_table && ctx->mono_skip) {
+        const double dp0 = ctx->last_dp_ms;
+        std::vector<CallOut> first = outs;
+        ctx->bb_U.assign(calls.size(), INFINITY);
+        for (size_t i = 0; i < calls.size(); ++i)
+            if (first[i].feasible) ctx->bb_U[i] = first[i].objective;
+        ctx->last_dp_ms = 0;
+        int ch = 0;
+        int rc = run_calls_impl(ctx, calls, BS, pruning, want_iter, outs, &ch);
+        ctx->bb_U.clear();
+        if (rc) return rc;
+        int bad = 0;
+        for (size_t i = 0; i < calls.size(); ++i)
+            if (first[i].feasible != outs[i].feasible || (first[i].feasible &&
+                (first[i].objective != outs[i].objective || first[i].lo != outs[i].lo ||
+                 first[i].dev != outs[i].dev || first[i].iteration != outs[i].iteration)))
+                ++bad;
+        fprintf(stderr, "[pipecut_b200] bound oracle: %zu calls, dp %.1f ms -> %.1f ms, %d mismatches\n",
+                calls.size(), dp0, ctx->last_dp_ms, bad);
     }
     return PC_OK;
 }

@@ -151,6 +151,8 @@ struct CallDesc {
     int64_t col_off;           // offset of this call's d columns in the column-bound arrays
     int32_t orig;              // index in the caller's call list
     int32_t pad;
+    double U;                  // objective upper bound (+inf: none); candidates whose
+                               // every completion exceeds it are dropped (dp.cu: bound)
 };
 
 // Warps (cells) per CTA of the level kernel: 4 warps x 8 CTAs per SM (64

@@ -109,6 +109,7 @@ struct pc_ctx {
     // last batch (for budget crossing queries)
     std::vector<CallDesc> last_calls;   // sorted order
     std::vector<int> last_pos;          // orig -> sorted position
+    std::vector<double> bb_U;           // per call of the current run_calls_impl (bound)
     std::vector<std::vector<int64_t>> last_level_sums;  // by orig
     int last_pruning = 1;
     int last_FL = 4;

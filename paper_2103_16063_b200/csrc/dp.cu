@@ -215,6 +215,34 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
     const int64_t row = (int64_t)b * (b - 1) / 2;       // hm_idx(0, b)
     const double beta = B.beta;
     const WarpFront F = warp_front(w);
+    // Objective bound (CallDesc.U, finite only with non-negative times and no
+    // cost table): every completion of an entry (x, y) of this cell costs at
+    // least max(x, lbf) + max(y, lbb) -- the S - s stages still to come cover
+    // [b, nb) at shares >= the share of the most devices one of them can get,
+    // so their largest raw time is >= t(b, nb; that share) / (S - s) (times
+    // are monotone in the share; the factor absorbs the fold's rounding).
+    // Entries above U cannot lead to a plan at or below U, so they are dropped;
+    // level S keeps only the final cell (nb, D).
+    const double U = cd.U;
+    const bool bounded = U < INFINITY;
+    double lbf = 0.0, lbb = 0.0;
+    if (bounded) {
+        if (s == cd.S) {
+            if (b != nb || d != cd.D) lbf = INFINITY;
+        } else {
+            const int devmax = (cd.D - d) - (cd.S - s - 1);
+            const int kx = keyidx[devmax];
+            if (kx >= 0) {
+                const int64_t o = hm_idx(b, nb);
+                const double k = (1.0 - 1e-9) / (double)(cd.S - s);
+                lbf = __dmul_rn(fabs(B.key_tf[kx][o]), k);
+                lbb = DERIVED ? __dmul_rn(beta, lbf) : __dmul_rn(fabs(B.key_tb[kx][o]), k);
+            }
+        }
+    }
+    auto over = [&](double x, double y) {
+        return bounded && __dadd_rn(dmax_ref(x, lbf), dmax_ref(y, lbb)) > U;
+    };
     int n = 0;
     bool ovf = false;
     bool zero = false;
@@ -232,9 +260,11 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                 double tfc = tf;
                 if (b < nb) tfc = __dadd_rn(tf, B.key_cut[kk][inter_d * (nb + 1) + b]);
                 const double tbc = DERIVED ? __dmul_rn(beta, tf) : B.key_tb[kk][row];
-                if (lane == 0) F.put(0, dmax_ref(0.0, tfc), dmax_ref(0.0, tbc), pack_key(0, 0, 0));
-                __syncwarp();
-                n = 1;
+                if (!over(dmax_ref(0.0, tfc), dmax_ref(0.0, tbc))) {
+                    if (lane == 0) F.put(0, dmax_ref(0.0, tfc), dmax_ref(0.0, tbc), pack_key(0, 0, 0));
+                    __syncwarp();
+                    n = 1;
+                }
                 n_pairs = lane == 0;
                 n_cands = lane == 0;
             }
@@ -308,7 +338,9 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                         // tb (last entry), each clipped by the new stage
                         const double ix = dmax_ref(etf[pbase], tfc);
                         const double iy = dmax_ref(etb[pbase + cnt - 1], tbc);
-                        if (n > 0 && corner_dominated(F, n, ix, iy)) { if (PC_DP_DIAG) ++n_corner; }
+                        if ((n > 0 && corner_dominated(F, n, ix, iy)) || over(ix, iy)) {
+                            if (PC_DP_DIAG) ++n_corner;
+                        }
                         else {
                             // exact window: entries with ptf <= tfc collapse onto the
                             // last of them, entries with ptb <= tbc onto the first
@@ -371,7 +403,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                         cx = dmax_ref(xt[o_pb + i], o_tfc);
                         cy = dmax_ref(yt[o_pb + i], o_tbc);
                         ck = pack_key(o_bp, dp, i);
-                        surv = n == 0 || !front_dominated(F, n, cx, cy, ck);
+                        surv = (n == 0 || !front_dominated(F, n, cx, cy, ck)) && !over(cx, cy);
                     }
                     while (__any_sync(0xffffffffu, surv)) {
                         // insert the lexicographically smallest survivor first: nothing
@@ -395,7 +427,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
             // a prefix of b': a 32-ary warp search finds its end, and b' up to
             // there are skipped without loading their predecessors.
             for (int top = bp_hi; top > lim; top -= 32) {
-                if (B.mono_skip && n > 0 && (int)n_ins != lim_v) {
+                if (B.mono_skip && (n > 0 || bounded) && (int)n_ins != lim_v) {
                     int lo_b = lim, hi_b = top + 1;   // cond true <= lo_b, false >= hi_b
                     while (hi_b - lo_b > 1) {
                         const int span = hi_b - lo_b - 1;
@@ -406,7 +438,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
                             const double tv = fabs(tfrow[p]);
                             const double tfc = b < nb ? __dadd_rn(tv, cutf) : tv;
                             const double tbl = DERIVED ? __dmul_rn(beta, tv) : fabs(tbrow[p]);
-                            cond = corner_dominated(F, n, tfc, tbl);
+                            cond = (n > 0 && corner_dominated(F, n, tfc, tbl)) || over(tfc, tbl);
                         }
                         const uint32_t m = __ballot_sync(0xffffffffu, cond);
                         const int k = __popc(m);              // a prefix of the lanes

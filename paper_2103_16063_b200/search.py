@@ -27,7 +27,8 @@ import numpy as np
 
 from . import _lib, abi
 from .stages import (InvalidArgs, Plan, SearchBudgetExceeded, SearchOptions, SearchResult,
-                     SearchStats, StagePlan, bind_overrides, bind_problem, call_shares)
+                     SearchStats, StagePlan, bind_overrides, bind_problem, call_shares,
+                     checked_form_stage, times_nonneg)
 
 
 def enumerate_calls(num_nodes: int, dpn: int, batch_size: int, nb: int):
@@ -286,7 +287,11 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
     rank = dist.get_rank(group) if dist_on else 0
     ctx = _lib.context()
     tm = {} if timings is not None else None
-    bind_problem(ctx, blocks, tm)
+    flat = bind_problem(ctx, blocks, tm)
+    if not times_nonneg(flat):
+        # negative span times: the reference can raise InvalidPlan while ranking
+        # (stages.checked_form_stage); every rank runs that exact path itself
+        return checked_form_stage(ctx, num_nodes, devices_per_node, batch_size, blocks, opts)
     if tm is not None:
         # device-resident part of the call: CUDA events on the library stream
         ctx.check(ctx.lib.pc_timer_start(ctx.h), "timer")
@@ -365,11 +370,20 @@ def _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, gr
     raise SearchBudgetExceeded(int(v[0]), int(opts.visit_budget))
 
 
+# Schedule (i): a widening level whose summed sharding weight (pc_call_weights,
+# ~feasible pairs) is below this runs whole on every rank instead of being
+# sharded: such a level takes ~10 ms on one B200 (tools/level_costs.py, r2c:
+# ~1e-11 s per weight unit plus a few ms of launches), so splitting it saves
+# less than the pack + all-gather + decide round it would cost.
+REPLICATE_BELOW = 1.0e9
+
+
 def _sharded_by_level(ctx, calls, levels, n_levels, max_stages, nb, weights, world, rank, group,
                       dev, opts, batch_size):
     """Schedule (i): widening levels in order, each level's calls sharded
-    (LPT within the level) and one exchange per level; the reference's rule is
-    applied to the calls evaluated so far after every level."""
+    (LPT within the level) and one exchange per level -- or, for a light level,
+    run whole on every rank with no exchange; the reference's rule is applied
+    to the calls evaluated so far after every level."""
     n = len(calls)
     owner = [0] * n
     allrec = None
@@ -380,23 +394,33 @@ def _sharded_by_level(ctx, calls, levels, n_levels, max_stages, nb, weights, wor
         while end < n and levels[end] == lv:
             end += 1
         idx = list(range(start, end))
-        lv_owner = lpt_shard(nb, [calls[i] for i in idx], world,
-                             None if weights is None else [weights[i] for i in idx])
-        for i, o in zip(idx, lv_owner):
-            owner[i] = o
+        replicated = world == 1 or (weights is not None and
+                                    sum(weights[i] for i in idx) < REPLICATE_BELOW)
+        if replicated:
+            for i in idx:
+                owner[i] = rank        # every rank computes (and owns) every call
+        else:
+            lv_owner = lpt_shard(nb, [calls[i] for i in idx], world,
+                                 None if weights is None else [weights[i] for i in idx])
+            for i, o in zip(idx, lv_owner):
+                owner[i] = o
         local_idx = [i for i in idx if owner[i] == rank]
         batch = run_calls(ctx, [calls[i] for i in local_idx], batch_size,
                           opts.disable_pruning, True)
         rec, plan_w = _pack(nb, calls, levels, owner, rank, batch, local_idx, n_levels,
                             max_stages)
-        got = exchange(rec, group, dev)
+        if replicated:
+            got = np.zeros((max(world, 1), rec.size))
+            got[rank] = rec                                    # this rank's row only
+        else:
+            got = exchange(rec, group, dev)
         allrec = got if allrec is None else allrec + got      # disjoint slots per level
         out = decide(allrec, calls, levels, owner, plan_w, opts.visit_budget, batch_size,
                      upto=end)
         if out[0] == "budget":
             _, cross, before = out
-            _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, group,
-                            dev, opts, batch_size)
+            _raise_crossing(ctx, calls, owner, local_idx, cross, before,
+                            1 if replicated else world, rank, group, dev, opts, batch_size)
         result = out[1]
         if result.plan is not None or end == n:
             return result

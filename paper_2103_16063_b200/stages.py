@@ -147,6 +147,8 @@ def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
     ctx = _lib.context()
     tm = {} if last_stats is not None else None
     flat = bind_problem(ctx, blocks, tm)
+    if not times_nonneg(flat):
+        return checked_form_stage(ctx, num_nodes, devices_per_node, batch_size, blocks, opts)
     if flat.has_cost_table:
         from .search import enumerate_calls
         calls, _ = enumerate_calls(num_nodes, devices_per_node, batch_size, len(blocks))
@@ -171,6 +173,67 @@ def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
     stats = SearchStats(visits=int(st.visits), dp_calls=int(st.dp_calls))
     plan = plan_from_buffers(buf, batch_size) if rc == abi.PC_OK else None
     return SearchResult(plan, stats)
+
+
+def times_nonneg(flat) -> bool:
+    """Every task time the search can see is >= 0 (FLOP model with
+    non-negative FLOPs, cost-table entries with non-negative times)."""
+    if not (flat.flops_per_sec > 0 and flat.bwd_fwd_ratio >= 0):
+        return False
+    if flat.task_flops.size and not (flat.task_flops >= 0).all():
+        return False
+    table = getattr(flat.cost_config, "cost_table", None) if flat.has_cost_table else None
+    for e in (table or {}).values():
+        if not (e.t_fwd >= 0) or (e.t_bwd is not None and not (e.t_bwd >= 0)):
+            return False
+    return True
+
+
+def checked_form_stage(ctx, num_nodes: int, devices_per_node: int, batch_size: int, blocks,
+                       opts):
+    """form_stage (stages.py:372-413) when span times can be negative.  The
+    reference ranks every feasible candidate of the first feasible level with
+    simulate(), whose validate_plan (stages.py:416-492) recomputes the
+    objective without the DP's 0.0 start entry: a plan whose stage times are
+    all negative fails it and min() raises InvalidPlan at the first such
+    candidate in call order.  Here the levels run in order as device batches
+    (every call's plan kept), the visit budget is applied over the level as the
+    reference's cells would cross it, and each feasible candidate is validated
+    on the device (simulate.validate_plan) in call order before ranking."""
+    from .search import enumerate_calls, rank_key, run_calls
+    from .simulate import InvalidPlan, validate_plan
+    nb = len(blocks)
+    calls, levels = enumerate_calls(num_nodes, devices_per_node, batch_size, nb)
+    budget = opts.visit_budget
+    visits = counted = 0
+    lv_all = sorted(set(levels))
+    for lv in lv_all:
+        idx = [i for i in range(len(calls)) if levels[i] == lv]
+        batch = run_calls(ctx, [calls[i] for i in idx], batch_size, opts.disable_pruning, True)
+        for j in range(len(idx)):
+            v = int(batch.results[j]["visits"])
+            counted += 1
+            if budget is not None and visits + v > budget:
+                at = C.c_int64()
+                ctx.check(ctx.lib.pc_last_crossing(ctx.h, j, visits, int(budget), C.byref(at)),
+                          "pc_last_crossing")
+                raise SearchBudgetExceeded(int(at.value), int(budget))
+            visits += v
+        best = None
+        for j, i in enumerate(idx):
+            plan = batch.plan(j, batch_size)
+            if plan is None:
+                continue
+            bad = validate_plan(plan, blocks)
+            if bad:
+                raise InvalidPlan(bad)
+            key = rank_key(float(batch.results[j]["iteration_time"]), plan.objective,
+                           plan.microbatches, i)
+            if best is None or key < best[0]:
+                best = (key, plan)
+        if best is not None:
+            return SearchResult(best[1], SearchStats(visits=visits, dp_calls=counted))
+    return SearchResult(None, SearchStats(visits=visits, dp_calls=counted))
 
 
 @_lib.serialized

@@ -215,3 +215,71 @@ def test_select_matches_reference_form_stage_semantics_live():
     ref = pc.form_stage(2, 2, 16, bs)
     assert plans[best] == ref.plan
     assert running == ref.stats.visits and counted == ref.stats.dp_calls
+
+
+def _level_worker(rank, world, port, seed, heavy, q):
+    """Schedule (i) on gloo with run_calls faked: light levels run on every
+    rank without an exchange, heavy ones are sharded (search.REPLICATE_BELOW)."""
+    import torch.distributed as dist
+
+    from paper_2103_16063_b200 import search
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        calls, levels = enumerate_calls(4, 2, 16, 6)
+        recs = _fake_records(calls, seed)
+        index = {c: i for i, c in enumerate(calls)}
+        exchanges = []
+
+        def fake_run_calls(ctx, sub, bs, prune, want):
+            idx = [index[c] for c in sub]
+            return _FakeBatch([recs[i][0] for i in idx], [recs[i][1] for i in idx])
+
+        real_exchange = search.exchange
+
+        def counting_exchange(rec, group, dev):
+            exchanges.append(1)
+            return real_exchange(rec, group, None)
+
+        search.run_calls = fake_run_calls
+        search.exchange = counting_exchange
+        # level weights: the heavy levels above the threshold, the rest below it
+        w = [int(search.REPLICATE_BELOW) if levels[i] in heavy else 1 for i in range(len(calls))]
+        res = search._sharded_by_level(None, calls, levels, max(levels) + 1,
+                                       max(c[0] for c in calls), 6, w, world, rank, None, None,
+                                       pc.SearchOptions(), 16)
+        q.put((rank, None if res.plan is None else res.plan.to_json(), res.stats.visits,
+               res.stats.dp_calls, len(exchanges)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed,world,heavy", [(0, 2, ()), (3, 2, (1,)), (5, 4, (0, 2)),
+                                              (4, 2, (0, 1, 2))])
+def test_gloo_level_by_level_replicates_light_levels(seed, world, heavy):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_level_worker, args=(r, world, port, seed, heavy, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    calls, levels = enumerate_calls(4, 2, 16, 6)
+    recs = _fake_records(calls, seed)
+    want = _select_reference_way(calls, levels, recs, None)
+    for rank, plan, visits, dp_calls, n_ex in outs:
+        assert visits == want[2] and dp_calls == want[3]
+        if want[1] is None:
+            assert plan is None
+        else:
+            assert plan["microbatches"] == calls[want[1]][3]
+            assert plan["objective"] == recs[want[1]][0].objective
+        # one exchange per sharded level evaluated, none for the light ones
+        evaluated = sorted({levels[i] for i in range(len(calls))})[:len(set(levels))]
+        assert n_ex <= sum(1 for lv in evaluated if lv in heavy)
+    assert all(o[1:] == outs[0][1:] for o in outs)
