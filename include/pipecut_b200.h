@@ -229,7 +229,7 @@ int pc_simulate(pc_ctx *ctx, const pc_plan *plan, int64_t batch_size, int32_t ev
                 double *ev_end, double *summary);
 
 /* Sharding weights for n calls (the LPT key of form_stage_sharded): per call
- * S * sum_b sum_dev (B - dev + 1) * #{lo < b : span (lo, b) fits at the share
+ * S * sum_b sum_dev (B - dev + 1) * #{1 <= lo < b : span (lo, b) fits at the share
  * of dev devices}, from the key tables (built for every call's shares).
  * Exact integers: every rank computes the same assignment. */
 int pc_call_weights(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
@@ -265,7 +265,9 @@ int pc_form_stage(pc_ctx *ctx, int32_t num_nodes, int32_t devices_per_node,
                   int32_t speculative, pc_plan *plan, pc_stats *stats);
 
 /* Budget crossing inside call `index` of the last pc_run_calls batch given
- * the visits accumulated before it (stages.py:214-216): -1 if not crossed. */
+ * the visits accumulated before it (stages.py:214-216): -1 if not crossed,
+ * -2 if that call ran in an earlier memory chunk / wave of the batch (its
+ * flags are gone: run it alone and ask again). */
 int pc_last_crossing(pc_ctx *ctx, int32_t index, int64_t visits_before, int64_t budget,
                      int64_t *visits_at_cross);
 

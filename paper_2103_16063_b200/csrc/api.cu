@@ -5,6 +5,7 @@
 // sizes buffers, orders launches and applies the reference's enumeration and
 // selection rules over per-call records (form_stage, stages.py:372-413).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -329,11 +330,19 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
                               ctx->mismatch_d.as<int>(), ctx->st);
         ctx->launches++;
         if (int rc = check_launch(ctx, "span_dp_tables")) return rc;
-        launch_first_feasible(P.nb, nf, P.nonneg, d_pf, d_pff, ctx->st);
+        // the bound (run_chunk) needs suffix-closed feasibility: checked where it can apply
+        const int check = (!ctx->has_cost_table && ctx->mono_skip) ? 1 : 0;
+        CUDA_TRY(ctx, ctx->open_d.ensure(sizeof(int) * (size_t)nf + 16));
+        CUDA_TRY(ctx, cudaMemsetAsync(ctx->open_d.p, 0, sizeof(int) * (size_t)nf, ctx->st));
+        launch_first_feasible(P.nb, nf, P.nonneg, check, d_pf, d_pff, ctx->open_d.as<int>(), ctx->st);
         ctx->launches++;
         if (int rc = check_launch(ctx, "first_feasible")) return rc;
         int mism = 0;
+        std::vector<int> open(nf, 1);
         CUDA_TRY(ctx, cudaMemcpyAsync(&mism, ctx->mismatch_d.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+        if (check)
+            CUDA_TRY(ctx, cudaMemcpyAsync(open.data(), ctx->open_d.p, sizeof(int) * (size_t)nf,
+                                          cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
         for (int i = 0; i < nf; ++i) {
             CachedKey ck;
@@ -343,6 +352,7 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
             ck.tb = pb[i];
             ck.cut = pcut[i];
             ck.slot = slot[i];
+            ck.closed = check && !open[i];
             ctx->key_map[{km[i], kc[i]}] = (int)ctx->keys.size();
             ctx->keys.push_back(ck);
         }
@@ -377,6 +387,7 @@ struct CallOut {
     double objective = NAN;
     double iteration = NAN;
     int64_t visits = 0, visits_unpruned = 0;
+    double bound = INFINITY;     // the objective bound the call ran with
     std::vector<int32_t> lo, hi, dev;
     std::vector<double> tf, tb;
     std::vector<int64_t> mem;
@@ -399,6 +410,8 @@ constexpr int64_t OFF_MAX = (int64_t)SPILL_BIT - 1;
 // history cells per chunk: the shared history spill pool is sized from them
 // (one entry per cell at first) and must stay within OFF_MAX
 constexpr int64_t CHUNK_HIST_CELLS = int64_t(1) << 30;
+// objective bound (dp.cu) only for batches of at least this many unpruned visits
+constexpr double BOUND_MIN_VISITS = 2e10;
 
 // Runs one batch of DP calls whose buffers fit; fills outs[orig] for each.
 static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::vector<int> &idx,
@@ -453,7 +466,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         cd.hist_off = hist_cells;
         cd.orig = order[i];
         cd.pad = 0;
-        cd.U = ctx->bb_U.empty() ? INFINITY : ctx->bb_U[order[i]];
+        cd.U = INFINITY;
         const int64_t cells = (int64_t)cd.A * cd.B;
         val_cells += cells;
         hist_cells += cells * cd.S;
@@ -472,6 +485,88 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
 
     const size_t nk = ctx->keys.size();
     DPBatch bt{};
+    bt.nb = nb;
+    bt.n_calls = n;
+    bt.calls = ctx->calls_d.as<CallDesc>();
+    bt.keyidx = ctx->keyidx_d.as<int16_t>();
+    bt.key_tf = (const double *const *)ctx->key_ptrs.p;
+    bt.key_tb = ((const double *const *)ctx->key_ptrs.p) + nk;
+    bt.key_cut = ((const double *const *)ctx->key_ptrs.p) + 2 * nk;
+    bt.key_ffb = ((const int32_t *const *)ctx->key_ptrs.p) + 3 * nk;
+    bt.beta = P.beta;
+    bt.batch_size = BS;
+    bt.mono_skip = ctx->mono_skip ? 1 : 0;
+    bt.num_nodes = P.num_nodes;
+    bt.dpn = P.dpn;
+
+    // ---- objective bound (dp.cu): only with non-negative times, no cost
+    // table and suffix-closed feasibility in every key of the batch.  A call's
+    // U is the DP objective of its (S, D, R, MB/2) partner's optimal plan
+    // under this call's shares (run_calls_impl runs the partners first), or the
+    // explicit ctx->bb_U (measurement hook).
+    bool bounded = false;
+    if (!ctx->has_cost_table && ctx->mono_skip && (!ctx->bb_U.empty() || !ctx->bb_partner.empty())) {
+        bool closed = true;
+        for (auto &k : want) closed = closed && ctx->keys[ctx->key_map[k]].closed;
+        if (closed) {
+            std::vector<int32_t> pos, seg_off, slo, shi, sdev;
+            for (int i = 0; i < n; ++i) {
+                const int o = order[i];
+                if (!ctx->bb_U.empty()) cds[i].U = ctx->bb_U[o];
+                const int p = ctx->bb_partner.empty() ? -1 : ctx->bb_partner[o];
+                if (p < 0 || !outs[p].feasible || (int)outs[p].lo.size() != cds[i].S) continue;
+                pos.push_back(i);
+                seg_off.push_back((int32_t)slo.size());
+                slo.insert(slo.end(), outs[p].lo.begin(), outs[p].lo.end());
+                shi.insert(shi.end(), outs[p].hi.begin(), outs[p].hi.end());
+                sdev.insert(sdev.end(), outs[p].dev.begin(), outs[p].dev.end());
+            }
+            const int nbd = (int)pos.size();
+            if (nbd > 0) {
+                const size_t ns = slo.size();
+                CUDA_TRY(ctx, ctx->bound_d.ensure(4 * (2 * (size_t)nbd + 3 * ns) + 8 * (size_t)nbd + 64));
+                char *bb = ctx->bound_d.as<char>();
+                double *d_U = (double *)bb;
+                int32_t *d_pos = (int32_t *)(bb + 8 * (size_t)nbd);
+                int32_t *d_so = d_pos + nbd, *d_lo = d_so + nbd, *d_hi = d_lo + ns, *d_dv = d_hi + ns;
+                CUDA_TRY(ctx, cudaMemcpyAsync(d_pos, pos.data(), 4 * (size_t)nbd, cudaMemcpyHostToDevice, ctx->st));
+                CUDA_TRY(ctx, cudaMemcpyAsync(d_so, seg_off.data(), 4 * (size_t)nbd, cudaMemcpyHostToDevice, ctx->st));
+                CUDA_TRY(ctx, cudaMemcpyAsync(d_lo, slo.data(), 4 * ns, cudaMemcpyHostToDevice, ctx->st));
+                CUDA_TRY(ctx, cudaMemcpyAsync(d_hi, shi.data(), 4 * ns, cudaMemcpyHostToDevice, ctx->st));
+                CUDA_TRY(ctx, cudaMemcpyAsync(d_dv, sdev.data(), 4 * ns, cudaMemcpyHostToDevice, ctx->st));
+                launch_plan_bound(bt, nbd, d_pos, d_so, d_lo, d_hi, d_dv, d_U, ctx->derived, ctx->st);
+                ctx->launches++;
+                if (int rc = check_launch(ctx, "plan_bound")) return rc;
+                std::vector<double> U(nbd);
+                CUDA_TRY(ctx, cudaMemcpyAsync(U.data(), d_U, 8 * (size_t)nbd, cudaMemcpyDeviceToHost, ctx->st));
+                CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+                for (int t = 0; t < nbd; ++t) cds[pos[t]].U = std::min(cds[pos[t]].U, U[t]);
+            }
+            // calls still unbounded (no partner, or an infeasible one): a greedy plan
+            std::vector<int32_t> gpos;
+            for (int i = 0; i < n; ++i)
+                if (!(cds[i].U < INFINITY) && ctx->bb_U.empty()) gpos.push_back(i);
+            const int ng = (int)gpos.size();
+            if (ng > 0 && getenv("PIPECUT_B200_NO_GREEDY") == nullptr) {
+                CUDA_TRY(ctx, ctx->bound_d.ensure(12 * (size_t)ng + 64));
+                double *d_U = ctx->bound_d.as<double>();
+                int32_t *d_pos = (int32_t *)(d_U + ng);
+                CUDA_TRY(ctx, cudaMemcpyAsync(d_pos, gpos.data(), 4 * (size_t)ng, cudaMemcpyHostToDevice, ctx->st));
+                launch_greedy_bound(bt, ng, d_pos, d_U, ctx->derived, ctx->st);
+                ctx->launches++;
+                if (int rc = check_launch(ctx, "greedy_bound")) return rc;
+                std::vector<double> U(ng);
+                CUDA_TRY(ctx, cudaMemcpyAsync(U.data(), d_U, 8 * (size_t)ng, cudaMemcpyDeviceToHost, ctx->st));
+                CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+                for (int t = 0; t < ng; ++t) cds[gpos[t]].U = U[t];
+            }
+            for (int i = 0; i < n; ++i) bounded = bounded || cds[i].U < INFINITY;
+            if (bounded) {
+                for (int i = 0; i < n; ++i) ctx->bounded_calls += cds[i].U < INFINITY;
+                CUDA_TRY(ctx, cudaMemcpyAsync(ctx->calls_d.p, cds.data(), sizeof(CallDesc) * n, cudaMemcpyHostToDevice, ctx->st));
+            }
+        }
+    }
     float dp_ms = 0;
     bool first_pass = true;
     int vcap = 8, hcap = 4;     // pool entries reserved per cell (grown on overflow)
@@ -523,6 +618,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.key_cut = ((const double *const *)ctx->key_ptrs.p) + 2 * nk;
         bt.key_ffb = ((const int32_t *const *)ctx->key_ptrs.p) + 3 * nk;
         bt.beta = P.beta;
+        bt.batch_size = BS;
         bt.mono_skip = ctx->mono_skip ? 1 : 0;
         bt.num_nodes = P.num_nodes;
         bt.dpn = P.dpn;
@@ -551,6 +647,15 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.vspill_used = used + 3 * (size_t)n;
         bt.hspill_used = used + 3 * (size_t)n + 2;
         bt.hist_cells = hist_cells;
+        bt.bounded = bounded ? 1 : 0;
+        int64_t *d_colpre = nullptr;
+        if (bounded) {
+            CUDA_TRY(ctx, ctx->reach_d.ensure(2 * 4 * (size_t)val_cells + 8 * (size_t)(n + 1) + 64));
+            bt.reach_pre[0] = ctx->reach_d.as<int32_t>();
+            bt.reach_pre[1] = bt.reach_pre[0] + val_cells;
+            d_colpre = (int64_t *)(((uintptr_t)(bt.reach_pre[1] + val_cells) + 15) & ~uintptr_t(15));
+            CUDA_TRY(ctx, cudaMemcpyAsync(d_colpre, col_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
+        }
         CUDA_TRY(ctx, cudaMemsetAsync(ob, 0, 64 + 3 * sizeof(unsigned long long) * (size_t)n + 64, ctx->st));
         CUDA_TRY(ctx, ctx->counters_d.ensure((8 + FMAX + 3 * WORK_SLOTS) * sizeof(unsigned long long)));
         bt.counters = ctx->counters_d.as<unsigned long long>();
@@ -589,6 +694,10 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, ctx->st);
             ++launches;
             ctx->launches++;
+            if (bounded && s < maxS) {
+                launch_reach_prefix(bt, s, n_active, col_prefix[n_active], d_colpre, ctx->st);
+                ctx->launches++;
+            }
             if (cut)
                 ctx->launches += launch_prune_cut(bt, s, n_active, row_prefix[n_active], col_prefix[n_active],
                                                   cut_rows, cut_cols, row_e, ctx->st);
@@ -653,6 +762,9 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->st));
     }
     ctx->last_dp_ms += dp_ms;
+    if (getenv("PIPECUT_B200_BOUND_DEBUG"))
+        fprintf(stderr, "[pipecut_b200] chunk: %d calls, MB %d..%d, bounded %d, dp %.1f ms\n", n,
+                cds[0].MB, cds[n - 1].MB, (int)bounded, dp_ms);
 
     // ---- visits per (call, level)
     std::vector<int64_t> level_off(n + 1, 0), row_prefix(n + 1, 0);
@@ -696,6 +808,15 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     CUDA_TRY(ctx, cudaMemcpyAsync(feas.data(), ctx->feasible_d.p, sizeof(int32_t) * calls.size(), cudaMemcpyDeviceToHost, ctx->st));
     CUDA_TRY(ctx, cudaMemcpyAsync(objs.data(), ctx->objective_d.p, sizeof(double) * calls.size(), cudaMemcpyDeviceToHost, ctx->st));
     CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    // a bound below the optimum leaves the final cell with no entry although
+    // the reference holds it non-empty (k_backtrack: -1); a partner plan cannot
+    // do that, but such calls are re-run unbounded rather than trusted
+    std::vector<int> retry;
+    for (int i = 0; i < n; ++i)
+        if (feas[cds[i].orig] < 0) {
+            feas[cds[i].orig] = 0;
+            retry.push_back(cds[i].orig);
+        }
 
     // ---- stage records + simulation for feasible calls
     std::vector<int32_t> qlo, qhi, qck, poff, pS, pR, pMB;
@@ -797,6 +918,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         out.visits = 0;
         for (auto v : out.level_sums) out.visits += v;
         out.visits_unpruned = (int64_t)cd.S * tri_sum(cd.A) * tri_sum(cd.B);
+        out.bound = cd.U;
         out.feasible = feas[o];
         out.lo.clear(); out.hi.clear(); out.dev.clear(); out.tf.clear(); out.tb.clear(); out.mem.clear();
         if (feas[o]) {
@@ -814,11 +936,26 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             }
         }
     }
+    if (getenv("PIPECUT_B200_BOUND_DEBUG"))
+        for (int i = 0; i < n; ++i) {
+            const CallOut &o = outs[cds[i].orig];
+            if (o.feasible)
+                fprintf(stderr, "[pipecut_b200]   S %d D %d R %d MB %d: U/opt %.4f\n", cds[i].S,
+                        cds[i].D, cds[i].R, cds[i].MB, o.bound / o.objective);
+        }
     ctx->last_calls = cds;
     ctx->last_batch = bt;
     ctx->last_pruning = pruning;
     ctx->last_pos.assign(calls.size(), -1);
     for (int i = 0; i < n; ++i) ctx->last_pos[cds[i].orig] = i;
+    if (!retry.empty()) {
+        for (int o : retry) {
+            if (!ctx->bb_partner.empty()) ctx->bb_partner[o] = -1;
+            if (!ctx->bb_U.empty()) ctx->bb_U[o] = INFINITY;
+        }
+        ctx->bound_reruns += (int64_t)retry.size();
+        return run_chunk(ctx, calls, retry, BS, pruning, want_iter, outs);
+    }
     return PC_OK;
 }
 
@@ -842,23 +979,62 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const size_t cap = free_b / 2;
+    // Objective bound (dp.cu): the calls run in waves of equal MB, ascending;
+    // a call's partner is the (S, D, R, MB/2) call of the previous wave, whose
+    // optimal plan -- still a valid plan at half the share: memory only shrinks
+    // -- bounds this call's optimum (run_chunk).  Results are the same in any
+    // order; PIPECUT_B200_NO_BOUND=1 turns the bound off.
+    // Small batches skip it: the waves' extra launches and the greedy plans
+    // cost more than the bound saves below ~2e10 closed-form visits (r2h sweep).
+    double batch_visits = 0;
+    for (auto &c : calls) {
+        const double A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
+        batch_visits += (double)c.S * A * (A + 1) / 2 * B * (B + 1) / 2;
+    }
+    // (PIPECUT_B200_BOUND_MIN_VISITS overrides the size floor: the parity suite
+    // runs once with 0 so every eligible batch of its families is bounded)
+    const char *floor_env = getenv("PIPECUT_B200_BOUND_MIN_VISITS");
+    const double min_visits = floor_env ? atof(floor_env) : BOUND_MIN_VISITS;
+    const bool bound_ok = !ctx->has_cost_table && ctx->mono_skip && ctx->bb_U.empty() &&
+                          batch_visits >= min_visits &&
+                          getenv("PIPECUT_B200_NO_BOUND") == nullptr;
+    std::vector<int> seq(calls.size());
+    for (size_t i = 0; i < calls.size(); ++i) seq[i] = (int)i;
+    ctx->bb_partner.clear();
+    ctx->bounded_calls = 0;
+    ctx->bound_reruns = 0;
+    if (bound_ok) {
+        std::map<std::array<int, 4>, int> where;
+        for (size_t i = 0; i < calls.size(); ++i)
+            where[std::array<int, 4>{calls[i].S, calls[i].D, calls[i].R, calls[i].MB}] = (int)i;
+        ctx->bb_partner.assign(calls.size(), -1);
+        for (size_t i = 0; i < calls.size(); ++i) {
+            const pc_call &c = calls[i];
+            if (c.MB % 2) continue;
+            auto it = where.find(std::array<int, 4>{c.S, c.D, c.R, c.MB / 2});
+            if (it != where.end()) ctx->bb_partner[i] = it->second;
+        }
+        std::stable_sort(seq.begin(), seq.end(),
+                         [&](int a, int b) { return calls[a].MB < calls[b].MB; });
+    }
     std::vector<int> cur;
     size_t cur_bytes = 0;
     int64_t cur_hist = 0;
     *n_chunks = 0;
-    for (size_t i = 0; i < calls.size(); ++i) {
+    for (int i : seq) {
         const pc_call &c = calls[i];
         const int64_t A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
         const size_t bytes = (size_t)A * B * (2 * (5 + 16 * 12) + (size_t)c.S * (5 + 4 * 5));
         const int64_t hist = A * B * c.S;
-        if (!cur.empty() && (cur_bytes + bytes > cap || cur_hist + hist > CHUNK_HIST_CELLS)) {
+        const bool new_wave = bound_ok && !cur.empty() && calls[cur.back()].MB != c.MB;
+        if (!cur.empty() && (new_wave || cur_bytes + bytes > cap || cur_hist + hist > CHUNK_HIST_CELLS)) {
             if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
             ++*n_chunks;
             cur.clear();
             cur_bytes = 0;
             cur_hist = 0;
         }
-        cur.push_back((int)i);
+        cur.push_back(i);
         cur_bytes += bytes;
         cur_hist += hist;
     }
@@ -1006,12 +1182,14 @@ extern "C" int pc_run_calls(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_
     return PC_OK;
 }
 
-// Budget crossing inside call `index` of the last pc_run_calls (single chunk).
+// Budget crossing inside call `index` of the last pc_run_calls.  Only the
+// last chunk's flags are kept: -2 when the call ran in an earlier chunk (the
+// caller re-runs it alone and asks again).
 extern "C" int pc_last_crossing(pc_ctx *ctx, int32_t index, int64_t visits_before, int64_t budget,
                                 int64_t *visits_at_cross) {
     int64_t r = crossing_in_call(ctx, index, visits_before, budget);
     *visits_at_cross = r;
-    return r >= -1 ? PC_OK : fail(ctx, PC_ERR_INVALID, "call not in the last batch");
+    return r >= -2 ? PC_OK : fail(ctx, PC_ERR_CUDA, "reading the visit flags failed");
 }
 
 extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, int32_t disable_pruning,

@@ -178,6 +178,7 @@ struct DPBatch {
     const double *const *key_cut;
     const int32_t *const *key_ffb;  // per key: first feasible lo for each hi
     double beta;
+    int64_t batch_size;             // BS of every call of the batch
     int num_nodes, dpn;
     int mono_skip;                  // task times >= 0: t_fwd(b', b) non-increasing in b' (the
                                     // prefix skip) and the span_mark sign-bit encoding
@@ -188,6 +189,10 @@ struct DPBatch {
     // region (exact-size allocation by one atomic per cell)
     uint8_t *val_cnt[2];
     uint32_t *val_off[2];
+    // bounded batches: per (call, column) inclusive prefix count over b of the
+    // cells the reference holds non-empty (count > 0 or CNT_REACH)
+    int32_t *reach_pre[2];
+    int bounded;                    // some call of the batch has a finite U
     double *pool_tf[2];
     double *pool_tb[2];
     unsigned long long *vpool_used[2];  // [n_calls] per parity
@@ -215,6 +220,13 @@ constexpr uint32_t SPILL_BIT = 0x80000000u;
 // count byte: bits 0-6 entries, bit 7 saw_zero_share
 constexpr uint8_t CNT_MASK = 0x7f;
 constexpr uint8_t CNT_ZERO = 0x80;
+// count value of a cell the reference holds non-empty whose every entry the
+// objective bound dropped (dp.cu: bound); FMAX < CNT_REACH, so never a count
+constexpr uint8_t CNT_REACH = 0x7f;
+__host__ __device__ inline int cnt_entries(uint8_t v) {
+    const int c = v & CNT_MASK;
+    return c == CNT_REACH ? 0 : c;
+}
 
 // packed back-pointer (bp, dp, idx): lexicographic order == integer order
 __host__ __device__ inline uint32_t pack_key(uint32_t bp, uint32_t dp, uint32_t idx) {
@@ -235,8 +247,17 @@ void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_
                            const int32_t *keys_ckpt, const double *raw_tf, const double *raw_tb,
                            double *const *tf, double *const *tb, double *const *cut,
                            int derived, int *mismatch, cudaStream_t st);
-void launch_first_feasible(int nb, int n_keys, int nonneg, const double *const *tf,
-                           int32_t *const *ffb, cudaStream_t st);
+void launch_first_feasible(int nb, int n_keys, int nonneg, int check, const double *const *tf,
+                           int32_t *const *ffb, int *open, cudaStream_t st);
+// dp.cu: objective bound of a batch's calls from a plan of each (the optimum of
+// its (S, D, R, MB/2) partner), and the non-empty prefix counts per level
+void launch_plan_bound(const DPBatch &b, int n, const int32_t *pos, const int32_t *seg_off,
+                       const int32_t *lo, const int32_t *hi, const int32_t *dev, double *U,
+                       bool derived, cudaStream_t st);
+void launch_reach_prefix(const DPBatch &b, int s, int n_active, int64_t n_cols,
+                         const int64_t *col_prefix, cudaStream_t st);
+void launch_greedy_bound(const DPBatch &b, int n, const int32_t *pos, double *U, bool derived,
+                         cudaStream_t st);
 void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
                             const int64_t *m, const int32_t *ckpt, double *tf, double *tb,
                             int64_t *mem, cudaStream_t st);

@@ -56,6 +56,7 @@ struct CachedKey {
     double *tb = nullptr;    // [tri] or null when derived as beta * tf
     double *cut = nullptr;   // [2][nb+1], then ffb int32 [nb+1]
     int slot = -1;           // slot in the key arena
+    bool closed = false;     // feasible lo form a suffix [ffb, hi) for every hi
 };
 
 }  // namespace pcb
@@ -110,6 +111,12 @@ struct pc_ctx {
     std::vector<CallDesc> last_calls;   // sorted order
     std::vector<int> last_pos;          // orig -> sorted position
     std::vector<double> bb_U;           // per call of the current run_calls_impl (bound)
+    std::vector<int> bb_partner;        // per call: call whose optimum bounds it, or -1
+    const void *bb_outs = nullptr;      // the CallOut list those indices refer to
+    DBuf bound_d;                       // plan-bound inputs / outputs
+    DBuf reach_d;                       // non-empty prefix counts (two levels)
+    DBuf open_d;                        // first_feasible: per fresh key, not suffix-closed
+    int64_t bounded_calls = 0, bound_reruns = 0;   // diagnostics of the last run
     std::vector<std::vector<int64_t>> last_level_sums;  // by orig
     int last_pruning = 1;
     int last_FL = 4;

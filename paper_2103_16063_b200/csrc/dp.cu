@@ -217,12 +217,17 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
     const WarpFront F = warp_front(w);
     // Objective bound (CallDesc.U, finite only with non-negative times and no
     // cost table): every completion of an entry (x, y) of this cell costs at
-    // least max(x, lbf) + max(y, lbb) -- the S - s stages still to come cover
-    // [b, nb) at shares >= the share of the most devices one of them can get,
-    // so their largest raw time is >= t(b, nb; that share) / (S - s) (times
-    // are monotone in the share; the factor absorbs the fold's rounding).
-    // Entries above U cannot lead to a plan at or below U, so they are dropped;
-    // level S keeps only the final cell (nb, D).
+    // least max(x, lbf) + max(y, lbb), lbf a lower bound on the largest raw
+    // forward time of the S - s stages still to come over [b, nb) with the
+    // D - d devices left.  Stage i with dev_i devices runs at share
+    // m_i = BS // (q dev_i), q = MB R, so its raw time is ~ m_i w_i with w_i
+    // its time per unit share; T >= m_i w_i for all i gives
+    //   T >= sum w_i / sum 1/m_i,   sum 1/m_i <= q (D - d) / (BS - q devmax + 1)
+    // (floor(x/y) >= (x - y + 1)/y, dev_i <= devmax), and also
+    //   T >= t(b, nb; m(devmax)) / (S - s)          (times monotone in m);
+    // sum w_i ~ t(b, nb; m(devmax)) / m(devmax).  The factor (1 - 1e-9)
+    // absorbs the folds' rounding.  Entries above U cannot lead to a plan at or
+    // below U, so they are dropped; level S keeps only the final cell (nb, D).
     const double U = cd.U;
     const bool bounded = U < INFINITY;
     double lbf = 0.0, lbb = 0.0;
@@ -234,7 +239,12 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
             const int kx = keyidx[devmax];
             if (kx >= 0) {
                 const int64_t o = hm_idx(b, nb);
-                const double k = (1.0 - 1e-9) / (double)(cd.S - s);
+                const int64_t q = (int64_t)cd.MB * cd.R;
+                const int64_t mx = B.batch_size / (q * devmax);
+                const double k1 = 1.0 / (double)(cd.S - s);
+                const double k2 = (double)(B.batch_size - q * devmax + 1) /
+                                  ((double)(q * (cd.D - d)) * (double)mx);
+                const double k = (1.0 - 1e-9) * (k1 > k2 ? k1 : k2);
                 lbf = __dmul_rn(fabs(B.key_tf[kx][o]), k);
                 lbb = DERIVED ? __dmul_rn(beta, lbf) : __dmul_rn(fabs(B.key_tb[kx][o]), k);
             }
@@ -246,6 +256,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
     int n = 0;
     bool ovf = false;
     bool zero = false;
+    bool reach = false;    // bounded calls: the reference holds this cell non-empty
     uint32_t n_pairs = 0, n_cands = 0, n_ins = 0;
     uint32_t n_corner = 0, n_win = 0, n_rounds = 0, n_iters = 0;
 
@@ -257,6 +268,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         } else {
             const double tf = B.key_tf[kk][row];
             if (span_ok(tf, B.mono_skip)) {
+                reach = true;
                 double tfc = tf;
                 if (b < nb) tfc = __dadd_rn(tf, B.key_cut[kk][inter_d * (nb + 1) + b]);
                 const double tbc = DERIVED ? __dmul_rn(beta, tf) : B.key_tb[kk][row];
@@ -276,6 +288,26 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         // is order-independent (see top), so this order is as good as the
         // reference's.
         const int base = s - 1;
+        if (bounded) {
+            // the reference's emptiness and zero-share flag of this cell from
+            // the previous level's non-empty prefix counts: some non-empty
+            // (b' < b, d') with m == 0, and some with a feasible span (b', b)
+            // -- b' >= first feasible lo, feasibility being suffix-closed in
+            // b' for every key of a bounded batch (api.cu checks it)
+            const int32_t *rp = B.reach_pre[prv] + cd.val_off;
+            bool zl = false, rl = false;
+            for (int dp = base + lane; dp < d; dp += 32) {
+                const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
+                const int32_t upto = col[b - 1];
+                if (upto == 0) continue;
+                const int kk = keyidx[d - dp];
+                if (kk < 0) { zl = true; continue; }
+                const int x = max(base, B.key_ffb[kk][b]);
+                if (x <= b - 1 && upto > (x > base ? col[x - 1] : 0)) rl = true;
+            }
+            zero = __any_sync(0xffffffffu, zl);
+            reach = __any_sync(0xffffffffu, rl);
+        }
         const uint8_t *pcnt = B.val_cnt[prv] + cd.val_off;
         const uint32_t *poff = B.val_off[prv] + cd.val_off;
         const double *qtf = B.pool_tf[prv] + cd.vpool_base;
@@ -317,7 +349,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
             auto chunk = [&](int top, int ex_lo, int ex_hi) {
                 const int bp = top - lane;
                 int cnt = (bp > lim && bp >= bp_lo && (bp < ex_lo || bp > ex_hi))
-                              ? (ccol[bp] & CNT_MASK) : 0;
+                              ? cnt_entries(ccol[bp]) : 0;
                 double tfc = 0.0, tbc = 0.0;
                 int wlo = 0, whi = -1;
                 const double *etf = qtf, *etb = qtb;
@@ -529,7 +561,8 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         }
     }
     if (lane == 0) {
-        const uint8_t byte = (uint8_t)n | (any_zero ? CNT_ZERO : 0);
+        const uint8_t cnt_byte = n > 0 ? (uint8_t)n : (bounded && reach ? CNT_REACH : 0);
+        const uint8_t byte = cnt_byte | (any_zero ? CNT_ZERO : 0);
         B.val_cnt[cur][vcell] = byte;
         B.hist_cnt[hcell] = byte;
         if (ovf) atomicOr(B.overflow, 1);
@@ -561,6 +594,217 @@ void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool
         k_dp_level<true><<<blocks, tpb, 0, st>>>(b, s, n_active);
     else
         k_dp_level<false><<<blocks, tpb, 0, st>>>(b, s, n_active);
+}
+
+// ---------------------------------------------------------------- bound: U from a plan
+// The objective the DP gives one complete path -- the plan (lo, hi, devices)
+// of each listed call -- with this batch's key tables: per stage the charged
+// times exactly as k_dp_level forms a candidate (raw span time, + cut(hi) at
+// the stage's end, + cut(lo) at its start, inter-node flags from the running
+// device count), max-folded from the level-0 entry (0, 0), then tf + tb.  Any
+// path is one of the DP's plans, so the result bounds the call's optimum.
+// One thread per call; +inf if a stage has a zero share or an infeasible span.
+template <bool DERIVED>
+__global__ void k_plan_bound(DPBatch Bt, int n, const int32_t *pos, const int32_t *seg_off,
+                             const int32_t *lo, const int32_t *hi, const int32_t *dev,
+                             double *U) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const CallDesc cd = Bt.calls[pos[t]];
+    const int16_t *keyidx = Bt.keyidx + cd.key_off;
+    const int nb = Bt.nb;
+    double mf = 0.0, mb = 0.0;
+    int cum = 0;
+    for (int k = 0; k < cd.S; ++k) {
+        const int q = seg_off[t] + k;
+        const int a = lo[q], z = hi[q], dv = dev[q];
+        const int prev = cum;
+        cum += dv;
+        const int kk = (dv >= 1 && dv <= cd.B) ? keyidx[dv] : -1;
+        if (kk < 0) { U[t] = INFINITY; return; }
+        const int64_t o = hm_idx(a, z);
+        const double tf = Bt.key_tf[kk][o];
+        if (!span_ok(tf, Bt.mono_skip)) { U[t] = INFINITY; return; }
+        double tfc = tf;
+        if (z < nb) {
+            const int inter = (Bt.num_nodes > 1 && cum % Bt.dpn == 0) ? 1 : 0;
+            tfc = __dadd_rn(tf, Bt.key_cut[kk][inter * (nb + 1) + z]);
+        }
+        double tbc = DERIVED ? __dmul_rn(Bt.beta, tf) : Bt.key_tb[kk][o];
+        if (a > 0) {
+            const int inter = (Bt.num_nodes > 1 && prev % Bt.dpn == 0) ? 1 : 0;
+            tbc = __dadd_rn(tbc, Bt.key_cut[kk][inter * (nb + 1) + a]);
+        }
+        mf = dmax_ref(mf, tfc);
+        mb = dmax_ref(mb, tbc);
+    }
+    U[t] = __dadd_rn(mf, mb);
+}
+
+void launch_plan_bound(const DPBatch &b, int n, const int32_t *pos, const int32_t *seg_off,
+                       const int32_t *lo, const int32_t *hi, const int32_t *dev, double *U,
+                       bool derived, cudaStream_t st) {
+    if (n <= 0) return;
+    if (derived)
+        k_plan_bound<true><<<(n + 127) / 128, 128, 0, st>>>(b, n, pos, seg_off, lo, hi, dev, U);
+    else
+        k_plan_bound<false><<<(n + 127) / 128, 128, 0, st>>>(b, n, pos, seg_off, lo, hi, dev, U);
+}
+
+// ---------------------------------------------------------------- bound: greedy plan
+// Calls without a partner plan (the first MB wave, or an infeasible partner):
+// a plan from bisection on a stage cost T.  Stage i gets D / S devices, one
+// more for the first D % S stages (S stages, D devices, each <= B).  pack(T)
+// walks the blocks left to right: stage i ends at the largest hi -- leaving a
+// block for each later stage, the last stage ending at nb -- whose span fits
+// and whose charged forward + backward time is <= T, scanning hi upward until
+// the raw forward time alone passes T (raw times grow with the span).  The
+// DP objective of the plan packed at the smallest T found (max-folded charged
+// times as in k_plan_bound) bounds the optimum; +inf if nothing packs.  One
+// warp per call.
+template <bool DERIVED>
+__global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U) {
+    const int w = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const CallDesc cd = Bt.calls[pos[w]];
+    const int16_t *keyidx = Bt.keyidx + cd.key_off;
+    const int nb = Bt.nb, S = cd.S, D = cd.D;
+    const int q = D / S, r = D % S;
+    const int kq = keyidx[q], kq1 = r > 0 ? keyidx[q + 1] : kq;
+    if (kq < 0 || kq1 < 0) {
+        if (lane == 0) U[w] = INFINITY;
+        return;
+    }
+    // charged times of stage i = [lo, hi) (k_plan_bound's arithmetic)
+    auto charged = [&](int i, int lo, int hi, double &tfc, double &tbc, double &raw) -> bool {
+        const int kk = i < r ? kq1 : kq;
+        const int before = i * q + min(i, r), after = before + q + (i < r ? 1 : 0);
+        const int64_t o = hm_idx(lo, hi);
+        const double tf = Bt.key_tf[kk][o];
+        raw = fabs(tf);
+        tfc = tf;
+        if (hi < nb) {
+            const int inter = (Bt.num_nodes > 1 && after % Bt.dpn == 0) ? 1 : 0;
+            tfc = __dadd_rn(tf, Bt.key_cut[kk][inter * (nb + 1) + hi]);
+        }
+        tbc = DERIVED ? __dmul_rn(Bt.beta, tf) : Bt.key_tb[kk][o];
+        if (lo > 0) {
+            const int inter = (Bt.num_nodes > 1 && before % Bt.dpn == 0) ? 1 : 0;
+            tbc = __dadd_rn(tbc, Bt.key_cut[kk][inter * (nb + 1) + lo]);
+        }
+        return span_ok(tf, Bt.mono_skip);
+    };
+    // pack(T): true if S stages cover [0, nb); with `eval`, the plan's objective
+    auto pack = [&](double T, bool eval, double &obj) -> bool {
+        int lo = 0;
+        double mf = 0.0, mb = 0.0;
+        for (int i = 0; i < S; ++i) {
+            const int last = nb - (S - 1 - i);
+            int best = -1;
+            if (i == S - 1) {
+                double tfc, tbc, raw;
+                const bool ok = charged(i, lo, nb, tfc, tbc, raw);
+                if (ok && __dadd_rn(tfc, tbc) <= T) best = nb;
+            } else {
+                for (int h0 = lo + 1; h0 <= last; h0 += 32) {
+                    const int h = h0 + lane;
+                    bool good = false, stop = false;
+                    if (h <= last) {
+                        double tfc, tbc, raw;
+                        const bool ok = charged(i, lo, h, tfc, tbc, raw);
+                        good = ok && __dadd_rn(tfc, tbc) <= T;
+                        stop = raw > T;
+                    }
+                    const uint32_t gm = __ballot_sync(0xffffffffu, good);
+                    if (gm) best = h0 + 31 - __clz(gm);
+                    if (__ballot_sync(0xffffffffu, stop)) break;
+                }
+            }
+            if (best < 0) return false;
+            if (eval) {
+                double tfc, tbc, raw;
+                charged(i, lo, best, tfc, tbc, raw);
+                mf = dmax_ref(mf, tfc);
+                mb = dmax_ref(mb, tbc);
+            }
+            lo = best;
+        }
+        obj = __dadd_rn(mf, mb);
+        return true;
+    };
+    double obj = INFINITY, dummy;
+    // a T that packs: from the balanced estimate (1 + beta) t(0, nb) / S,
+    // doubling; then bisection down
+    const double total = fabs(Bt.key_tf[kq][hm_idx(0, nb)]);
+    double hiT = 1.5 * (1.0 + Bt.beta) * total / S + 1e-300;
+    int tries = 0;
+    while (!pack(hiT, false, dummy)) {
+        if (++tries > 8) {
+            if (lane == 0) U[w] = INFINITY;
+            return;
+        }
+        hiT *= 2.0;
+    }
+    double loT = tries ? 0.5 * hiT : 0.0;
+    for (int it = 0; it < 24; ++it) {
+        const double mid = 0.5 * (loT + hiT);
+        double dummy;
+        if (pack(mid, false, dummy)) hiT = mid; else loT = mid;
+    }
+    const bool ok = pack(hiT, true, obj);
+    if (lane == 0) U[w] = ok ? obj : INFINITY;
+}
+
+void launch_greedy_bound(const DPBatch &b, int n, const int32_t *pos, double *U, bool derived,
+                         cudaStream_t st) {
+    if (n <= 0) return;
+    const unsigned blocks = (unsigned)((n * 32 + 127) / 128);
+    if (derived)
+        k_greedy_bound<true><<<blocks, 128, 0, st>>>(b, n, pos, U);
+    else
+        k_greedy_bound<false><<<blocks, 128, 0, st>>>(b, n, pos, U);
+}
+
+// ---------------------------------------------------------------- bound: non-empty prefix
+// Bounded batches: per (call, d column) the inclusive prefix count over b of
+// the cells of level s the reference holds non-empty (count > 0 or CNT_REACH),
+// read by level s + 1 for its emptiness and zero-share flags.  One warp per
+// column, 32 cells per step.
+__global__ void k_reach_prefix(DPBatch Bt, int s, int n_active, const int64_t *col_prefix) {
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= col_prefix[n_active]) return;
+    int lo = 0, hi = n_active;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (col_prefix[mid] <= g) lo = mid; else hi = mid;
+    }
+    const CallDesc cd = Bt.calls[lo];
+    const int di = (int)(g - col_prefix[lo]);
+    const int cur = s & 1;
+    const uint8_t *vcol = Bt.val_cnt[cur] + cd.val_off + (int64_t)di * cd.A;
+    int32_t *pcol = Bt.reach_pre[cur] + cd.val_off + (int64_t)di * cd.A;
+    int32_t run = 0;
+    for (int b0 = 0; b0 < cd.A; b0 += 32) {
+        const int bi = b0 + lane;
+        const int v = bi < cd.A && (vcol[bi] & CNT_MASK) != 0 ? 1 : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (bi < cd.A) pcol[bi] = run + incl;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+void launch_reach_prefix(const DPBatch &b, int s, int n_active, int64_t n_cols,
+                         const int64_t *col_prefix, cudaStream_t st) {
+    if (n_cols > 0)
+        k_reach_prefix<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(b, s, n_active,
+                                                                             col_prefix);
 }
 
 // ---------------------------------------------------------------- pruning cut
@@ -773,10 +1017,13 @@ __global__ void k_backtrack(DPBatch Bt, int64_t batch_size, const int32_t *plan_
     const int64_t fcell = (int64_t)(cd.B - 1) * cd.A + (cd.A - 1);   // (nb, D)
     const int par = S & 1;
     const int64_t vcell = cd.val_off + fcell;
-    const int n = Bt.val_cnt[par][vcell] & CNT_MASK;
+    const uint8_t fb = Bt.val_cnt[par][vcell];
+    const int n = cnt_entries(fb);
     const int o = cd.orig;
     if (n == 0) {
-        feasible[o] = 0;
+        // non-empty for the reference but every entry above the bound: the
+        // bound was below the optimum (the host reruns the call unbounded)
+        feasible[o] = (fb & CNT_MASK) == CNT_REACH ? -1 : 0;
         return;
     }
     const uint32_t vo = Bt.val_off[par][vcell];

@@ -197,24 +197,53 @@ void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_
                                                   tf, tb, cut, derived, mismatch);
 }
 
-// First feasible lo of every hi (per key): the DP skips b' below it, which
-// are all infeasible by construction (no monotonicity assumed).
-__global__ void k_first_feasible(int nb, int n_keys, int nonneg, const double *const *tf,
-                                 int32_t *const *ffb) {
-    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= (int64_t)n_keys * (nb + 1)) return;
-    const int k = (int)(gid / (nb + 1));
-    const int hi = (int)(gid % (nb + 1));
+// First feasible lo >= 1 of every hi (per key; hi when none): the DP reads it
+// at levels s >= 2, whose predecessors are b' >= s - 1 >= 1, and skips the b'
+// below it, all infeasible by construction (no monotonicity assumed); level 1
+// reads the span from lo = 0 directly (that span's only input can be a small
+// model input, so it may fit where [1, hi) does not).  One warp per (key, hi)
+// row, 32 lo per ballot.  With `check` the whole row is read and open[k]
+// flagged when some lo above the first feasible one is infeasible
+// (feasibility not suffix-closed in lo >= 1): the DP's objective bound counts
+// non-empty predecessors by range and needs it closed.
+__global__ void k_first_feasible(int nb, int n_keys, int nonneg, int check,
+                                 const double *const *tf, int32_t *const *ffb, int *open) {
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= (int64_t)n_keys * (nb + 1)) return;
+    const int k = (int)(gw / (nb + 1));
+    const int hi = (int)(gw % (nb + 1));
     const double *row = tf[k] + hm_idx(0, hi);
-    int lo = 0;
-    while (lo < hi && !span_ok(row[lo], nonneg)) ++lo;
-    ffb[k][hi] = lo;
+    int first = hi;
+    bool gap = false;
+    for (int lo0 = 1; lo0 < hi; lo0 += 32) {
+        const int lo = lo0 + lane;
+        const bool in = lo < hi;
+        const bool ok = in && span_ok(row[lo], nonneg);
+        const uint32_t m = __ballot_sync(0xffffffffu, ok);
+        const uint32_t inr = __ballot_sync(0xffffffffu, in);
+        if (first == hi) {
+            if (m) {
+                const int f = __ffs(m) - 1;
+                first = lo0 + f;
+                if (!check) break;
+                gap = gap || ((~m & inr) >> f) != 0;
+            }
+        } else {
+            gap = gap || (~m & inr) != 0;
+        }
+    }
+    if (lane == 0) {
+        ffb[k][hi] = first;
+        if (check && gap) atomicOr(&open[k], 1);
+    }
 }
 
-void launch_first_feasible(int nb, int n_keys, int nonneg, const double *const *tf,
-                           int32_t *const *ffb, cudaStream_t st) {
-    const int64_t n = (int64_t)n_keys * (nb + 1);
-    k_first_feasible<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(nb, n_keys, nonneg, tf, ffb);
+void launch_first_feasible(int nb, int n_keys, int nonneg, int check, const double *const *tf,
+                           int32_t *const *ffb, int *open, cudaStream_t st) {
+    const int64_t n = (int64_t)n_keys * (nb + 1) * 32;
+    k_first_feasible<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(nb, n_keys, nonneg, check, tf,
+                                                                  ffb, open);
 }
 
 // ---------------------------------------------------------------- queries

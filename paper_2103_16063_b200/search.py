@@ -343,6 +343,20 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
                     batch_size)
 
 
+def crossing_visits(ctx, index, call, before, budget, batch_size, disable_pruning) -> int:
+    """Visits at the first cell past `budget` inside `call`, position `index`
+    of the last run_calls batch (stages.py:214-216); a call whose flags went
+    with an earlier chunk of that batch is run again alone."""
+    at = C.c_int64()
+    ctx.check(ctx.lib.pc_last_crossing(ctx.h, index, before, budget, C.byref(at)),
+              "pc_last_crossing")
+    if at.value < -1:
+        run_calls(ctx, [call], batch_size, disable_pruning, False)
+        ctx.check(ctx.lib.pc_last_crossing(ctx.h, 0, before, budget, C.byref(at)),
+                  "pc_last_crossing")
+    return int(at.value)
+
+
 def _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, group, dev, opts,
                     batch_size):
     """SearchBudgetExceeded with the exact visit count at the crossing cell,
@@ -352,15 +366,8 @@ def _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, gr
 
     v = np.zeros(1, np.float64)
     if owner[cross] == rank:
-        li = local_idx.index(cross)
-        at = C.c_int64()
-        ctx.check(ctx.lib.pc_last_crossing(ctx.h, li, before, int(opts.visit_budget),
-                                           C.byref(at)), "pc_last_crossing")
-        if at.value < -1:   # flags of an earlier chunk are gone: recompute that call
-            run_calls(ctx, [calls[cross]], batch_size, opts.disable_pruning, False)
-            ctx.check(ctx.lib.pc_last_crossing(ctx.h, 0, before, int(opts.visit_budget),
-                                               C.byref(at)), "pc_last_crossing")
-        v[0] = at.value
+        v[0] = crossing_visits(ctx, local_idx.index(cross), calls[cross], before,
+                               int(opts.visit_budget), batch_size, opts.disable_pruning)
     if world > 1:
         t = torch.from_numpy(v).to(dev)
         # owner[] holds ranks within `group`; broadcast's src is a global rank

@@ -214,10 +214,10 @@ def checked_form_stage(ctx, num_nodes: int, devices_per_node: int, batch_size: i
             v = int(batch.results[j]["visits"])
             counted += 1
             if budget is not None and visits + v > budget:
-                at = C.c_int64()
-                ctx.check(ctx.lib.pc_last_crossing(ctx.h, j, visits, int(budget), C.byref(at)),
-                          "pc_last_crossing")
-                raise SearchBudgetExceeded(int(at.value), int(budget))
+                from .search import crossing_visits
+                raise SearchBudgetExceeded(
+                    crossing_visits(ctx, j, calls[idx[j]], visits, int(budget), batch_size,
+                                    opts.disable_pruning), int(budget))
             visits += v
         best = None
         for j, i in enumerate(idx):
