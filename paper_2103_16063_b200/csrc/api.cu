@@ -979,11 +979,14 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const size_t cap = free_b / 2;
-    // Objective bound (dp.cu): the calls run in waves of equal MB, ascending;
-    // a call's partner is the (S, D, R, MB/2) call of the previous wave, whose
-    // optimal plan -- still a valid plan at half the share: memory only shrinks
-    // -- bounds this call's optimum (run_chunk).  Results are the same in any
-    // order; PIPECUT_B200_NO_BOUND=1 turns the bound off.
+    // Objective bound (dp.cu): every call of the batch gets U from a greedy
+    // plan (k_greedy_bound; within 1% of the optimum at the median on the C5
+    // chains).  PIPECUT_B200_BOUND_WAVES=1 instead runs the calls in waves of
+    // equal MB, ascending, and bounds a call by its (S, D, R, MB/2) partner's
+    // optimal plan -- still a valid plan at half the share: memory only
+    // shrinks -- measured slower (12 sequential batches: 1.43 s vs 1.21 s of DP
+    // on 4096 x 256, r2j).  Results are the same either way;
+    // PIPECUT_B200_NO_BOUND=1 turns the bound off.
     // Small batches skip it: the waves' extra launches and the greedy plans
     // cost more than the bound saves below ~2e10 closed-form visits (r2h sweep).
     double batch_visits = 0;
@@ -1003,7 +1006,9 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     ctx->bb_partner.clear();
     ctx->bounded_calls = 0;
     ctx->bound_reruns = 0;
-    if (bound_ok) {
+    const bool waves = bound_ok && getenv("PIPECUT_B200_BOUND_WAVES") != nullptr;
+    if (bound_ok && !waves) ctx->bb_partner.assign(calls.size(), -1);   // greedy bounds only
+    if (waves) {
         std::map<std::array<int, 4>, int> where;
         for (size_t i = 0; i < calls.size(); ++i)
             where[std::array<int, 4>{calls[i].S, calls[i].D, calls[i].R, calls[i].MB}] = (int)i;
@@ -1026,7 +1031,7 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
         const int64_t A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
         const size_t bytes = (size_t)A * B * (2 * (5 + 16 * 12) + (size_t)c.S * (5 + 4 * 5));
         const int64_t hist = A * B * c.S;
-        const bool new_wave = bound_ok && !cur.empty() && calls[cur.back()].MB != c.MB;
+        const bool new_wave = waves && !cur.empty() && calls[cur.back()].MB != c.MB;
         if (!cur.empty() && (new_wave || cur_bytes + bytes > cap || cur_hist + hist > CHUNK_HIST_CELLS)) {
             if (int rc = run_chunk(ctx, calls, cur, BS, pruning, want_iter, outs)) return rc;
             ++*n_chunks;
