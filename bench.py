@@ -193,6 +193,7 @@ class Arm:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         torch.cuda.set_device(self.local)
         if self.world > 1:
+            os.environ.setdefault("NCCL_DEBUG", "WARN")   # stdout carries only the JSON line
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
         self.dev = torch.device("cuda", self.local)
         from paper_2103_16063_b200 import _lib
@@ -305,7 +306,7 @@ def roofline(nb, D, world, calls_local, tims, dadd_peak, mix_peak, steps, sm_cou
 def run_ours(a):
     arm = Arm()
     import ctypes as C
-    from paper_2103_16063_b200.search import device_weights, enumerate_calls, lpt_shard
+    from paper_2103_16063_b200.search import enumerate_calls, lpt_shard, shard_weights
     from paper_2103_16063_b200.stages import bind_problem
     from paper_2103_16063_b200.workloads import c5_blockset, unpruned_visits
 
@@ -317,7 +318,7 @@ def run_ours(a):
     calls, _ = enumerate_calls(nodes, dpn, BS, nb)
     unpruned = unpruned_visits(nb, calls)
     bind_problem(ctx, bs)
-    owner = lpt_shard(nb, calls, world, device_weights(ctx, calls, BS) if world > 1 else None)
+    owner = lpt_shard(nb, calls, world, shard_weights(ctx, calls, BS, nb) if world > 1 else None)
     my_calls = [calls[i] for i in range(len(calls)) if owner[i] == rank]
     smc, ccmaj, ccmin = C.c_int32(), C.c_int32(), C.c_int32()
     ctx.check(ctx.lib.pc_device_info(ctx.h, C.byref(smc), C.byref(ccmaj), C.byref(ccmin)), "info")

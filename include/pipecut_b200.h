@@ -25,7 +25,8 @@
  *   pc_simulate         simulate (simulate.py:79-179)
  *   pc_call_weights     sharding weights of form_stage's call enumeration
  *                       (stages.py:389-403); no reference counterpart
- *   pc_ctx_*, pc_device_info, pc_reset_cache, pc_timer_*, pc_measure_fp64_peak
+ *   pc_ctx_*, pc_device_info, pc_reset_cache, pc_timer_*, pc_measure_fp64_peak,
+ *   pc_measure_dadd_peak, pc_bound_info
  *                       library plumbing and measurement; no reference
  *                       counterpart
  *
@@ -292,6 +293,11 @@ int pc_timer_stop(pc_ctx *ctx, double *ms);
 /* Measured fp64 add/max issue rate of this device (Gop/s), the roofline
  * denominator of the DP kernel (no tensor-core roof: min/max/add recurrence). */
 int pc_measure_fp64_peak(pc_ctx *ctx, double *gops);
+
+/* Objective-bound diagnostics of the last pc_run_calls / pc_form_stage* call:
+ * calls that ran with a finite bound, and calls re-run unbounded because
+ * their bound was below the optimum.  No reference counterpart. */
+int pc_bound_info(pc_ctx *ctx, int64_t *bounded_calls, int64_t *reruns);
 
 /* Measured pure-DADD rate of this device (Gop/s): the fp64 pipe's peak op rate,
  * the denominator of the DP kernel's algorithmic-fp64 roofline. */

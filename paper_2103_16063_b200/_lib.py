@@ -82,10 +82,12 @@ def load():
         lib.pc_timer_stop.argtypes = [C.c_void_p, P(C.c_double)]
         lib.pc_measure_fp64_peak.argtypes = [C.c_void_p, P(C.c_double)]
         lib.pc_measure_dadd_peak.argtypes = [C.c_void_p, P(C.c_double)]
+        lib.pc_bound_info.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64)]
         for name in ("pc_ctx_create", "pc_device_info", "pc_set_problem", "pc_profile_spans",
                      "pc_form_stage_dp", "pc_run_calls", "pc_last_crossing", "pc_form_stage",
                      "pc_reset_cache", "pc_timer_start", "pc_timer_stop",
-                     "pc_measure_fp64_peak", "pc_measure_dadd_peak", "pc_partition_blocks",
+                     "pc_measure_fp64_peak", "pc_measure_dadd_peak", "pc_bound_info",
+                     "pc_partition_blocks",
                      "pc_set_overrides", "pc_brute_force", "pc_check_plan", "pc_simulate",
                      "pc_call_weights"):
             getattr(lib, name).restype = C.c_int
@@ -96,7 +98,8 @@ def load():
 EXPORTS = ("pc_ctx_create", "pc_ctx_destroy", "pc_last_error", "pc_device_info",
            "pc_set_problem", "pc_profile_spans", "pc_form_stage_dp", "pc_run_calls",
            "pc_last_crossing", "pc_form_stage", "pc_reset_cache", "pc_timer_start",
-           "pc_timer_stop", "pc_measure_fp64_peak", "pc_measure_dadd_peak", "pc_partition_blocks",
+           "pc_timer_stop", "pc_measure_fp64_peak", "pc_measure_dadd_peak", "pc_bound_info",
+           "pc_partition_blocks",
            "pc_set_overrides", "pc_brute_force", "pc_check_plan", "pc_simulate", "pc_call_weights")
 
 

@@ -560,6 +560,10 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
                 CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
                 for (int t = 0; t < ng; ++t) cds[gpos[t]].U = U[t];
             }
+            // PIPECUT_B200_BOUND_SCALE (tests only): scale U, below 1 forcing the
+            // too-tight path (final cell empty, the call re-run unbounded)
+            if (const char *sc = getenv("PIPECUT_B200_BOUND_SCALE"))
+                for (int i = 0; i < n; ++i) cds[i].U *= atof(sc);
             for (int i = 0; i < n; ++i) bounded = bounded || cds[i].U < INFINITY;
             if (bounded) {
                 for (int i = 0; i < n; ++i) ctx->bounded_calls += cds[i].U < INFINITY;
@@ -1004,8 +1008,6 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     std::vector<int> seq(calls.size());
     for (size_t i = 0; i < calls.size(); ++i) seq[i] = (int)i;
     ctx->bb_partner.clear();
-    ctx->bounded_calls = 0;
-    ctx->bound_reruns = 0;
     const bool waves = bound_ok && getenv("PIPECUT_B200_BOUND_WAVES") != nullptr;
     if (bound_ok && !waves) ctx->bb_partner.assign(calls.size(), -1);   // greedy bounds only
     if (waves) {
@@ -1143,6 +1145,7 @@ static void fill_stats(pc_ctx *ctx, pc_stats *stats, int64_t visits, int64_t cal
 extern "C" int pc_form_stage_dp(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_size, int32_t R,
                                 int32_t MB, int32_t disable_pruning, int64_t visit_budget,
                                 pc_plan *plan, pc_stats *stats) {
+    ctx->bounded_calls = ctx->bound_reruns = 0;
     std::vector<pc_call> calls = {{S, D, R, MB}};
     if (plan && S > plan->cap_stages && S <= ctx->nb) return fail(ctx, PC_ERR_CAPACITY, "plan capacity");
     std::vector<CallOut> outs;
@@ -1164,6 +1167,7 @@ extern "C" int pc_form_stage_dp(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch
 extern "C" int pc_run_calls(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
                             int32_t disable_pruning, int32_t want_iteration,
                             pc_call_result *results, pc_plan *plans, pc_stats *stats) {
+    ctx->bounded_calls = ctx->bound_reruns = 0;
     std::vector<pc_call> cv(calls, calls + n);
     std::vector<CallOut> outs;
     int chunks = 0;
@@ -1199,6 +1203,7 @@ extern "C" int pc_last_crossing(pc_ctx *ctx, int32_t index, int64_t visits_befor
 
 extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, int32_t disable_pruning,
                              int64_t visit_budget, int32_t speculative, pc_plan *plan, pc_stats *stats) {
+    ctx->bounded_calls = ctx->bound_reruns = 0;
     if (N < 1 || dpn < 1 || BS < 1)
         return fail(ctx, PC_ERR_INVALID, "node count, devices per node and batch size must be at least 1");
     if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
@@ -1721,6 +1726,12 @@ extern "C" int pc_timer_stop(pc_ctx *ctx, double *ms) {
     float f = 0;
     CUDA_TRY(ctx, cudaEventElapsedTime(&f, ctx->t0, ctx->t1));
     *ms = f;
+    return PC_OK;
+}
+
+extern "C" int pc_bound_info(pc_ctx *ctx, int64_t *bounded_calls, int64_t *reruns) {
+    *bounded_calls = ctx->bounded_calls;
+    *reruns = ctx->bound_reruns;
     return PC_OK;
 }
 

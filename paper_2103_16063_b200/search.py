@@ -86,6 +86,30 @@ def device_weights(ctx: _lib.Context, calls, batch_size: int):
     return out[:n].tolist()
 
 
+# the library bounds the DP of batches from this many closed-form visits up
+# (api.cu: BOUND_MIN_VISITS); their per-call cost then follows the DP cells
+BOUNDED_BATCH_VISITS = 2e10
+
+
+def shard_weights(ctx: _lib.Context, calls, batch_size: int, nb: int):
+    """LPT weights of the calls.  Unbounded searches: `device` -- feasible
+    pairs from the key tables (pc_call_weights).  Searches large enough for the
+    objective bound: `cells` -- S * A * B DP cells, which tracks the bounded
+    kernel's per-call cost best (4096 x 256 on 4 GPUs: 367 ms per step vs 405 ms
+    with either visit-based weight, r2n).  PIPECUT_B200_SHARD_WEIGHTS forces
+    `device`, `visits` (closed-form unpruned visits) or `cells`."""
+    import os
+    kind = os.environ.get("PIPECUT_B200_SHARD_WEIGHTS")
+    if kind is None:
+        kind = "cells" if sum(call_weight(nb, c) for c in calls) >= BOUNDED_BATCH_VISITS \
+            else "device"
+    if kind == "visits":
+        return [call_weight(nb, c) for c in calls]
+    if kind == "cells":
+        return [c[0] * (nb - c[0] + 1) * (c[1] - c[0] + 1) for c in calls]
+    return device_weights(ctx, calls, batch_size)
+
+
 class BatchResult:
     """Per-call records of one device batch: `results` is a structured array
     with the PcCallResult fields, `bufs[i]` the call's stage arrays."""
@@ -301,7 +325,7 @@ def form_stage_sharded(num_nodes: int, devices_per_node: int, batch_size: int, b
     n_levels = (max(levels) + 1) if levels else 0
     max_stages = max((c[0] for c in calls), default=1)
     dev = torch.device("cuda", ctx.device)
-    weights = device_weights(ctx, calls, batch_size) if world > 1 else None
+    weights = shard_weights(ctx, calls, batch_size, nb) if world > 1 else None
     if not speculative:
         return _sharded_by_level(ctx, calls, levels, n_levels, max_stages, nb, weights, world,
                                  rank, group, dev, opts, batch_size)
@@ -377,12 +401,12 @@ def _raise_crossing(ctx, calls, owner, local_idx, cross, before, world, rank, gr
     raise SearchBudgetExceeded(int(v[0]), int(opts.visit_budget))
 
 
-# Schedule (i): a widening level whose summed sharding weight (pc_call_weights,
-# ~feasible pairs) is below this runs whole on every rank instead of being
-# sharded: such a level takes ~10 ms on one B200 (tools/level_costs.py, r2c:
-# ~1e-11 s per weight unit plus a few ms of launches), so splitting it saves
-# less than the pack + all-gather + decide round it would cost.
-REPLICATE_BELOW = 1.0e9
+# Schedule (i): a widening level below this many closed-form unpruned visits
+# runs whole on every rank instead of being sharded: such a level takes
+# ~15 ms or less on one B200 (tools/level_costs.py, r2c: 1024 x 256 level 1,
+# 5.3e9 visits, 15 ms), so splitting it saves less than the pack + all-gather
+# + decide round it would cost.
+REPLICATE_BELOW = 5e9
 
 
 def _sharded_by_level(ctx, calls, levels, n_levels, max_stages, nb, weights, world, rank, group,
@@ -401,8 +425,7 @@ def _sharded_by_level(ctx, calls, levels, n_levels, max_stages, nb, weights, wor
         while end < n and levels[end] == lv:
             end += 1
         idx = list(range(start, end))
-        replicated = world == 1 or (weights is not None and
-                                    sum(weights[i] for i in idx) < REPLICATE_BELOW)
+        replicated = world == 1 or sum(call_weight(nb, calls[i]) for i in idx) < REPLICATE_BELOW
         if replicated:
             for i in idx:
                 owner[i] = rank        # every rank computes (and owns) every call

@@ -243,8 +243,10 @@ def _level_worker(rank, world, port, seed, heavy, q):
 
         search.run_calls = fake_run_calls
         search.exchange = counting_exchange
-        # level weights: the heavy levels above the threshold, the rest below it
-        w = [int(search.REPLICATE_BELOW) if levels[i] in heavy else 1 for i in range(len(calls))]
+        # heavy levels above the replication threshold, the rest below it
+        search.call_weight = lambda nb, c: (int(search.REPLICATE_BELOW)
+                                            if levels[calls.index(c)] in heavy else 1)
+        w = [1] * len(calls)
         res = search._sharded_by_level(None, calls, levels, max(levels) + 1,
                                        max(c[0] for c in calls), 6, w, world, rank, None, None,
                                        pc.SearchOptions(), 16)
