@@ -505,7 +505,8 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     // under this call's shares (run_calls_impl runs the partners first), or the
     // explicit ctx->bb_U (measurement hook).
     bool bounded = false;
-    if (!ctx->has_cost_table && ctx->mono_skip && (!ctx->bb_U.empty() || !ctx->bb_partner.empty())) {
+    if (!ctx->has_cost_table && ctx->mono_skip && !ctx->bb_off &&
+        (!ctx->bb_U.empty() || !ctx->bb_partner.empty())) {
         bool closed = true;
         for (auto &k : want) closed = closed && ctx->keys[ctx->key_map[k]].closed;
         if (closed) {
@@ -958,7 +959,10 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             if (!ctx->bb_U.empty()) ctx->bb_U[o] = INFINITY;
         }
         ctx->bound_reruns += (int64_t)retry.size();
-        return run_chunk(ctx, calls, retry, BS, pruning, want_iter, outs);
+        ctx->bb_off = true;                       // the re-run is unbounded
+        const int rc = run_chunk(ctx, calls, retry, BS, pruning, want_iter, outs);
+        ctx->bb_off = false;
+        return rc;
     }
     return PC_OK;
 }

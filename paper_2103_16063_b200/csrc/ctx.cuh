@@ -112,6 +112,7 @@ struct pc_ctx {
     std::vector<int> last_pos;          // orig -> sorted position
     std::vector<double> bb_U;           // per call of the current run_calls_impl (bound)
     std::vector<int> bb_partner;        // per call: call whose optimum bounds it, or -1
+    bool bb_off = false;                // re-running calls whose bound was too tight
     const void *bb_outs = nullptr;      // the CallOut list those indices refer to
     DBuf bound_d;                       // plan-bound inputs / outputs
     DBuf reach_d;                       // non-empty prefix counts (two levels)

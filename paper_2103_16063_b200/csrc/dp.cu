@@ -253,6 +253,27 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
     auto over = [&](double x, double y) {
         return bounded && __dadd_rn(dmax_ref(x, lbf), dmax_ref(y, lbb)) > U;
     };
+    // The whole cell above the bound: every entry (x, y) has x >= plf and
+    // y >= plb, the same two lower bounds for the s stages over [0, b) with d
+    // devices (devp = d - (s - 1) the most one of them can hold).  Then no
+    // predecessor is scanned; the cell's emptiness and zero-share flags come
+    // from the prefix counts below.
+    bool cell_dead = false;
+    if (bounded && s > 1) {
+        const int devp = d - (s - 1);
+        const int kp = keyidx[devp];
+        if (kp >= 0) {
+            const int64_t o = hm_idx(0, b);
+            const int64_t q = (int64_t)cd.MB * cd.R;
+            const int64_t mp = B.batch_size / (q * devp);
+            const double k1 = 1.0 / (double)s;
+            const double k2 = (double)(B.batch_size - q * devp + 1) / ((double)(q * d) * (double)mp);
+            const double k = (1.0 - 1e-9) * (k1 > k2 ? k1 : k2);
+            const double plf = __dmul_rn(fabs(B.key_tf[kp][o]), k);
+            const double plb = DERIVED ? __dmul_rn(beta, plf) : __dmul_rn(fabs(B.key_tb[kp][o]), k);
+            cell_dead = over(plf, plb);
+        }
+    }
     int n = 0;
     bool ovf = false;
     bool zero = false;
@@ -324,7 +345,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         const int dpn = B.dpn;
         const bool multi_node = B.num_nodes > 1;
         int rem = (int)((unsigned)(d - 1) % (unsigned)dpn);
-        for (int dp = d - 1; dp >= base; --dp, rem = rem == 0 ? dpn - 1 : rem - 1) {
+        for (int dp = d - 1; !cell_dead && dp >= base; --dp, rem = rem == 0 ? dpn - 1 : rem - 1) {
             const int lo_col = cmin[dp - base];
             const int hi_col = cmax[dp - base];
             if (lo_col > hi_col || lo_col >= b) continue;           // no predecessor cell
