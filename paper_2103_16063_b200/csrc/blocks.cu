@@ -786,8 +786,14 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
     double t_dev = 0.0;
     for (int li = (int)transitions.size() - 1; li >= 0; --li) {
         const auto &pairs = transitions[li];
-        size_t p = 0;
+        // Rounds evaluate a window of pairs from p on (48, doubling while a
+        // window holds no move): pairs past the first move would be evaluated
+        // against a state that move changes, so building their sets is wasted
+        // host and device work.  A window without a move is skipped exactly as
+        // the reference skips those pairs (same state).
+        size_t p = 0, win = 48;
         while (p < pairs.size()) {
+            const size_t end = std::min(pairs.size(), p + win);
             for (int l = li; l <= top; ++l)
                 if (co.dirty[l])
                     if (int rc = co.upload_level(l, co.levels[l])) return rc;
@@ -802,7 +808,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
             std::vector<Tri> tris;
             std::vector<SetDesc> sets;
             std::vector<MoveDesc> moves;
-            for (size_t q = p; q < pairs.size(); ++q) {
+            for (size_t q = p; q < end; ++q) {
                 for (int mi = 0; mi < 2; ++mi) {
                     const std::vector<int> &mover = mi == 0 ? pairs[q].first : pairs[q].second;
                     const int here = maps[top][mover[0]];
@@ -837,7 +843,7 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
             const int nlev = top - li;
             bool applied = false;
             size_t ti_ptr = 0;
-            for (size_t q = p; q < pairs.size() && !applied; ++q) {
+            for (size_t q = p; q < end && !applied; ++q) {
                 int64_t best_saving = 0;
                 int best = -1;
                 for (; ti_ptr < tris.size() && tris[ti_ptr].q == (int)q; ++ti_ptr) {
@@ -881,9 +887,14 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
                     }
                     applied = true;
                     p = q + 1;
+                    win = 48;
                 }
             }
-            if (!applied) break;
+            if (!applied) {
+                if (end == pairs.size()) break;
+                p = end;
+                win *= 2;
+            }
         }
     }
 

@@ -155,10 +155,11 @@ struct CallDesc {
                                // every completion exceeds it are dropped (dp.cu: bound)
 };
 
-// Warps (cells) per CTA of the level kernel: 4 warps x 8 CTAs per SM (64
+// Warps (cells) per CTA of the level kernel: 4 warps x 12 CTAs per SM (40
 // registers, DP_MIN_BLOCKS in dp.cu) -- small CTAs free their slot as soon as
 // their few cells finish; the occupancy/register split is re-measured whenever
-// the kernel changes (tuning log)
+// the kernel changes (round 2 sweep, 7 / 8 / 10 / 12 CTAs per SM =
+// 1258 / 1180 / 1159 / 1116 ms of DP on 4096 x 256)
 #ifndef PC_DP_WARPS
 #define PC_DP_WARPS 4
 #endif

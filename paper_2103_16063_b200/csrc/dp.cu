@@ -25,7 +25,7 @@
 #include "common.cuh"
 
 #ifndef DP_MIN_BLOCKS
-#define DP_MIN_BLOCKS 8
+#define DP_MIN_BLOCKS 12
 #endif
 // diagnostic counters (frontier-size histogram, rounds, chunks, corner-pruned
 // pairs, window entries) for PIPECUT_B200_DEBUG: build with -DPC_DP_DIAG=1
