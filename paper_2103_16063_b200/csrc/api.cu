@@ -408,8 +408,9 @@ static inline int64_t tri_sum(int64_t n) { return n * (n + 1) / 2; }
 // largest pool offset (entries) a 31-bit frontier offset can hold
 constexpr int64_t OFF_MAX = (int64_t)SPILL_BIT - 1;
 // history cells per chunk: the shared history spill pool is sized from them
-// (one entry per cell at first) and must stay within OFF_MAX
-constexpr int64_t CHUNK_HIST_CELLS = int64_t(1) << 30;
+// (one entry per cell at first) and must stay within OFF_MAX (the pools are
+// capped there anyway; fewer chunks means fewer passes over the levels)
+constexpr int64_t CHUNK_HIST_CELLS = 1900000000;
 // objective bound (dp.cu) only for batches of at least this many unpruned visits
 constexpr double BOUND_MIN_VISITS = 2e10;
 
@@ -653,13 +654,20 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.hspill_used = used + 3 * (size_t)n + 2;
         bt.hist_cells = hist_cells;
         bt.bounded = bounded ? 1 : 0;
-        int64_t *d_colpre = nullptr;
+        int64_t *d_colpre = nullptr, *d_cellpre = nullptr;
+        std::vector<int64_t> cell_prefix(n + 1, 0);
         if (bounded) {
-            CUDA_TRY(ctx, ctx->reach_d.ensure(2 * 4 * (size_t)val_cells + 8 * (size_t)(n + 1) + 64));
+            for (int i = 0; i < n; ++i) cell_prefix[i + 1] = cell_prefix[i] + (int64_t)cds[i].A * cds[i].B;
+            CUDA_TRY(ctx, ctx->reach_d.ensure(2 * 4 * (size_t)val_cells + 16 * (size_t)(n + 1) + 64));
             bt.reach_pre[0] = ctx->reach_d.as<int32_t>();
             bt.reach_pre[1] = bt.reach_pre[0] + val_cells;
             d_colpre = (int64_t *)(((uintptr_t)(bt.reach_pre[1] + val_cells) + 15) & ~uintptr_t(15));
+            d_cellpre = d_colpre + (n + 1);
             CUDA_TRY(ctx, cudaMemcpyAsync(d_colpre, col_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
+            CUDA_TRY(ctx, cudaMemcpyAsync(d_cellpre, cell_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
+            CUDA_TRY(ctx, ctx->live_d.ensure(8 * (size_t)val_cells + 64));
+            bt.live_count = ctx->live_d.as<unsigned long long>();
+            bt.live = bt.live_count + 8;
         }
         CUDA_TRY(ctx, cudaMemsetAsync(ob, 0, 64 + 3 * sizeof(unsigned long long) * (size_t)n + 64, ctx->st));
         CUDA_TRY(ctx, ctx->counters_d.ensure((8 + FMAX + 3 * WORK_SLOTS) * sizeof(unsigned long long)));
@@ -696,9 +704,18 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             CUDA_TRY(ctx, cudaMemsetAsync(bt.vspill_used + (s & 1), 0, sizeof(unsigned long long), ctx->st));
             CUDA_TRY(ctx, cudaMemsetAsync(bt.col_min[s & 1], 0x7f, sizeof(int32_t) * col_prefix[n_active], ctx->st));
             CUDA_TRY(ctx, cudaMemsetAsync(bt.col_max[s & 1], 0xff, sizeof(int32_t) * col_prefix[n_active], ctx->st));
-            launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, ctx->st);
+            if (bounded) {
+                // settle the cells above the bound by a thread each, then a
+                // persistent grid of warps over the live ones (dp.cu)
+                CUDA_TRY(ctx, cudaMemsetAsync(bt.live_count, 0, 2 * sizeof(unsigned long long), ctx->st));
+                launch_dp_triage(bt, s, n_active, cell_prefix[n_active], d_cellpre, ctx->derived, ctx->st);
+                launch_dp_level_list(bt, s, ctx->sm_count * DP_MIN_CTAS, ctx->derived, ctx->st);
+                ctx->launches += 2;
+            } else {
+                launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, ctx->st);
+                ctx->launches++;
+            }
             ++launches;
-            ctx->launches++;
             if (bounded && s < maxS) {
                 launch_reach_prefix(bt, s, n_active, col_prefix[n_active], d_colpre, ctx->st);
                 ctx->launches++;

@@ -164,6 +164,15 @@ struct CallDesc {
 #define PC_DP_WARPS 4
 #endif
 constexpr int DP_WARPS = PC_DP_WARPS;
+#ifndef DP_MIN_BLOCKS
+#define DP_MIN_BLOCKS 12
+#endif
+// the bounded batches' persistent list kernel: 8 CTAs per SM (64 registers)
+// measured best there (r2w: 813 vs 861 ms of DP on 4096 x 256 at 12)
+#ifndef DP_LIST_MIN_BLOCKS
+#define DP_LIST_MIN_BLOCKS 8
+#endif
+constexpr int DP_MIN_CTAS = DP_LIST_MIN_BLOCKS;   // resident list-kernel CTAs per SM
 constexpr int WORK_SLOTS = 64;  // work counters spread over slots (no same-address atomics)
 constexpr int FMAX = 64;       // Pareto frontier capacity per cell (two slots per lane)
 
@@ -194,6 +203,10 @@ struct DPBatch {
     // cells the reference holds non-empty (count > 0 or CNT_REACH)
     int32_t *reach_pre[2];
     int bounded;                    // some call of the batch has a finite U
+    // bounded batches: the live cells of the level (call << 40 | cell index),
+    // listed by k_dp_triage, walked by k_dp_level_list
+    unsigned long long *live;
+    unsigned long long *live_count;  // [0] cells listed, [1] cells taken (k_dp_level_list)
     double *pool_tf[2];
     double *pool_tb[2];
     unsigned long long *vpool_used[2];  // [n_calls] per parity
@@ -259,6 +272,9 @@ void launch_reach_prefix(const DPBatch &b, int s, int n_active, int64_t n_cols,
                          const int64_t *col_prefix, cudaStream_t st);
 void launch_greedy_bound(const DPBatch &b, int n, const int32_t *pos, double *U, bool derived,
                          cudaStream_t st);
+void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
+                      const int64_t *cell_prefix, bool derived, cudaStream_t st);
+void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, cudaStream_t st);
 void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
                             const int64_t *m, const int32_t *ckpt, double *tf, double *tb,
                             int64_t *mem, cudaStream_t st);

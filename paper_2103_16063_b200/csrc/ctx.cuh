@@ -116,6 +116,7 @@ struct pc_ctx {
     const void *bb_outs = nullptr;      // the CallOut list those indices refer to
     DBuf bound_d;                       // plan-bound inputs / outputs
     DBuf reach_d;                       // non-empty prefix counts (two levels)
+    DBuf live_d;                        // live-cell list of a bounded level + its count
     DBuf open_d;                        // first_feasible: per fresh key, not suffix-closed
     int64_t bounded_calls = 0, bound_reruns = 0;   // diagnostics of the last run
     std::vector<std::vector<int64_t>> last_level_sums;  // by orig

@@ -24,9 +24,6 @@
 
 #include "common.cuh"
 
-#ifndef DP_MIN_BLOCKS
-#define DP_MIN_BLOCKS 12
-#endif
 // diagnostic counters (frontier-size histogram, rounds, chunks, corner-pruned
 // pairs, window entries) for PIPECUT_B200_DEBUG: build with -DPC_DP_DIAG=1
 #ifndef PC_DP_DIAG
@@ -190,18 +187,55 @@ __device__ __forceinline__ int lex_min_lane(bool live, double x, double y, uint3
     return __ffs(m) - 1;
 }
 
+// Lower bounds on the largest raw forward / backward stage time of a group of
+// stages (see dp_cell): k stages over span [lo, hi) with `dev` devices in all,
+// so one of them holds at most devmax = dev - (k - 1).  Stage i runs at share
+// m_i = BS // (q dev_i), q = MB R; with T >= m_i w_i for every stage (w_i its
+// time per unit share), T >= sum w_i / sum 1/m_i and sum 1/m_i <=
+// q dev / (BS - q devmax + 1) (floor(x/y) >= (x - y + 1)/y); also
+// T >= t(lo, hi; m(devmax)) / k (times are monotone in the share), and
+// sum w_i ~ t(lo, hi; m(devmax)) / m(devmax).  The factor (1 - 1e-9) absorbs
+// the folds' rounding.  False when no share is positive at devmax.
 template <bool DERIVED>
-__global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBatch B, int s, int n_active) {
-    const int64_t cta = blockIdx.x;                  // grid = cta_prefix[n_active]
-    const int c = B.cta_call[cta];
+__device__ __forceinline__ bool group_bounds(const DPBatch &B, const CallDesc &cd,
+                                             const int16_t *keyidx, int lo, int hi, int k, int dev,
+                                             double &lf, double &lb) {
+    const int devmax = dev - (k - 1);
+    const int kx = keyidx[devmax];
+    if (kx < 0) return false;
+    const int64_t o = hm_idx(lo, hi);
+    const int64_t q = (int64_t)cd.MB * cd.R;
+    const int64_t mx = B.batch_size / (q * devmax);
+    const double k1 = 1.0 / (double)k;
+    const double k2 = (double)(B.batch_size - q * devmax + 1) / ((double)(q * dev) * (double)mx);
+    const double kk = (1.0 - 1e-9) * (k1 > k2 ? k1 : k2);
+    lf = __dmul_rn(fabs(B.key_tf[kx][o]), kk);
+    lb = DERIVED ? __dmul_rn(B.beta, lf) : __dmul_rn(fabs(B.key_tb[kx][o]), kk);
+    return true;
+}
+
+// the S - s stages after cell (b, d): [b, nb) on D - d devices
+template <bool DERIVED>
+__device__ __forceinline__ void suffix_bounds(const DPBatch &B, const CallDesc &cd,
+                                              const int16_t *keyidx, int s, int b, int d,
+                                              double &lf, double &lb) {
+    if (!group_bounds<DERIVED>(B, cd, keyidx, b, B.nb, cd.S - s, cd.D - d, lf, lb)) lf = lb = 0.0;
+}
+
+// the s stages of cell (b, d): [0, b) on d devices
+template <bool DERIVED>
+__device__ __forceinline__ bool prefix_bounds(const DPBatch &B, const CallDesc &cd,
+                                              const int16_t *keyidx, int s, int b, int d,
+                                              double &lf, double &lb) {
+    return group_bounds<DERIVED>(B, cd, keyidx, 0, b, s, d, lf, lb);
+}
+
+// One cell (b, d) = (s + idx / B, s + idx % B) of call c at level s, by one
+// warp (w = its warp in the CTA).
+template <bool DERIVED>
+__device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t idx) {
     const CallDesc cd = B.calls[c];
-    // warps take consecutive cells of the call in (b, d) order, so every warp
-    // of the CTA has a cell whatever B is
     const int w = threadIdx.x >> 5;
-    // heaviest cells (largest b: most predecessors) are dispatched first so
-    // the level's tail is short
-    const int64_t idx = (int64_t)cd.A * cd.B - 1 - ((cta - B.cta_prefix[c]) * DP_WARPS + w);
-    if (idx < 0) return;                              // whole warp
     const int bi = (int)(idx / cd.B);
     const int di = (int)(idx % cd.B);
     const int lane = threadIdx.x & 31;
@@ -235,19 +269,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         if (s == cd.S) {
             if (b != nb || d != cd.D) lbf = INFINITY;
         } else {
-            const int devmax = (cd.D - d) - (cd.S - s - 1);
-            const int kx = keyidx[devmax];
-            if (kx >= 0) {
-                const int64_t o = hm_idx(b, nb);
-                const int64_t q = (int64_t)cd.MB * cd.R;
-                const int64_t mx = B.batch_size / (q * devmax);
-                const double k1 = 1.0 / (double)(cd.S - s);
-                const double k2 = (double)(B.batch_size - q * devmax + 1) /
-                                  ((double)(q * (cd.D - d)) * (double)mx);
-                const double k = (1.0 - 1e-9) * (k1 > k2 ? k1 : k2);
-                lbf = __dmul_rn(fabs(B.key_tf[kx][o]), k);
-                lbb = DERIVED ? __dmul_rn(beta, lbf) : __dmul_rn(fabs(B.key_tb[kx][o]), k);
-            }
+            suffix_bounds<DERIVED>(B, cd, keyidx, s, b, d, lbf, lbb);
         }
     }
     auto over = [&](double x, double y) {
@@ -260,19 +282,8 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
     // from the prefix counts below.
     bool cell_dead = false;
     if (bounded && s > 1) {
-        const int devp = d - (s - 1);
-        const int kp = keyidx[devp];
-        if (kp >= 0) {
-            const int64_t o = hm_idx(0, b);
-            const int64_t q = (int64_t)cd.MB * cd.R;
-            const int64_t mp = B.batch_size / (q * devp);
-            const double k1 = 1.0 / (double)s;
-            const double k2 = (double)(B.batch_size - q * devp + 1) / ((double)(q * d) * (double)mp);
-            const double k = (1.0 - 1e-9) * (k1 > k2 ? k1 : k2);
-            const double plf = __dmul_rn(fabs(B.key_tf[kp][o]), k);
-            const double plb = DERIVED ? __dmul_rn(beta, plf) : __dmul_rn(fabs(B.key_tb[kp][o]), k);
-            cell_dead = over(plf, plb);
-        }
+        double plf, plb;
+        if (prefix_bounds<DERIVED>(B, cd, keyidx, s, b, d, plf, plb)) cell_dead = over(plf, plb);
     }
     int n = 0;
     bool ovf = false;
@@ -588,6 +599,139 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
         B.hist_cnt[hcell] = byte;
         if (ovf) atomicOr(B.overflow, 1);
     }
+}
+
+template <bool DERIVED>
+__global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBatch B, int s, int n_active) {
+    const int64_t cta = blockIdx.x;                  // grid = cta_prefix[n_active]
+    const int c = B.cta_call[cta];
+    // warps take consecutive cells of the call in (b, d) order, so every warp
+    // of the CTA has a cell whatever B is; heaviest cells (largest b: most
+    // predecessors) are dispatched first so the level's tail is short
+    const int64_t idx = (int64_t)B.calls[c].A * B.calls[c].B - 1 -
+                        ((cta - B.cta_prefix[c]) * DP_WARPS + (threadIdx.x >> 5));
+    if (idx < 0) return;                              // whole warp
+    dp_cell<DERIVED>(B, s, c, idx);
+}
+
+// Bounded batches: a warp per LIVE cell only.  k_dp_triage settled every cell
+// whose whole frontier is above its call's bound (thread per cell: flags
+// only) and listed the others, heaviest first within each call; a persistent
+// grid takes them in list order, one cell per warp per atomic pop (dynamic, so
+// a warp that drew a heavy cell does not hold up the level's tail).
+#ifndef PC_LIST_ATOMIC
+#define PC_LIST_ATOMIC 1
+#endif
+template <bool DERIVED>
+__global__ void __launch_bounds__(DP_WARPS * 32, DP_LIST_MIN_BLOCKS) k_dp_level_list(DPBatch B, int s) {
+    const unsigned long long n = B.live_count[0];
+    const int lane = threadIdx.x & 31;
+    if (PC_LIST_ATOMIC) {
+        for (;;) {
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(B.live_count + 1, 1ull);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= n) break;
+            const unsigned long long e = B.live[t];
+            dp_cell<DERIVED>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)));
+        }
+    } else {
+        const unsigned long long stride = (unsigned long long)gridDim.x * DP_WARPS;
+        for (unsigned long long t = (unsigned long long)blockIdx.x * DP_WARPS + (threadIdx.x >> 5);
+             t < n; t += stride) {
+            const unsigned long long e = B.live[t];
+            dp_cell<DERIVED>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)));
+        }
+    }
+}
+
+// One thread per cell of the active calls of a bounded batch at level s: a
+// cell of a bounded call whose whole frontier is above the bound (the same
+// tests as dp_cell: level S off the final cell, or the prefix lower bound) gets
+// its count byte here -- CNT_REACH or 0 for the reference's emptiness, plus the
+// zero-share flag, from the previous level's non-empty prefix counts -- and
+// every other cell is appended to the live list (warp-aggregated).
+template <bool DERIVED>
+__global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_prefix) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    bool live = false;
+    int c = 0;
+    int64_t idx = 0;
+    if (g < cell_prefix[n_active]) {
+        int lo = 0, hi = n_active;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (cell_prefix[mid] <= g) lo = mid; else hi = mid;
+        }
+        c = lo;
+        const CallDesc cd = B.calls[c];
+        idx = (int64_t)cd.A * cd.B - 1 - (g - cell_prefix[c]);     // heaviest first
+        const int bi = (int)(idx / cd.B), di = (int)(idx % cd.B);
+        const int b = s + bi, d = s + di, nb = B.nb;
+        const int16_t *keyidx = B.keyidx + cd.key_off;
+        bool dead = false;
+        if (cd.U < INFINITY) {
+            if (s == cd.S) {
+                dead = b != nb || d != cd.D;
+            } else if (s > 1) {
+                double lbf = 0.0, lbb = 0.0;
+                suffix_bounds<DERIVED>(B, cd, keyidx, s, b, d, lbf, lbb);
+                double plf, plb;
+                if (prefix_bounds<DERIVED>(B, cd, keyidx, s, b, d, plf, plb))
+                    dead = __dadd_rn(dmax_ref(plf, lbf), dmax_ref(plb, lbb)) > cd.U;
+            }
+        }
+        if (dead) {
+            bool reach = false, zero = false;
+            if (s == 1) {
+                const int kk = keyidx[d];
+                if (kk < 0) zero = true;
+                else reach = span_ok(B.key_tf[kk][(int64_t)b * (b - 1) / 2], B.mono_skip);
+            } else {
+                const int base = s - 1;
+                const int32_t *rp = B.reach_pre[(s - 1) & 1] + cd.val_off;
+                for (int dp = base; dp < d; ++dp) {
+                    const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
+                    const int32_t upto = col[b - 1];
+                    if (upto == 0) continue;
+                    const int kk = keyidx[d - dp];
+                    if (kk < 0) { zero = true; continue; }
+                    const int x = max(base, B.key_ffb[kk][b]);
+                    if (x <= b - 1 && upto > (x > base ? col[x - 1] : 0)) reach = true;
+                }
+            }
+            const int64_t cell = (int64_t)di * cd.A + bi;
+            const uint8_t byte = (reach ? CNT_REACH : 0) | (zero ? CNT_ZERO : 0);
+            B.val_cnt[s & 1][cd.val_off + cell] = byte;
+            B.hist_cnt[cd.hist_off + (int64_t)(s - 1) * cd.A * cd.B + cell] = byte;
+        } else {
+            live = true;
+        }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, live);
+    unsigned long long base = 0;
+    if (lane == 0 && m) base = atomicAdd(B.live_count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (live) B.live[base + __popc(m & ((1u << lane) - 1u))] = ((unsigned long long)c << 40) | (unsigned long long)idx;
+}
+
+void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
+                      const int64_t *cell_prefix, bool derived, cudaStream_t st) {
+    if (n_cells <= 0) return;
+    const unsigned blocks = (unsigned)((n_cells + 255) / 256);
+    if (derived)
+        k_dp_triage<true><<<blocks, 256, 0, st>>>(b, s, n_active, cell_prefix);
+    else
+        k_dp_triage<false><<<blocks, 256, 0, st>>>(b, s, n_active, cell_prefix);
+}
+
+void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, cudaStream_t st) {
+    const int tpb = DP_WARPS * 32;
+    if (derived)
+        k_dp_level_list<true><<<n_ctas, tpb, 0, st>>>(b, s);
+    else
+        k_dp_level_list<false><<<n_ctas, tpb, 0, st>>>(b, s);
 }
 
 // CTA -> call of a batch, once per batch: the active calls of every level are
