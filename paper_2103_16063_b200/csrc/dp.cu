@@ -912,7 +912,7 @@ __global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U)
         hiT *= 2.0;
     }
     double loT = tries ? 0.5 * hiT : 0.0;
-    for (int it = 0; it < 24; ++it) {
+    for (int it = 0; it < 14; ++it) {        // T within ~1e-4 relative: ample for a bound
         const double mid = 0.5 * (loT + hiT);
         double dummy;
         if (pack(mid, false, dummy)) hiT = mid; else loT = mid;
