@@ -861,32 +861,44 @@ __global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U)
         return span_ok(tf, Bt.mono_skip);
     };
     // pack(T): true if S stages cover [0, nb); with `eval`, the plan's objective
-    auto pack = [&](double T, bool eval, double &obj) -> bool {
+    // pack(T): 1 if S stages cover [0, nb), 0 if T is too small, -1 to give up
+    // (a stage whose one-block span does not fit and that found no fitting span
+    // at all: memory, not T, is what fails -- no bound then)
+    auto pack = [&](double T, bool eval, double &obj) -> int {
         int lo = 0;
         double mf = 0.0, mb = 0.0;
         for (int i = 0; i < S; ++i) {
             const int last = nb - (S - 1 - i);
             int best = -1;
+            bool any_fit = false;
             if (i == S - 1) {
                 double tfc, tbc, raw;
                 const bool ok = charged(i, lo, nb, tfc, tbc, raw);
+                any_fit = ok;
                 if (ok && __dadd_rn(tfc, tbc) <= T) best = nb;
             } else {
                 for (int h0 = lo + 1; h0 <= last; h0 += 32) {
                     const int h = h0 + lane;
-                    bool good = false, stop = false;
+                    bool good = false, stop = false, fit = false;
                     if (h <= last) {
                         double tfc, tbc, raw;
-                        const bool ok = charged(i, lo, h, tfc, tbc, raw);
-                        good = ok && __dadd_rn(tfc, tbc) <= T;
+                        fit = charged(i, lo, h, tfc, tbc, raw);
+                        good = fit && __dadd_rn(tfc, tbc) <= T;
                         stop = raw > T;
                     }
                     const uint32_t gm = __ballot_sync(0xffffffffu, good);
                     if (gm) best = h0 + 31 - __clz(gm);
+                    any_fit = any_fit || __any_sync(0xffffffffu, fit);
                     if (__ballot_sync(0xffffffffu, stop)) break;
                 }
             }
-            if (best < 0) return false;
+            if (best < 0) {
+                if (!any_fit) {
+                    double tfc, tbc, raw;
+                    if (!charged(i, lo, lo + 1, tfc, tbc, raw)) return -1;
+                }
+                return 0;
+            }
             if (eval) {
                 double tfc, tbc, raw;
                 charged(i, lo, best, tfc, tbc, raw);
@@ -896,7 +908,7 @@ __global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U)
             lo = best;
         }
         obj = __dadd_rn(mf, mb);
-        return true;
+        return 1;
     };
     double obj = INFINITY, dummy;
     // a T that packs: from the balanced estimate (1 + beta) t(0, nb) / S,
@@ -904,8 +916,10 @@ __global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U)
     const double total = fabs(Bt.key_tf[kq][hm_idx(0, nb)]);
     double hiT = 1.5 * (1.0 + Bt.beta) * total / S + 1e-300;
     int tries = 0;
-    while (!pack(hiT, false, dummy)) {
-        if (++tries > 8) {
+    for (;;) {
+        const int r = pack(hiT, false, dummy);
+        if (r > 0) break;
+        if (r < 0 || ++tries > 8) {
             if (lane == 0) U[w] = INFINITY;
             return;
         }
@@ -914,10 +928,9 @@ __global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U)
     double loT = tries ? 0.5 * hiT : 0.0;
     for (int it = 0; it < 14; ++it) {        // T within ~1e-4 relative: ample for a bound
         const double mid = 0.5 * (loT + hiT);
-        double dummy;
-        if (pack(mid, false, dummy)) hiT = mid; else loT = mid;
+        if (pack(mid, false, dummy) > 0) hiT = mid; else loT = mid;
     }
-    const bool ok = pack(hiT, true, obj);
+    const bool ok = pack(hiT, true, obj) > 0;
     if (lane == 0) U[w] = ok ? obj : INFINITY;
 }
 
