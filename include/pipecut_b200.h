@@ -52,7 +52,7 @@ extern "C" {
 #define PC_ERR_ATOM          (-3) /* InfeasibleAtom (blocks.py:22-31, 366-369) */
 #define PC_ERR_STUCK         (-4) /* CompactionStuck (blocks.py:34-42, 291) */
 #define PC_ERR_CUDA          (-5) /* CUDA / device error; see pc_last_error */
-#define PC_ERR_CAPACITY      (-6) /* frontier / table capacity exceeded (never truncated) */
+#define PC_ERR_CAPACITY      (-6) /* frontier (> 126 entries) / table capacity exceeded (never truncated) */
 
 typedef struct pc_ctx pc_ctx;
 
@@ -294,10 +294,12 @@ int pc_timer_stop(pc_ctx *ctx, double *ms);
  * denominator of the DP kernel (no tensor-core roof: min/max/add recurrence). */
 int pc_measure_fp64_peak(pc_ctx *ctx, double *gops);
 
-/* Objective-bound diagnostics of the last pc_run_calls / pc_form_stage* call:
- * calls that ran with a finite bound, and calls re-run unbounded because
- * their bound was below the optimum.  No reference counterpart. */
-int pc_bound_info(pc_ctx *ctx, int64_t *bounded_calls, int64_t *reruns);
+/* Diagnostics of the last pc_run_calls / pc_form_stage* call: calls that ran
+ * with a finite objective bound, calls re-run unbounded because their bound
+ * was below the optimum, and calls re-run with the 126-entry frontier kernels
+ * because some cell outgrew 64 entries (frontier_reruns may be NULL).  No
+ * reference counterpart. */
+int pc_bound_info(pc_ctx *ctx, int64_t *bounded_calls, int64_t *reruns, int64_t *frontier_reruns);
 
 /* Measured pure-DADD rate of this device (Gop/s): the fp64 pipe's peak op rate,
  * the denominator of the DP kernel's algorithmic-fp64 roofline. */

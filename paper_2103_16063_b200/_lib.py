@@ -82,7 +82,7 @@ def load():
         lib.pc_timer_stop.argtypes = [C.c_void_p, P(C.c_double)]
         lib.pc_measure_fp64_peak.argtypes = [C.c_void_p, P(C.c_double)]
         lib.pc_measure_dadd_peak.argtypes = [C.c_void_p, P(C.c_double)]
-        lib.pc_bound_info.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64)]
+        lib.pc_bound_info.argtypes = [C.c_void_p, P(C.c_int64), P(C.c_int64), P(C.c_int64)]
         for name in ("pc_ctx_create", "pc_device_info", "pc_set_problem", "pc_profile_spans",
                      "pc_form_stage_dp", "pc_run_calls", "pc_last_crossing", "pc_form_stage",
                      "pc_reset_cache", "pc_timer_start", "pc_timer_stop",

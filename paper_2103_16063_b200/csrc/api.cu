@@ -576,6 +576,11 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
     float dp_ms = 0;
     bool first_pass = true;
     int vcap = 8, hcap = 4;     // pool entries reserved per cell (grown on overflow)
+    bool big = false;           // four-slot (FMAX_BIG) kernels after a frontier overflow
+    // PIPECUT_B200_FMAX_LIMIT (tests only): a lower capacity for the two-slot
+    // kernels, so the four-slot re-run path runs on ordinary inputs
+    const char *lim_env = getenv("PIPECUT_B200_FMAX_LIMIT");
+    const int small_limit = lim_env ? std::max(1, std::min(FMAX, atoi(lim_env))) : FMAX;
     for (;;) {
         int64_t vpool_total = 0, hpool_total = 0, col_total = 0;
         std::vector<int64_t> col_prefix(n + 1, 0);
@@ -654,6 +659,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
         bt.hspill_used = used + 3 * (size_t)n + 2;
         bt.hist_cells = hist_cells;
         bt.bounded = bounded ? 1 : 0;
+        bt.fmax_limit = big ? FMAX_BIG : small_limit;
         int64_t *d_colpre = nullptr, *d_cellpre = nullptr;
         std::vector<int64_t> cell_prefix(n + 1, 0);
         if (bounded) {
@@ -709,10 +715,10 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
                 // persistent grid of warps over the live ones (dp.cu)
                 CUDA_TRY(ctx, cudaMemsetAsync(bt.live_count, 0, 2 * sizeof(unsigned long long), ctx->st));
                 launch_dp_triage(bt, s, n_active, cell_prefix[n_active], d_cellpre, ctx->derived, ctx->st);
-                launch_dp_level_list(bt, s, ctx->sm_count * DP_MIN_CTAS, ctx->derived, ctx->st);
+                launch_dp_level_list(bt, s, ctx->sm_count * DP_MIN_CTAS, ctx->derived, big, ctx->st);
                 ctx->launches += 2;
             } else {
-                launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, ctx->st);
+                launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, big, ctx->st);
                 ctx->launches++;
             }
             ++launches;
@@ -772,12 +778,21 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             first_pass = false;
         }
         ctx->last_dp_launches += launches;
-        if (ovf & 1) return fail(ctx, PC_ERR_CAPACITY, "a Pareto frontier exceeded 64 entries");
+        if (ovf & 1) {
+            // a cell outgrew the frontier capacity: re-run the pass with the
+            // four-slot kernels (126 entries, never truncated); beyond that
+            // the call is refused
+            if (big) return fail(ctx, PC_ERR_CAPACITY, "a Pareto frontier exceeded 126 entries");
+            big = true;
+            ctx->frontier_reruns += n;
+            CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->st));
+            continue;
+        }
         if (!ovf) break;
-        // a pool region ran out: grow and rerun the batch.  With FMAX entries
-        // reserved per cell every frontier fits its region unless the 31-bit
-        // offset cap clipped it: then the batch is beyond the offset range.
-        if (vcap >= FMAX && hcap >= FMAX)
+        // a pool region ran out: grow and rerun the batch.  With FMAX_BIG
+        // entries reserved per cell every frontier fits its region unless the
+        // 31-bit offset cap clipped it: then the batch is beyond the offset range.
+        if (vcap >= FMAX_BIG && hcap >= FMAX_BIG)
             return fail(ctx, PC_ERR_CAPACITY, "frontier pools beyond the 31-bit offset range");
         vcap *= 2;
         hcap *= 2;
@@ -1166,7 +1181,7 @@ static void fill_stats(pc_ctx *ctx, pc_stats *stats, int64_t visits, int64_t cal
 extern "C" int pc_form_stage_dp(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch_size, int32_t R,
                                 int32_t MB, int32_t disable_pruning, int64_t visit_budget,
                                 pc_plan *plan, pc_stats *stats) {
-    ctx->bounded_calls = ctx->bound_reruns = 0;
+    ctx->bounded_calls = ctx->bound_reruns = ctx->frontier_reruns = 0;
     std::vector<pc_call> calls = {{S, D, R, MB}};
     if (plan && S > plan->cap_stages && S <= ctx->nb) return fail(ctx, PC_ERR_CAPACITY, "plan capacity");
     std::vector<CallOut> outs;
@@ -1188,7 +1203,7 @@ extern "C" int pc_form_stage_dp(pc_ctx *ctx, int32_t S, int32_t D, int64_t batch
 extern "C" int pc_run_calls(pc_ctx *ctx, int32_t n, const pc_call *calls, int64_t batch_size,
                             int32_t disable_pruning, int32_t want_iteration,
                             pc_call_result *results, pc_plan *plans, pc_stats *stats) {
-    ctx->bounded_calls = ctx->bound_reruns = 0;
+    ctx->bounded_calls = ctx->bound_reruns = ctx->frontier_reruns = 0;
     std::vector<pc_call> cv(calls, calls + n);
     std::vector<CallOut> outs;
     int chunks = 0;
@@ -1224,7 +1239,7 @@ extern "C" int pc_last_crossing(pc_ctx *ctx, int32_t index, int64_t visits_befor
 
 extern "C" int pc_form_stage(pc_ctx *ctx, int32_t N, int32_t dpn, int64_t BS, int32_t disable_pruning,
                              int64_t visit_budget, int32_t speculative, pc_plan *plan, pc_stats *stats) {
-    ctx->bounded_calls = ctx->bound_reruns = 0;
+    ctx->bounded_calls = ctx->bound_reruns = ctx->frontier_reruns = 0;
     if (N < 1 || dpn < 1 || BS < 1)
         return fail(ctx, PC_ERR_INVALID, "node count, devices per node and batch size must be at least 1");
     if (!ctx->has_problem) return fail(ctx, PC_ERR_INVALID, "no problem set");
@@ -1750,9 +1765,11 @@ extern "C" int pc_timer_stop(pc_ctx *ctx, double *ms) {
     return PC_OK;
 }
 
-extern "C" int pc_bound_info(pc_ctx *ctx, int64_t *bounded_calls, int64_t *reruns) {
+extern "C" int pc_bound_info(pc_ctx *ctx, int64_t *bounded_calls, int64_t *reruns,
+                             int64_t *frontier_reruns) {
     *bounded_calls = ctx->bounded_calls;
     *reruns = ctx->bound_reruns;
+    if (frontier_reruns) *frontier_reruns = ctx->frontier_reruns;
     return PC_OK;
 }
 

@@ -175,6 +175,7 @@ constexpr int DP_WARPS = PC_DP_WARPS;
 constexpr int DP_MIN_CTAS = DP_LIST_MIN_BLOCKS;   // resident list-kernel CTAs per SM
 constexpr int WORK_SLOTS = 64;  // work counters spread over slots (no same-address atomics)
 constexpr int FMAX = 64;       // Pareto frontier capacity per cell (two slots per lane)
+constexpr int FMAX_BIG = 126;  // the re-run variant (four slots per lane; 127 = CNT_REACH)
 
 struct DPBatch {
     int nb;
@@ -224,7 +225,8 @@ struct DPBatch {
     unsigned long long *hspill_used;
     int64_t hspill_cap;
     int64_t hist_cells;
-    int *overflow;                  // 1: frontier > FMAX, 2: a pool region ran out
+    int *overflow;                  // 1: frontier > fmax_limit, 2: a pool region ran out
+    int fmax_limit;                 // frontier entries a cell may hold in this pass
     unsigned long long *counters;   // [0] pairs, [1] candidates, [2] inserts, [3..] sizes
 };
 
@@ -274,7 +276,8 @@ void launch_greedy_bound(const DPBatch &b, int n, const int32_t *pos, double *U,
                          cudaStream_t st);
 void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
                       const int64_t *cell_prefix, bool derived, cudaStream_t st);
-void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, cudaStream_t st);
+void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, bool big,
+                          cudaStream_t st);
 void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
                             const int64_t *m, const int32_t *ckpt, double *tf, double *tb,
                             int64_t *mem, cudaStream_t st);
@@ -284,7 +287,7 @@ void launch_call_weights(int nb, int n, const int32_t *calls, const int32_t *kof
 // dp.cu
 void launch_cta_call(const int64_t *prefix, int n, int64_t total, int32_t *out, cudaStream_t st);
 void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool derived,
-                     cudaStream_t st);
+                     bool big, cudaStream_t st);
 // cost tables: the reference's pruning break applied to the level's cells;
 // returns the number of kernels launched
 int launch_prune_cut(const DPBatch &b, int s, int n_active, int64_t n_rows, int64_t n_cols,

@@ -119,6 +119,7 @@ struct pc_ctx {
     DBuf live_d;                        // live-cell list of a bounded level + its count
     DBuf open_d;                        // first_feasible: per fresh key, not suffix-closed
     int64_t bounded_calls = 0, bound_reruns = 0;   // diagnostics of the last run
+    int64_t frontier_reruns = 0;                     // calls re-run with FMAX_BIG frontiers
     std::vector<std::vector<int64_t>> last_level_sums;  // by orig
     int last_pruning = 1;
     int last_FL = 4;

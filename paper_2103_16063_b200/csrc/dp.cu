@@ -44,12 +44,11 @@ __device__ __forceinline__ bool dominates(double ex, double ey, uint32_t ek, dou
 }
 
 // Per-warp Pareto frontiers in shared memory, each sorted by x ascending
-// (y strictly descending).  Accessed through one 32-bit shared-window base
-// per warp (ld/st.shared), so no generic addressing and no per-access
+// (y strictly descending), 32 * SLOTS entries per warp: SLOTS = 2 (FMAX) in
+// the kernels every search runs, 4 (FMAX_BIG) in the variant a pass is re-run
+// with when some cell outgrew FMAX.  Accessed through one 32-bit shared-window
+// base per warp (ld/st.shared), so no generic addressing and no per-access
 // rematerialization of the warp index.
-__shared__ double g_fx[DP_WARPS][FMAX];
-__shared__ double g_fy[DP_WARPS][FMAX];
-__shared__ uint32_t g_fk[DP_WARPS][FMAX];
 
 __device__ __forceinline__ double lds_f64(uint32_t a) {
     double v;
@@ -80,10 +79,14 @@ struct WarpFront {
     }
 };
 
+template <int SLOTS>
 __device__ __forceinline__ WarpFront warp_front(int w) {
-    return WarpFront{(uint32_t)__cvta_generic_to_shared(&g_fx[w][0]),
-                     (uint32_t)__cvta_generic_to_shared(&g_fy[w][0]),
-                     (uint32_t)__cvta_generic_to_shared(&g_fk[w][0])};
+    __shared__ double fx[DP_WARPS][32 * SLOTS];
+    __shared__ double fy[DP_WARPS][32 * SLOTS];
+    __shared__ uint32_t fk[DP_WARPS][32 * SLOTS];
+    return WarpFront{(uint32_t)__cvta_generic_to_shared(&fx[w][0]),
+                     (uint32_t)__cvta_generic_to_shared(&fy[w][0]),
+                     (uint32_t)__cvta_generic_to_shared(&fk[w][0])};
 }
 
 __device__ __forceinline__ int log2_steps(int n) {
@@ -119,8 +122,51 @@ __device__ __forceinline__ bool corner_dominated(const WarpFront &f, int n, doub
 // Warp-cooperative exact insert of c (same c in every lane); lane l owns
 // slots l and l + 32 (the second only once the frontier exceeds 32).
 // Returns the new size, or -1 beyond FMAX.
+template <int SLOTS>
 __device__ __forceinline__ int front_insert(const WarpFront &f, int n, int lane, double cx, double cy,
-                                            uint32_t ck) {
+                                            uint32_t ck);
+
+// the same for SLOTS = 4 (lane l owns slots l + 32 j), capacity FMAX_BIG
+template <>
+__device__ __forceinline__ int front_insert<4>(const WarpFront &f, int n, int lane, double cx,
+                                               double cy, uint32_t ck) {
+    double xs[4], ys[4];
+    uint32_t ks[4], m[4];
+    bool keep[4], lt[4];
+    int pos_c = 0, tot = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int q = lane + 32 * j;
+        const bool h = q < n;
+        xs[j] = 0; ys[j] = 0; ks[j] = 0;
+        if (h) { xs[j] = f.x(q); ys[j] = f.y(q); ks[j] = f.k(q); }
+        keep[j] = h && !dominates(cx, cy, ck, xs[j], ys[j], ks[j]);
+        m[j] = __ballot_sync(0xffffffffu, keep[j]);
+        lt[j] = keep[j] && xs[j] < cx;
+        pos_c += __popc(__ballot_sync(0xffffffffu, lt[j]));
+        tot += __popc(m[j]);
+    }
+    const int nn = tot + 1;
+    if (nn > FMAX_BIG) return -1;
+    const uint32_t below = (1u << lane) - 1u;
+    int p[4], acc = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        p[j] = acc + __popc(m[j] & below) + (lt[j] ? 0 : 1);
+        acc += __popc(m[j]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (keep[j]) f.put(p[j], xs[j], ys[j], ks[j]);
+    if (lane == 0) f.put(pos_c, cx, cy, ck);
+    __syncwarp();
+    return nn;
+}
+
+template <>
+__device__ __forceinline__ int front_insert<2>(const WarpFront &f, int n, int lane, double cx,
+                                               double cy, uint32_t ck) {
     const bool h0 = lane < n;
     double x0 = 0, y0 = 0;
     uint32_t k0 = 0;
@@ -231,8 +277,8 @@ __device__ __forceinline__ bool prefix_bounds(const DPBatch &B, const CallDesc &
 }
 
 // One cell (b, d) = (s + idx / B, s + idx % B) of call c at level s, by one
-// warp (w = its warp in the CTA).
-template <bool DERIVED>
+// warp (w = its warp in the CTA), frontier capacity 32 * SLOTS.
+template <bool DERIVED, int SLOTS>
 __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t idx) {
     const CallDesc cd = B.calls[c];
     const int w = threadIdx.x >> 5;
@@ -248,7 +294,7 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
     const int inter_d = (B.num_nodes > 1 && (unsigned)d % (unsigned)B.dpn == 0) ? 1 : 0;
     const int64_t row = (int64_t)b * (b - 1) / 2;       // hm_idx(0, b)
     const double beta = B.beta;
-    const WarpFront F = warp_front(w);
+    const WarpFront F = warp_front<SLOTS>(w);
     // Objective bound (CallDesc.U, finite only with non-negative times and no
     // cost table): every completion of an entry (x, y) of this cell costs at
     // least max(x, lbf) + max(y, lbb), lbf a lower bound on the largest raw
@@ -477,8 +523,8 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
                         const double ty = __shfl_sync(0xffffffffu, cy, t);
                         const uint32_t tk = __shfl_sync(0xffffffffu, ck, t);
                         ++n_ins;
-                        const int nn = front_insert(F, n, lane, tx, ty, tk);
-                        if (nn < 0) ovf = true; else n = nn;
+                        const int nn = front_insert<SLOTS>(F, n, lane, tx, ty, tk);
+                        if (nn < 0 || nn > B.fmax_limit) ovf = true; else n = nn;
                         surv = surv && lane != t && !dominates(tx, ty, tk, cx, cy, ck);
                     }
                 }
@@ -601,7 +647,7 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
     }
 }
 
-template <bool DERIVED>
+template <bool DERIVED, int SLOTS>
 __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBatch B, int s, int n_active) {
     const int64_t cta = blockIdx.x;                  // grid = cta_prefix[n_active]
     const int c = B.cta_call[cta];
@@ -611,7 +657,7 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
     const int64_t idx = (int64_t)B.calls[c].A * B.calls[c].B - 1 -
                         ((cta - B.cta_prefix[c]) * DP_WARPS + (threadIdx.x >> 5));
     if (idx < 0) return;                              // whole warp
-    dp_cell<DERIVED>(B, s, c, idx);
+    dp_cell<DERIVED, SLOTS>(B, s, c, idx);
 }
 
 // Bounded batches: a warp per LIVE cell only.  k_dp_triage settled every cell
@@ -622,25 +668,30 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
 #ifndef PC_LIST_ATOMIC
 #define PC_LIST_ATOMIC 1
 #endif
-template <bool DERIVED>
+#ifndef PC_LIST_GRAB
+#define PC_LIST_GRAB 1          // consecutive list cells a warp takes per pop
+#endif
+template <bool DERIVED, int SLOTS>
 __global__ void __launch_bounds__(DP_WARPS * 32, DP_LIST_MIN_BLOCKS) k_dp_level_list(DPBatch B, int s) {
     const unsigned long long n = B.live_count[0];
     const int lane = threadIdx.x & 31;
     if (PC_LIST_ATOMIC) {
         for (;;) {
             unsigned long long t = 0;
-            if (lane == 0) t = atomicAdd(B.live_count + 1, 1ull);
+            if (lane == 0) t = atomicAdd(B.live_count + 1, (unsigned long long)PC_LIST_GRAB);
             t = __shfl_sync(0xffffffffu, t, 0);
             if (t >= n) break;
-            const unsigned long long e = B.live[t];
-            dp_cell<DERIVED>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)));
+            for (int g = 0; g < PC_LIST_GRAB && t + g < n; ++g) {
+                const unsigned long long e = B.live[t + g];
+                dp_cell<DERIVED, SLOTS>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)));
+            }
         }
     } else {
         const unsigned long long stride = (unsigned long long)gridDim.x * DP_WARPS;
         for (unsigned long long t = (unsigned long long)blockIdx.x * DP_WARPS + (threadIdx.x >> 5);
              t < n; t += stride) {
             const unsigned long long e = B.live[t];
-            dp_cell<DERIVED>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)));
+            dp_cell<DERIVED, SLOTS>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)));
         }
     }
 }
@@ -726,12 +777,16 @@ void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
         k_dp_triage<false><<<blocks, 256, 0, st>>>(b, s, n_active, cell_prefix);
 }
 
-void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, cudaStream_t st) {
+void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, bool big,
+                          cudaStream_t st) {
     const int tpb = DP_WARPS * 32;
-    if (derived)
-        k_dp_level_list<true><<<n_ctas, tpb, 0, st>>>(b, s);
-    else
-        k_dp_level_list<false><<<n_ctas, tpb, 0, st>>>(b, s);
+    if (big) {
+        if (derived) k_dp_level_list<true, 4><<<n_ctas, tpb, 0, st>>>(b, s);
+        else k_dp_level_list<false, 4><<<n_ctas, tpb, 0, st>>>(b, s);
+    } else {
+        if (derived) k_dp_level_list<true, 2><<<n_ctas, tpb, 0, st>>>(b, s);
+        else k_dp_level_list<false, 2><<<n_ctas, tpb, 0, st>>>(b, s);
+    }
 }
 
 // CTA -> call of a batch, once per batch: the active calls of every level are
@@ -752,13 +807,16 @@ void launch_cta_call(const int64_t *prefix, int n, int64_t total, int32_t *out, 
 }
 
 void launch_dp_level(const DPBatch &b, int s, int n_active, int64_t n_ctas, bool derived,
-                     cudaStream_t st) {
+                     bool big, cudaStream_t st) {
     const int tpb = DP_WARPS * 32;
     const unsigned blocks = (unsigned)n_ctas;
-    if (derived)
-        k_dp_level<true><<<blocks, tpb, 0, st>>>(b, s, n_active);
-    else
-        k_dp_level<false><<<blocks, tpb, 0, st>>>(b, s, n_active);
+    if (big) {
+        if (derived) k_dp_level<true, 4><<<blocks, tpb, 0, st>>>(b, s, n_active);
+        else k_dp_level<false, 4><<<blocks, tpb, 0, st>>>(b, s, n_active);
+    } else {
+        if (derived) k_dp_level<true, 2><<<blocks, tpb, 0, st>>>(b, s, n_active);
+        else k_dp_level<false, 2><<<blocks, tpb, 0, st>>>(b, s, n_active);
+    }
 }
 
 // ---------------------------------------------------------------- bound: U from a plan

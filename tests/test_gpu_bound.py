@@ -23,8 +23,8 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
 def _bound_info(ctx):
-    b, r = C.c_int64(), C.c_int64()
-    ctx.check(ctx.lib.pc_bound_info(ctx.h, C.byref(b), C.byref(r)), "pc_bound_info")
+    b, r, f = C.c_int64(), C.c_int64(), C.c_int64()
+    ctx.check(ctx.lib.pc_bound_info(ctx.h, C.byref(b), C.byref(r), C.byref(f)), "pc_bound_info")
     return b.value, r.value
 
 
