@@ -1172,23 +1172,37 @@ __device__ __forceinline__ int64_t row_visits(const uint8_t *row, int stride, in
 __global__ void k_visit_rows(DPBatch Bt, int pruning, const int64_t *call_row_prefix,
                              const int64_t *level_off, int64_t *level_sums) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= call_row_prefix[Bt.n_calls]) return;
-    int lo = 0, hi = Bt.n_calls;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (call_row_prefix[mid] <= r) lo = mid; else hi = mid;
+    int64_t key = -1;                 // level_sums slot of this row, -1: none
+    unsigned long long v = 0;
+    if (r < call_row_prefix[Bt.n_calls]) {
+        int lo = 0, hi = Bt.n_calls;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (call_row_prefix[mid] <= r) lo = mid; else hi = mid;
+        }
+        const int c = lo;
+        const int A = Bt.calls[c].A, B = Bt.calls[c].B;
+        const int64_t rl = r - call_row_prefix[c];
+        const int s = 1 + (int)(rl / A);
+        const int bi = (int)(rl % A);
+        if (s > 1) {                      // level 1 carries d_min: k_visit_level1
+            const uint8_t *row = Bt.hist_cnt + Bt.calls[c].hist_off + (int64_t)(s - 1) * A * B + bi;
+            int dead;
+            v = (unsigned long long)row_visits(row, A, s, s + bi, B, 0, pruning, &dead);
+            key = level_off[c] + s - 1;
+        }
     }
-    const int c = lo;
-    const CallDesc cd = Bt.calls[c];
-    const int64_t rl = r - call_row_prefix[c];
-    const int s = 1 + (int)(rl / cd.A);
-    const int bi = (int)(rl % cd.A);
-    if (s == 1) return;  // level 1 carries d_min: k_visit_level1
-    const int64_t cells = (int64_t)cd.A * cd.B;
-    const uint8_t *row = Bt.hist_cnt + cd.hist_off + (int64_t)(s - 1) * cells + bi;
-    int dead;
-    const int64_t v = row_visits(row, cd.A, s, s + bi, cd.B, 0, pruning, &dead);
-    atomicAdd((unsigned long long *)&level_sums[level_off[c] + s - 1], (unsigned long long)v);
+    // consecutive rows share their (call, level) slot: one atomic per warp then
+    // (every row of a level adding to one address was the kernel's bottleneck)
+    const int64_t k0 = __shfl_sync(0xffffffffu, key, 0);
+    if (__all_sync(0xffffffffu, key == k0)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && k0 >= 0)
+            atomicAdd((unsigned long long *)&level_sums[k0], v);
+    } else if (key >= 0) {
+        atomicAdd((unsigned long long *)&level_sums[key], v);
+    }
 }
 
 // Level 1 carries d_min from row to row (stages.py:205-209, 247-248): one
