@@ -137,9 +137,12 @@ def form_stage(num_nodes: int, devices_per_node: int, batch_size: int, blocks,
 
     Batching of the widening levels: ``speculative=True`` evaluates every level
     in one device batch, ``False`` one batch per level, and the default
-    (``None``) the first level alone and then, only if it has no feasible plan,
-    all the others in one batch.  The reference's first-feasible-level rule is
-    applied afterwards, so the result and the stats are identical either way.
+    (``None``) the first level alone and then, only while no level was
+    feasible, the later ones in batches of consecutive levels up to 2e9
+    closed-form visits each (small levels share a batch, large ones run alone
+    so the search stops at the first feasible one).  The reference's
+    first-feasible-level rule is applied afterwards, so the result and the
+    stats are identical either way.
     """
     if num_nodes < 1 or devices_per_node < 1 or batch_size < 1:
         raise InvalidArgs("node count, devices per node and batch size must be at least 1")
