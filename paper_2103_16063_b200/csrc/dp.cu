@@ -321,16 +321,9 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
     auto over = [&](double x, double y) {
         return bounded && __dadd_rn(dmax_ref(x, lbf), dmax_ref(y, lbb)) > U;
     };
-    // The whole cell above the bound: every entry (x, y) has x >= plf and
-    // y >= plb, the same two lower bounds for the s stages over [0, b) with d
-    // devices (devp = d - (s - 1) the most one of them can hold).  Then no
-    // predecessor is scanned; the cell's emptiness and zero-share flags come
-    // from the prefix counts below.
-    bool cell_dead = false;
-    if (bounded && s > 1) {
-        double plf, plb;
-        if (prefix_bounds<DERIVED>(B, cd, keyidx, s, b, d, plf, plb)) cell_dead = over(plf, plb);
-    }
+    // (Cells whose whole frontier is above the bound -- the prefix lower bound,
+    // see k_dp_triage -- never get here: bounded batches run only the cells
+    // k_dp_triage listed.)
     int n = 0;
     bool ovf = false;
     bool zero = false;
@@ -366,26 +359,6 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
         // is order-independent (see top), so this order is as good as the
         // reference's.
         const int base = s - 1;
-        if (bounded) {
-            // the reference's emptiness and zero-share flag of this cell from
-            // the previous level's non-empty prefix counts: some non-empty
-            // (b' < b, d') with m == 0, and some with a feasible span (b', b)
-            // -- b' >= first feasible lo, feasibility being suffix-closed in
-            // b' for every key of a bounded batch (api.cu checks it)
-            const int32_t *rp = B.reach_pre[prv] + cd.val_off;
-            bool zl = false, rl = false;
-            for (int dp = base + lane; dp < d; dp += 32) {
-                const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
-                const int32_t upto = col[b - 1];
-                if (upto == 0) continue;
-                const int kk = keyidx[d - dp];
-                if (kk < 0) { zl = true; continue; }
-                const int x = max(base, B.key_ffb[kk][b]);
-                if (x <= b - 1 && upto > (x > base ? col[x - 1] : 0)) rl = true;
-            }
-            zero = __any_sync(0xffffffffu, zl);
-            reach = __any_sync(0xffffffffu, rl);
-        }
         const uint8_t *pcnt = B.val_cnt[prv] + cd.val_off;
         const uint32_t *poff = B.val_off[prv] + cd.val_off;
         const double *qtf = B.pool_tf[prv] + cd.vpool_base;
@@ -402,7 +375,7 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
         const int dpn = B.dpn;
         const bool multi_node = B.num_nodes > 1;
         int rem = (int)((unsigned)(d - 1) % (unsigned)dpn);
-        for (int dp = d - 1; !cell_dead && dp >= base; --dp, rem = rem == 0 ? dpn - 1 : rem - 1) {
+        for (int dp = d - 1; dp >= base; --dp, rem = rem == 0 ? dpn - 1 : rem - 1) {
             const int lo_col = cmin[dp - base];
             const int hi_col = cmax[dp - base];
             if (lo_col > hi_col || lo_col >= b) continue;           // no predecessor cell
@@ -594,6 +567,29 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
             atomicAdd(&B.counters[4 + FMAX + 2], (unsigned long long)a);
             atomicAdd(&B.counters[4 + FMAX + 3], (unsigned long long)bw);
         }
+    }
+    if (bounded && s > 1 && n == 0) {
+        // A bounded cell left without entries: the reference's emptiness and
+        // zero-share flag come from the previous level's non-empty prefix
+        // counts -- some non-empty (b' < b, d') with m == 0, and some with a
+        // feasible span (b', b): b' >= first feasible lo, feasibility being
+        // suffix-closed in b' for every key of a bounded batch (api.cu checks
+        // it).  (With entries the cell is non-empty and the zero-share flag
+        // is never read: the visit scan only asks it of empty cells.)
+        const int base = s - 1;
+        const int32_t *rp = B.reach_pre[prv] + cd.val_off;
+        bool zl = false, rl = false;
+        for (int dp = base + lane; dp < d; dp += 32) {
+            const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
+            const int32_t upto = col[b - 1];
+            if (upto == 0) continue;
+            const int kk = keyidx[d - dp];
+            if (kk < 0) { zl = true; continue; }
+            const int x = max(base, B.key_ffb[kk][b]);
+            if (x <= b - 1 && upto > (x > base ? col[x - 1] : 0)) rl = true;
+        }
+        zero = __any_sync(0xffffffffu, zl);
+        reach = __any_sync(0xffffffffu, rl);
     }
     const bool any_zero = __any_sync(0xffffffffu, zero);
 
