@@ -52,6 +52,7 @@ struct DevAtoms {
     const uint8_t *ov_has;          // null without a cost table
     const double *ov_tf, *ov_tb;
     const int64_t *ov_act;
+    const int32_t *nbr_off, *nbr;   // sorted(succ | pred) per atom (blocks.py:87-88)
 };
 
 // per-task time at m = 1, cost-table entry first (costs.py:130-140)
@@ -153,13 +154,12 @@ __device__ __forceinline__ bool bit_at(const uint32_t *bits, int i) {
     return (bits[i >> 5] >> (i & 31)) & 1u;
 }
 
-__global__ void k_eval_sets_warp(DevAtoms A, DevLevels L, const SetDesc *sets, int nsets,
-                                 uint32_t *scratch, int words, int64_t *out_mem,
-                                 int32_t *out_count, uint8_t *out_convex) {
-    const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+// One warp evaluates set s: member count, memory, convexity (bits: the
+// warp's bitmap scratch, >= n/32 + 1 words).  All lanes return the results.
+__device__ __noinline__ void eval_set_warp(const DevAtoms &A, const DevLevels &L, const SetDesc s,
+                                           uint32_t *bits, int &count_out, int64_t &mem_out,
+                                           bool &convex_out) {
     const int lane = threadIdx.x & 31;
-    if (i >= nsets) return;                                   // warp-uniform
-    const SetDesc s = sets[i];
     const int n = L.n;
     const int32_t *offa = L.goff + (int64_t)s.la * (n + 1);
     const int32_t *ata = L.gat + (int64_t)s.la * n;
@@ -219,17 +219,14 @@ __global__ void k_eval_sets_warp(DevAtoms A, DevLevels L, const SetDesc *sets, i
         mfp = m2 > mfp ? m2 : mfp;
     }
     if (count == 0) {
-        if (lane == 0) {
-            out_count[i] = 0;
-            out_mem[i] = 0;
-            out_convex[i] = 1;
-        }
+        count_out = 0;
+        mem_out = 0;
+        convex_out = true;
         return;
     }
     bool convex = true;
     if (hi - lo + 1 != count) {
         const int span = hi - lo + 1;
-        uint32_t *bits = scratch + (int64_t)i * words;
         for (int w = lane; w < (span + 31) / 32; w += 32) bits[w] = 0u;
         __syncwarp();
         for (int base = lo + 1; base <= hi; base += 32) {
@@ -282,10 +279,24 @@ __global__ void k_eval_sets_warp(DevAtoms A, DevLevels L, const SetDesc *sets, i
             __syncwarp();
         }
     }
-    if (lane == 0) {
+    count_out = count;
+    const double memd = __dadd_rn(__dmul_rn((double)param, A.factor), (double)(inb + mfp));
+    mem_out = (int64_t)memd;
+    convex_out = convex;
+}
+
+__global__ void k_eval_sets_warp(DevAtoms A, DevLevels L, const SetDesc *sets, int nsets,
+                                 uint32_t *scratch, int words, int64_t *out_mem,
+                                 int32_t *out_count, uint8_t *out_convex) {
+    const int i = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (i >= nsets) return;                                   // warp-uniform
+    int count;
+    int64_t mem;
+    bool convex;
+    eval_set_warp(A, L, sets[i], scratch + (int64_t)i * words, count, mem, convex);
+    if ((threadIdx.x & 31) == 0) {
         out_count[i] = count;
-        const double memd = __dadd_rn(__dmul_rn((double)param, A.factor), (double)(inb + mfp));
-        out_mem[i] = (int64_t)memd;
+        out_mem[i] = mem;
         out_convex[i] = convex ? 1 : 0;
     }
 }
@@ -392,6 +403,300 @@ __global__ void k_move_savings(DevAtoms A, DevLevels L, const MoveDesc *mv, int 
     out[i] = saving;
 }
 
+// ---------------------------------------------------------------- refinement
+// _uncoarsen (blocks.py:173-232) as one resident CTA: no host round trip per
+// pair.  For each transition level li (coarsest first) the pairs are walked
+// in order; a pair moves one side (mover, a level-li group) into a
+// neighbouring level-li group's block when that strictly cuts the top-level
+// traffic and both touched groups stay convex and inside memory at every
+// coarser level.  The reference tests fit first and saving second; the
+// choice is the same if the saving is computed first: the answer is the
+// candidate with the largest positive saving among those that fit, the
+// earliest (side v before w, target index ascending) on ties.  So the CTA
+//   1. computes, for a window of pairs at once (one warp per pair side), the
+//      best positive-saving candidate of every side -- savings depend only on
+//      the top-level labels, which change only when a move is applied;
+//   2. takes the first pair of the window with a positive candidate and tests
+//      that candidate's fit (2 sets per coarser level, one warp each); if it
+//      does not fit, the next candidate in (saving desc, side, target) order
+//      is recomputed and tested, and so on;
+//   3. applies an accepted move on the device (relabel the mover's atoms and
+//      splice its atoms between the two groups' member lists at every coarser
+//      level) and restarts the window after the pair; a pair without an
+//      accepted move leaves the state as it was, so the window's other
+//      results stay valid.
+// Member order inside a group is free at levels above li (every set
+// predicate is order-independent), so the splice appends the mover.
+constexpr int RF_THREADS = 512;
+constexpr int RF_WARPS = RF_THREADS / 32;
+constexpr int RF_WMAX = 512;          // pairs per window (2 sides each)
+
+struct RefineArgs {
+    int ntrans, top;
+    const int32_t *pair_off;          // [ntrans + 1]
+    const int2 *pairs;                // level-li group indices (v, w)
+    int32_t *grp, *goff, *gat;        // the level arrays (written by moves)
+    uint32_t *bits;                   // [RF_WARPS][words] convexity bitmaps
+    int words;
+    int32_t *tmp;                     // [RF_WARPS][n] splice scratch
+    int32_t *src, *dst;               // [top] a move's groups per coarser level
+    int64_t budget;
+    long long *stats;                 // windows, side evaluations, fit tests, moves
+};
+
+struct Cand {
+    long long s;                      // saving; 0 = none
+    int side, ti;
+};
+
+// a ranks before b: larger saving, then side v, then smaller target index
+__device__ __forceinline__ bool cand_before(const Cand &a, const Cand &b) {
+    if (a.s != b.s) return a.s > b.s;
+    if (a.side != b.side) return a.side < b.side;
+    return a.ti < b.ti;
+}
+
+// the warp's share of base_traffic - traffic(moved) for level-li group `mover`
+// moving into top-level block `dest` (k_move_savings' sum, lanes over atoms)
+__device__ long long move_saving_warp(const DevAtoms &A, const DevLevels &L, int li, int top,
+                                      int mover, int dest) {
+    const int lane = threadIdx.x & 31;
+    const int32_t *gl = L.grp + (int64_t)li * L.n;
+    const int32_t *gt = L.grp + (int64_t)top * L.n;
+    const int32_t *off = L.goff + (int64_t)li * (L.n + 1);
+    const int32_t *at = L.gat + (int64_t)li * L.n;
+    long long saving = 0;
+    for (int j = off[mover] + lane; j < off[mover + 1]; j += 32) {
+        const int x = at[j];
+        for (int q = A.atom_tr_off[x]; q < A.atom_tr_off[x + 1]; ++q) {
+            const int e = A.atom_tr[q];
+            const int owner = A.tr_owner[e];
+            int first = gl[owner] == mover ? owner : 0x7fffffff;
+            for (int r = A.tr_cons_off[e]; r < A.tr_cons_off[e + 1]; ++r) {
+                const int c = A.tr_cons[r];
+                if (gl[c] == mover && c < first) first = c;
+            }
+            if (first != x) continue;
+            const int home0 = gt[owner];
+            const int home1 = gl[owner] == mover ? dest : home0;
+            int before = 0, after = 0;
+            const int c0 = A.tr_cons_off[e], c1 = A.tr_cons_off[e + 1];
+            for (int r = c0; r < c1; ++r) {
+                const int c = A.tr_cons[r];
+                const int b0 = gt[c];
+                const int b1 = gl[c] == mover ? dest : b0;
+                bool seen0 = b0 == home0, seen1 = b1 == home1;
+                for (int u = c0; u < r && !(seen0 && seen1); ++u) {
+                    const int cu = A.tr_cons[u];
+                    if (gt[cu] == b0) seen0 = true;
+                    if ((gl[cu] == mover ? dest : gt[cu]) == b1) seen1 = true;
+                }
+                before += !seen0;
+                after += !seen1;
+            }
+            saving += A.tr_size[e] * (long long)(before - after);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) saving += __shfl_xor_sync(0xffffffffu, saving, o);
+    return saving;
+}
+
+// Best positive-saving candidate of one pair side ranking after `after`
+// (after.s < 0: no bound).  Targets are visited in ascending index: each
+// step takes the smallest neighbouring group index above the last one.
+__device__ Cand side_best(const DevAtoms &A, const DevLevels &L, int li, int top, int mover,
+                          int side, const Cand &after) {
+    const int lane = threadIdx.x & 31;
+    const int32_t *gl = L.grp + (int64_t)li * L.n;
+    const int32_t *gt = L.grp + (int64_t)top * L.n;
+    const int32_t *off = L.goff + (int64_t)li * (L.n + 1);
+    const int32_t *at = L.gat + (int64_t)li * L.n;
+    const int here = gt[at[off[mover]]];
+    Cand best{0, side, 0x7fffffff};
+    int last = -1;
+    for (;;) {
+        int cur = 0x7fffffff;
+        for (int j = off[mover] + lane; j < off[mover + 1]; j += 32) {
+            const int x = at[j];
+            for (int r = A.nbr_off[x]; r < A.nbr_off[x + 1]; ++r) {
+                const int t = gl[A.nbr[r]];
+                if (t > last && t < cur && t != mover) cur = t;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cur = min(cur, __shfl_xor_sync(0xffffffffu, cur, o));
+        if (cur == 0x7fffffff) break;
+        last = cur;
+        const int dest = gt[at[off[cur]]];
+        if (dest == here) continue;                              // blocks.py:189
+        const Cand c{move_saving_warp(A, L, li, top, mover, dest), side, cur};
+        if (c.s > 0 && (after.s < 0 || cand_before(after, c)) && (best.s == 0 || cand_before(c, best)))
+            best = c;
+    }
+    return best;
+}
+
+// move `cnt` atoms (mover) from group src to group dst in one level's CSR
+// (labels already rewritten): the groups between the two shift by cnt
+__device__ void splice_warp(int32_t *off, int32_t *at, const int32_t *grp, int src, int dst,
+                            const int32_t *mover, int cnt, int32_t *tmp) {
+    const int lane = threadIdx.x & 31;
+    const int s0 = off[src], s1 = off[src + 1], d0 = off[dst], d1 = off[dst + 1];
+    const int base = min(s0, d0), end = max(s1, d1);
+    int w = 0;
+    auto copy_range = [&](int b, int e) {
+        for (int j = b + lane; j < e; j += 32) tmp[w + j - b] = at[j];
+        w += e - b;
+    };
+    auto keep_src = [&]() {                                      // src minus the mover
+        for (int j0 = s0; j0 < s1; j0 += 32) {
+            const int j = j0 + lane;
+            const int x = j < s1 ? at[j] : -1;
+            const bool keep = j < s1 && grp[x] == src;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) tmp[w + __popc(m & ((1u << lane) - 1u))] = x;
+            w += __popc(m);
+        }
+    };
+    auto add_mover = [&]() {
+        for (int j = lane; j < cnt; j += 32) tmp[w + j] = mover[j];
+        w += cnt;
+    };
+    if (src < dst) {
+        keep_src();
+        copy_range(s1, d1);
+        add_mover();
+    } else {
+        copy_range(d0, d1);
+        add_mover();
+        copy_range(d1, s0);
+        keep_src();
+    }
+    __syncwarp();
+    for (int j = lane; j < end - base; j += 32) at[base + j] = tmp[j];
+    const int lo = min(src, dst), hi = max(src, dst), delta = src < dst ? -cnt : cnt;
+    for (int g = lo + 1 + lane; g <= hi; g += 32) off[g] += delta;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(RF_THREADS, 1) k_refine(DevAtoms A, DevLevels L, RefineArgs R) {
+    __shared__ long long s_sav[2 * RF_WMAX];
+    __shared__ int s_ti[2 * RF_WMAX];
+    __shared__ int s_bad, s_first;
+    __shared__ Cand s_next[2];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n = L.n;
+    uint32_t *bits = R.bits + (int64_t)warp * R.words;
+    long long n_win = 0, n_side = 0, n_fit = 0, n_move = 0;
+    for (int li = R.ntrans - 1; li >= 0; --li) {
+        const int2 *pairs = R.pairs + R.pair_off[li];
+        const int np = R.pair_off[li + 1] - R.pair_off[li];
+        const int nlev = R.top - li;
+        const int32_t *offl = L.goff + (int64_t)li * (n + 1);
+        const int32_t *atl = L.gat + (int64_t)li * n;
+        int p = 0, ws = 0, we = 0, W = RF_WARPS / 2;
+        while (p < np) {
+            if (p >= we) {                                       // 1. a new window
+                ws = p;
+                we = min(np, p + W);
+                for (int it = warp; it < 2 * (we - ws); it += RF_WARPS) {
+                    const int2 pr = pairs[ws + (it >> 1)];
+                    const Cand c = side_best(A, L, li, R.top, (it & 1) ? pr.y : pr.x, it & 1,
+                                             Cand{-1, 0, 0});
+                    if (lane == 0) {
+                        s_sav[it] = c.s;
+                        s_ti[it] = c.ti;
+                    }
+                }
+                ++n_win;
+                n_side += 2 * (we - ws);
+            }
+            if (tid == 0) s_first = 0x7fffffff;
+            __syncthreads();
+            for (int it = 2 * (p - ws) + tid; it < 2 * (we - ws); it += RF_THREADS)
+                if (s_sav[it] > 0) atomicMin(&s_first, it >> 1);
+            __syncthreads();
+            const int fq = s_first;
+            __syncthreads();                                     // s_first is reset next
+            if (fq == 0x7fffffff) {                              // no candidate in the window
+                p = we;
+                W = min(2 * W, RF_WMAX);
+                continue;
+            }
+            // 2. the first pair with a candidate: test candidates in rank order
+            const int q = ws + fq;
+            const int2 pr = pairs[q];
+            Cand c0{s_sav[2 * fq], 0, s_ti[2 * fq]}, c1{s_sav[2 * fq + 1], 1, s_ti[2 * fq + 1]};
+            Cand c = c0.s > 0 && (c1.s <= 0 || cand_before(c0, c1)) ? c0 : c1;
+            bool moved = false;
+            while (c.s > 0) {
+                const int mv = c.side ? pr.y : pr.x;
+                const int a0 = atl[offl[mv]], t0 = atl[offl[c.ti]];
+                for (int e = tid; e < nlev; e += RF_THREADS) {
+                    const int ell = li + 1 + e;
+                    R.src[e] = L.grp[(int64_t)ell * n + a0];
+                    R.dst[e] = L.grp[(int64_t)ell * n + t0];
+                }
+                if (tid == 0) s_bad = 0;
+                __syncthreads();
+                for (int k = warp; k < 2 * nlev; k += RF_WARPS) {    // _move_fits (blocks.py:206-221)
+                    const int e = k >> 1, ell = li + 1 + e;
+                    const SetDesc sd = (k & 1) ? SetDesc{ell, R.dst[e], li, mv, 0}     // grown
+                                               : SetDesc{ell, R.src[e], li, mv, 1};    // shrunk
+                    int cnt;
+                    int64_t mem;
+                    bool convex;
+                    eval_set_warp(A, L, sd, bits, cnt, mem, convex);
+                    const bool ok = convex && mem < R.budget && ((k & 1) || cnt > 0);
+                    if (lane == 0 && !ok) s_bad = 1;
+                }
+                ++n_fit;
+                __syncthreads();
+                if (!s_bad) {                                    // 3. _apply_move (blocks.py:224-232)
+                    const int m0 = offl[mv], cnt = offl[mv + 1] - m0;
+                    for (int k = tid; k < nlev * cnt; k += RF_THREADS) {
+                        const int e = k / cnt;
+                        R.grp[(int64_t)(li + 1 + e) * n + atl[m0 + k % cnt]] = R.dst[e];
+                    }
+                    __syncthreads();
+                    for (int e = warp; e < nlev; e += RF_WARPS) {
+                        const int ell = li + 1 + e;
+                        splice_warp(R.goff + (int64_t)ell * (n + 1), R.gat + (int64_t)ell * n,
+                                    R.grp + (int64_t)ell * n, R.src[e], R.dst[e], atl + m0, cnt,
+                                    R.tmp + (int64_t)warp * n);
+                    }
+                    __syncthreads();
+                    moved = true;
+                    ++n_move;
+                    break;
+                }
+                // next candidate of this pair after the rejected one
+                if (warp < 2) {
+                    const Cand b = side_best(A, L, li, R.top, warp ? pr.y : pr.x, warp, c);
+                    if (lane == 0) s_next[warp] = b;
+                }
+                __syncthreads();
+                const Cand b0 = s_next[0], b1 = s_next[1];
+                __syncthreads();
+                c = b0.s > 0 && (b1.s <= 0 || cand_before(b0, b1)) ? b0 : b1;
+                n_side += 2;
+            }
+            p = q + 1;
+            if (moved) {                                         // later savings changed
+                we = p;
+                W = RF_WARPS / 2;
+            }
+        }
+    }
+    if (tid == 0) {
+        R.stats[0] = n_win;
+        R.stats[1] = n_side;
+        R.stats[2] = n_fit;
+        R.stats[3] = n_move;
+    }
+}
+
 // ====================================================================== host side
 namespace {
 
@@ -449,6 +754,8 @@ struct Coarsener {
         const bool ov = H->ov_has != nullptr;
         size_t i24 = ov ? add(H->ov_has, T) : 0, i25 = ov ? add(H->ov_tf, 8 * T) : 0;
         size_t i26 = ov ? add(H->ov_tb, 8 * T) : 0, i27 = ov ? add(H->ov_act, 8 * T) : 0;
+        const size_t nnb = H->nbr_off[N];
+        size_t i28 = add(H->nbr_off, 4 * (N + 1)), i29 = add(H->nbr, 4 * nnb);
         CUDA_TRY(ctx, atoms_d.ensure(total + 64));
         std::vector<char> staging(total + 64, 0);
         for (auto &p : parts)
@@ -492,6 +799,8 @@ struct Coarsener {
         A.ov_tf = ov ? (const double *)at(i25) : nullptr;
         A.ov_tb = ov ? (const double *)at(i26) : nullptr;
         A.ov_act = ov ? (const int64_t *)at(i27) : nullptr;
+        A.nbr_off = (const int32_t *)at(i28);
+        A.nbr = (const int32_t *)at(i29);
         return PC_OK;
     }
 
@@ -630,6 +939,73 @@ struct Coarsener {
         return PC_OK;
     }
 };
+
+std::vector<int> member_map(int n, const std::vector<std::vector<int>> &level);
+void sort_by_first(std::vector<std::vector<int>> &level);
+
+using Transitions = std::vector<std::vector<std::pair<std::vector<int>, std::vector<int>>>>;
+
+// _uncoarsen on the device (k_refine): the recorded merges go up as level
+// group-index pairs, one launch walks every level, and the top level's labels
+// come back (the only level used afterwards).  stats: windows, side
+// evaluations, fit tests, moves.
+int refine_on_device(Coarsener &co, const Transitions &tr, long long stats[4]) {
+    pc_ctx *ctx = co.ctx;
+    const int n = co.n, top = (int)co.levels.size() - 1, nt = (int)tr.size();
+    for (int l = 0; l <= top; ++l)
+        if (l < (int)co.dirty.size() && co.dirty[l])
+            if (int rc = co.upload_level(l, co.levels[l])) return rc;
+    std::vector<int32_t> head(nt + 1, 0);
+    std::vector<int2> pairs;
+    for (int li = 0; li < nt; ++li) {
+        const std::vector<int> gm = member_map(n, co.levels[li]);
+        for (const auto &vw : tr[li]) pairs.push_back(make_int2(gm[vw.first[0]], gm[vw.second[0]]));
+        head[li + 1] = (int32_t)pairs.size();
+    }
+    const int words = (n + 31) / 32 + 1;
+    size_t total = 0;
+    auto carve = [&](size_t bytes) { const size_t o = (total + 15) & ~size_t(15); total = o + bytes; return o; };
+    const size_t o_stats = carve(4 * sizeof(long long)), o_head = carve(4 * head.size());
+    const size_t o_pairs = carve(sizeof(int2) * pairs.size()), o_src = carve(4 * (size_t)top);
+    const size_t o_dst = carve(4 * (size_t)top), o_bits = carve(4 * (size_t)RF_WARPS * words);
+    const size_t o_tmp = carve(4 * (size_t)RF_WARPS * n), o_lab = carve(4 * (size_t)n);
+    CUDA_TRY(ctx, ctx->cb.refine_d.ensure(total + 64));
+    char *b = ctx->cb.refine_d.as<char>();
+    std::vector<char> up(o_src - o_head);
+    memcpy(up.data(), head.data(), 4 * head.size());
+    if (!pairs.empty()) memcpy(up.data() + (o_pairs - o_head), pairs.data(), sizeof(int2) * pairs.size());
+    CUDA_TRY(ctx, cudaMemcpyAsync(b + o_head, up.data(), up.size(), cudaMemcpyHostToDevice, ctx->st));
+    RefineArgs R;
+    R.ntrans = nt;
+    R.top = top;
+    R.pair_off = (const int32_t *)(b + o_head);
+    R.pairs = (const int2 *)(b + o_pairs);
+    R.grp = co.lev_grp.as<int32_t>();
+    R.goff = co.lev_off.as<int32_t>();
+    R.gat = co.lev_at.as<int32_t>();
+    R.bits = (uint32_t *)(b + o_bits);
+    R.words = words;
+    R.tmp = (int32_t *)(b + o_tmp);
+    R.src = (int32_t *)(b + o_src);
+    R.dst = (int32_t *)(b + o_dst);
+    R.budget = co.H->budget;
+    R.stats = (long long *)(b + o_stats);
+    k_refine<<<1, RF_THREADS, 0, ctx->st>>>(co.A, co.dev_levels(), R);
+    ctx->launches++;
+    if (int rc = check_launch(ctx, "refine")) return rc;
+    std::vector<int32_t> lab(n);
+    CUDA_TRY(ctx, cudaMemcpyAsync(lab.data(), co.lev_grp.as<int32_t>() + (size_t)top * n, 4 * (size_t)n,
+                                  cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(stats, b + o_stats, 4 * sizeof(long long), cudaMemcpyDeviceToHost, ctx->st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+    // the top level from its labels; levels 1..top-1 are stale on the host
+    // from here (moves changed them on the device) and are not read again
+    std::vector<std::vector<int>> groups(co.levels[top].size());
+    for (int x = 0; x < n; ++x) groups[lab[x]].push_back(x);
+    sort_by_first(groups);
+    co.levels[top] = groups;
+    return PC_OK;
+}
 
 std::vector<int> member_map(int n, const std::vector<std::vector<int>> &level) {
     std::vector<int> m(n, -1);
@@ -778,13 +1154,21 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
     }
 
     phase("coarsen");
-    // ---- refinement: speculative rounds over the recorded merges (blocks.py:173-232)
     const int top = (int)co.levels.size() - 1;
+    const bool host_refine = getenv("PIPECUT_B200_HOST_REFINE") != nullptr;
+    if (!transitions.empty() && !host_refine) {
+        long long st[4];
+        if (int rc = refine_on_device(co, transitions, st)) return rc;
+        if (phase_times)
+            fprintf(stderr, "[pipecut_b200] refine (device): %lld windows, %lld side evaluations, "
+                            "%lld fit tests, %lld moves\n", st[0], st[1], st[2], st[3]);
+    }
+    // ---- refinement: speculative rounds over the recorded merges (blocks.py:173-232)
     long long n_rounds = 0, n_sets = 0, n_moves = 0;
     std::vector<std::vector<int>> map_cache(co.levels.size());
     std::vector<char> map_valid(co.levels.size(), 0);
     double t_dev = 0.0;
-    for (int li = (int)transitions.size() - 1; li >= 0; --li) {
+    for (int li = host_refine ? (int)transitions.size() - 1 : -1; li >= 0; --li) {
         const auto &pairs = transitions[li];
         // Rounds evaluate a window of pairs from p on (48, doubling while a
         // window holds no move): pairs past the first move would be evaluated

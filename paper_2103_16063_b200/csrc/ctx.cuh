@@ -40,6 +40,7 @@ struct DBuf {
 // pinned staging would otherwise cost more than a small coarsening)
 struct CoarsenBufs {
     DBuf atoms_d, lev_grp, lev_off, lev_at, sets_d, scratch_d, out_d, comp_d, mv_d;
+    DBuf refine_d;            // device refinement: pairs, scratch, labels out
     int lev_cap = 0;          // level slots valid for lev_n atoms
     int lev_n = -1;
     int32_t *pin = nullptr;   // pinned level staging [lev_cap][3 * lev_n + 1]
