@@ -324,37 +324,56 @@ __global__ void k_group_comps(DevLevels L, int level, int ngroups, const double 
     out[g] = f;
 }
 
-// CostModel.profile(group, 1, checkpointing=True) for every group of a level:
-// time folds over the group's tasks in global sorted node-id order.
-__global__ void k_group_profiles(DevAtoms A, DevLevels L, int level, int ngroups, int single_atoms,
-                                 double *out_tf, double *out_tb, double *out_comp, int64_t *out_mem) {
+// CostModel.profile(atom, 1, checkpointing=True) for every atom (level 0)
+__global__ void k_atom_profiles(DevAtoms A, DevLevels L, int level, int ngroups, double *out_tf,
+                                double *out_tb, double *out_comp, int64_t *out_mem) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= ngroups) return;
     double tf = 0.0, tb = 0.0;
-    if (single_atoms) {
-        const int x = L.gat[(int64_t)level * L.n + L.goff[(int64_t)level * (L.n + 1) + g]];
-        for (int q = A.atom_task_off[x]; q < A.atom_task_off[x + 1]; ++q) {
-            const int t = A.atom_tasks[q];
-            double v, w;
-            atom_task_times(A, t, v, w);
-            tf = __dadd_rn(tf, v);
-            tb = __dadd_rn(tb, w);
-        }
-    } else {
-        const int32_t *grp = L.grp + (int64_t)level * L.n;
-        for (int t = 0; t < A.T; ++t) {
-            if (grp[A.task_atom[t]] != g) continue;
-            double v, w;
-            atom_task_times(A, t, v, w);
-            tf = __dadd_rn(tf, v);
-            tb = __dadd_rn(tb, w);
-        }
+    const int x = L.gat[(int64_t)level * L.n + L.goff[(int64_t)level * (L.n + 1) + g]];
+    for (int q = A.atom_task_off[x]; q < A.atom_task_off[x + 1]; ++q) {
+        const int t = A.atom_tasks[q];
+        double v, w;
+        atom_task_times(A, t, v, w);
+        tf = __dadd_rn(tf, v);
+        tb = __dadd_rn(tb, w);
     }
     out_tf[g] = tf;
     out_tb[g] = tb;
     out_comp[g] = __dadd_rn(tf, tb);                      // blocks.py:93
-    const SetDesc s{level, g, level, -1, 0};
-    out_mem[g] = set_mem(A, L, s);
+    out_mem[g] = set_mem(A, L, SetDesc{level, g, level, -1, 0});
+}
+
+// CostModel.profile(group, 1, checkpointing=True) for every group of a level,
+// one warp per group: the time folds over the group's tasks in global sorted
+// node-id order -- the warp scans the tasks 32 at a time, a ballot picks the
+// members, and their times are added one by one in index order.
+__global__ void k_group_profiles(DevAtoms A, DevLevels L, int level, int ngroups, double *out_tf,
+                                 double *out_tb, double *out_comp, int64_t *out_mem) {
+    const int g = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (g >= ngroups) return;                             // warp-uniform
+    const int32_t *grp = L.grp + (int64_t)level * L.n;
+    double tf = 0.0, tb = 0.0;
+    for (int base = 0; base < A.T; base += 32) {
+        const int t = base + lane;
+        const bool in = t < A.T && grp[A.task_atom[t]] == g;
+        double v = 0.0, w = 0.0;
+        if (in) atom_task_times(A, t, v, w);
+        unsigned m = __ballot_sync(0xffffffffu, in);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            tf = __dadd_rn(tf, __shfl_sync(0xffffffffu, v, src));
+            tb = __dadd_rn(tb, __shfl_sync(0xffffffffu, w, src));
+            m &= m - 1;
+        }
+    }
+    if (lane == 0) {
+        out_tf[g] = tf;
+        out_tb[g] = tb;
+        out_comp[g] = __dadd_rn(tf, tb);                  // blocks.py:93
+        out_mem[g] = set_mem(A, L, SetDesc{level, g, level, -1, 0});
+    }
 }
 
 // Traffic saving of moving level-li group `mover` into top-level block `dest`
@@ -856,24 +875,24 @@ struct Coarsener {
         return PC_OK;
     }
 
-    int comps(int l, int ngroups, std::vector<double> &out) {
-        CUDA_TRY(ctx, out_d.ensure(sizeof(double) * ngroups + 64));
-        k_group_comps<<<(ngroups + 127) / 128, 128, 0, ctx->st>>>(dev_levels(), l, ngroups, comp_d.as<double>(),
-                                                                 out_d.as<double>());
-        ctx->launches++;
-        if (int rc = check_launch(ctx, "group_comps")) return rc;
-        out.resize(ngroups);
-        CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), out_d.p, sizeof(double) * ngroups, cudaMemcpyDeviceToHost, ctx->st));
-        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
-        return PC_OK;
+    // pinned read-back staging (pageable D2H copies would each block)
+    char *pinned_out(size_t bytes) {
+        CoarsenBufs &cb = ctx->cb;
+        if (cb.pout_bytes < bytes) {
+            cudaStreamSynchronize(ctx->st);
+            if (cb.pout) cudaFreeHost(cb.pout);
+            cb.pout = nullptr;
+            cb.pout_bytes = 0;
+            const size_t want = std::max(bytes, (size_t)1 << 20);
+            if (cudaMallocHost(&cb.pout, want) != cudaSuccess) return nullptr;
+            cb.pout_bytes = want;
+        }
+        return cb.pout;
     }
 
-    int eval(const std::vector<SetDesc> &sets, std::vector<int64_t> &mem, std::vector<int32_t> &count,
-             std::vector<uint8_t> &convex) {
+    // k_eval_sets over `sets` (launch only; outputs in out_d)
+    int eval_launch(const std::vector<SetDesc> &sets) {
         const int ns = (int)sets.size();
-        mem.assign(ns, 0);
-        count.assign(ns, 0);
-        convex.assign(ns, 0);
         if (!ns) return PC_OK;
         const int words = (n + 31) / 32 + 1;
         CUDA_TRY(ctx, sets_d.ensure(sizeof(SetDesc) * ns));
@@ -886,11 +905,53 @@ struct Coarsener {
         k_eval_sets_warp<<<(unsigned)(((int64_t)ns * 32 + 127) / 128), 128, 0, ctx->st>>>(
             A, dev_levels(), sets_d.as<SetDesc>(), ns, scratch_d.as<uint32_t>(), words, om, oc, ov);
         ctx->launches++;
-        if (int rc = check_launch(ctx, "eval_sets")) return rc;
-        CUDA_TRY(ctx, cudaMemcpyAsync(mem.data(), om, 8 * (size_t)ns, cudaMemcpyDeviceToHost, ctx->st));
-        CUDA_TRY(ctx, cudaMemcpyAsync(count.data(), oc, 4 * (size_t)ns, cudaMemcpyDeviceToHost, ctx->st));
-        CUDA_TRY(ctx, cudaMemcpyAsync(convex.data(), ov, (size_t)ns, cudaMemcpyDeviceToHost, ctx->st));
+        return check_launch(ctx, "eval_sets");
+    }
+
+    // group compute times of level l and the set evaluations, one sync
+    int comps_eval(int l, int ngroups, std::vector<double> &gc, const std::vector<SetDesc> &sets,
+                   std::vector<int64_t> &mem, std::vector<int32_t> &count, std::vector<uint8_t> &convex) {
+        const size_t ns = sets.size();
+        CUDA_TRY(ctx, ctx->cb.gc_d.ensure(sizeof(double) * ngroups + 64));
+        k_group_comps<<<(ngroups + 127) / 128, 128, 0, ctx->st>>>(dev_levels(), l, ngroups, comp_d.as<double>(),
+                                                                 ctx->cb.gc_d.as<double>());
+        ctx->launches++;
+        if (int rc = check_launch(ctx, "group_comps")) return rc;
+        if (int rc = eval_launch(sets)) return rc;
+        const size_t gbytes = sizeof(double) * (size_t)ngroups, sbytes = 13 * ns;
+        char *h = pinned_out(gbytes + sbytes + 16);
+        if (!h) return fail(ctx, PC_ERR_CUDA, "pinned staging");
+        CUDA_TRY(ctx, cudaMemcpyAsync(h, ctx->cb.gc_d.p, gbytes, cudaMemcpyDeviceToHost, ctx->st));
+        if (ns) CUDA_TRY(ctx, cudaMemcpyAsync(h + gbytes, out_d.p, sbytes, cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        gc.assign((const double *)h, (const double *)h + ngroups);
+        const int64_t *om = (const int64_t *)(h + gbytes);
+        const int32_t *oc = (const int32_t *)(om + ns);
+        const uint8_t *ov = (const uint8_t *)(oc + ns);
+        mem.assign(om, om + ns);
+        count.assign(oc, oc + ns);
+        convex.assign(ov, ov + ns);
+        return PC_OK;
+    }
+
+    int eval(const std::vector<SetDesc> &sets, std::vector<int64_t> &mem, std::vector<int32_t> &count,
+             std::vector<uint8_t> &convex) {
+        const size_t ns = sets.size();
+        mem.assign(ns, 0);
+        count.assign(ns, 0);
+        convex.assign(ns, 0);
+        if (!ns) return PC_OK;
+        if (int rc = eval_launch(sets)) return rc;
+        char *h = pinned_out(13 * ns + 16);
+        if (!h) return fail(ctx, PC_ERR_CUDA, "pinned staging");
+        CUDA_TRY(ctx, cudaMemcpyAsync(h, out_d.p, 13 * ns, cudaMemcpyDeviceToHost, ctx->st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        const int64_t *om = (const int64_t *)h;
+        const int32_t *oc = (const int32_t *)(om + ns);
+        const uint8_t *ov = (const uint8_t *)(oc + ns);
+        mem.assign(om, om + ns);
+        count.assign(oc, oc + ns);
+        convex.assign(ov, ov + ns);
         return PC_OK;
     }
 
@@ -922,20 +983,23 @@ struct Coarsener {
                  std::vector<double> &comp, std::vector<int64_t> &mem) {
         CUDA_TRY(ctx, out_d.ensure(32 * (size_t)ngroups + 64));
         double *a = out_d.as<double>();
-        k_group_profiles<<<(ngroups + 127) / 128, 128, 0, ctx->st>>>(A, dev_levels(), l, ngroups, single ? 1 : 0,
-                                                                    a, a + ngroups, a + 2 * ngroups,
-                                                                    (int64_t *)(a + 3 * ngroups));
+        if (single)
+            k_atom_profiles<<<(ngroups + 127) / 128, 128, 0, ctx->st>>>(A, dev_levels(), l, ngroups, a, a + ngroups,
+                                                                       a + 2 * ngroups, (int64_t *)(a + 3 * ngroups));
+        else
+            k_group_profiles<<<(unsigned)(((int64_t)ngroups * 32 + 127) / 128), 128, 0, ctx->st>>>(
+                A, dev_levels(), l, ngroups, a, a + ngroups, a + 2 * ngroups, (int64_t *)(a + 3 * ngroups));
         ctx->launches++;
         if (int rc = check_launch(ctx, "group_profiles")) return rc;
-        tf.resize(ngroups);
-        tb.resize(ngroups);
-        comp.resize(ngroups);
-        mem.resize(ngroups);
-        CUDA_TRY(ctx, cudaMemcpyAsync(tf.data(), a, 8 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
-        CUDA_TRY(ctx, cudaMemcpyAsync(tb.data(), a + ngroups, 8 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
-        CUDA_TRY(ctx, cudaMemcpyAsync(comp.data(), a + 2 * ngroups, 8 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
-        CUDA_TRY(ctx, cudaMemcpyAsync(mem.data(), a + 3 * ngroups, 8 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
+        char *h = pinned_out(32 * (size_t)ngroups + 16);
+        if (!h) return fail(ctx, PC_ERR_CUDA, "pinned staging");
+        CUDA_TRY(ctx, cudaMemcpyAsync(h, a, 32 * (size_t)ngroups, cudaMemcpyDeviceToHost, ctx->st));
         CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+        const double *hd = (const double *)h;
+        tf.assign(hd, hd + ngroups);
+        tb.assign(hd + ngroups, hd + 2 * ngroups);
+        comp.assign(hd + 2 * ngroups, hd + 3 * ngroups);
+        mem.assign((const int64_t *)(hd + 3 * ngroups), (const int64_t *)(hd + 4 * ngroups));
         return PC_OK;
     }
 };
@@ -1074,20 +1138,13 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         const int L = (int)co.levels.size() - 1;
         const std::vector<std::vector<int>> &G = co.levels[L];
         const int m = (int)G.size();
-        std::vector<double> gc;
-        if (int rc = co.comps(L, m, gc)) return rc;
         const std::vector<int> gmap = member_map(n, G);
-        auto key_less = [&](int a, int b) {
-            if (gc[a] != gc[b]) return gc[a] < gc[b];
-            return G[a][0] < G[b][0];
-        };
-        std::vector<int> order(m);
-        for (int i = 0; i < m; ++i) order[i] = i;
-        std::sort(order.begin(), order.end(), key_less);
-        // every adjacent pair, evaluated once on the device
-        std::vector<std::vector<int>> adj(m);
+        // every adjacent pair (CSR, ascending per group), evaluated once on
+        // the device; aset = the pair's set index from either side
+        std::vector<int> aoff(m + 1, 0), adj, aset;
+        std::vector<int> c;
         for (int gi = 0; gi < m; ++gi) {
-            std::vector<int> &c = adj[gi];
+            c.clear();
             for (int a : G[gi])
                 for (int q = nbr_off[a]; q < nbr_off[a + 1]; ++q) {
                     const int gj = gmap[nbr[q]];
@@ -1095,19 +1152,37 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
                 }
             std::sort(c.begin(), c.end());
             c.erase(std::unique(c.begin(), c.end()), c.end());
+            adj.insert(adj.end(), c.begin(), c.end());
+            aoff[gi + 1] = (int)adj.size();
         }
         std::vector<SetDesc> sets;
-        std::map<std::pair<int, int>, int> pair_idx;
+        aset.assign(adj.size(), -1);
         for (int gi = 0; gi < m; ++gi)
-            for (int gj : adj[gi])
-                if (gi < gj) {
-                    pair_idx[{gi, gj}] = (int)sets.size();
-                    sets.push_back(SetDesc{L, gi, L, gj, 0});
+            for (int e = aoff[gi]; e < aoff[gi + 1]; ++e)
+                if (gi < adj[e]) {
+                    aset[e] = (int)sets.size();
+                    sets.push_back(SetDesc{L, gi, L, adj[e], 0});
                 }
+        for (int gi = 0; gi < m; ++gi)
+            for (int e = aoff[gi]; e < aoff[gi + 1]; ++e)
+                if (gi > adj[e]) {
+                    const int gj = adj[e];
+                    const int f = (int)(std::lower_bound(adj.begin() + aoff[gj], adj.begin() + aoff[gj + 1], gi) -
+                                        adj.begin());
+                    aset[e] = aset[f];
+                }
+        std::vector<double> gc;
         std::vector<int64_t> smem;
         std::vector<int32_t> scount;
         std::vector<uint8_t> sconv;
-        if (int rc = co.eval(sets, smem, scount, sconv)) return rc;
+        if (int rc = co.comps_eval(L, m, gc, sets, smem, scount, sconv)) return rc;
+        auto key_less = [&](int a, int b) {
+            if (gc[a] != gc[b]) return gc[a] < gc[b];
+            return G[a][0] < G[b][0];
+        };
+        std::vector<int> order(m);
+        for (int i = 0; i < m; ++i) order[i] = i;
+        std::sort(order.begin(), order.end(), key_less);
         // the greedy pass over the device's answers
         std::vector<char> used(m, 0);
         std::vector<int> partner(m, -1);
@@ -1115,12 +1190,13 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         for (int gi : order) {
             if (count <= k) break;
             if (used[gi]) continue;
-            std::vector<int> cands;
-            for (int gj : adj[gi])
-                if (!used[gj]) cands.push_back(gj);
-            std::sort(cands.begin(), cands.end(), key_less);
-            for (int gj : cands) {
-                const int si = pair_idx[{std::min(gi, gj), std::max(gi, gj)}];
+            std::vector<std::pair<int, int>> cands;             // (group, set)
+            for (int e = aoff[gi]; e < aoff[gi + 1]; ++e)
+                if (!used[adj[e]]) cands.push_back({adj[e], aset[e]});
+            std::sort(cands.begin(), cands.end(),
+                      [&](const std::pair<int, int> &a, const std::pair<int, int> &b) { return key_less(a.first, b.first); });
+            for (const auto &gs : cands) {
+                const int gj = gs.first, si = gs.second;
                 if (sconv[si] && smem[si] < budget) {           // is_convex and fits (blocks.py:115-116)
                     partner[gi] = gj;
                     used[gi] = used[gj] = 1;
@@ -1318,8 +1394,13 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         while ((int)glist.size() > k) {
             if (int rc = co.upload_level(scratch, glist)) return rc;
             const int m = (int)glist.size();
+            std::vector<SetDesc> sets;
+            for (int pos = 0; pos + 1 < m; ++pos) sets.push_back(SetDesc{scratch, pos, scratch, pos + 1, 0});
             std::vector<double> gc;
-            if (int rc = co.comps(scratch, m, gc)) return rc;
+            std::vector<int64_t> smem;
+            std::vector<int32_t> scount;
+            std::vector<uint8_t> sconv;
+            if (int rc = co.comps_eval(scratch, m, gc, sets, smem, scount, sconv)) return rc;
             // groups of glist are disjoint, so level `scratch` indexes them by position
             std::vector<int> order(m);
             for (int i = 0; i < m; ++i) order[i] = i;
@@ -1328,12 +1409,6 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
                 return glist[a][0] < glist[b][0];
             };
             std::sort(order.begin(), order.end(), key_less);
-            std::vector<SetDesc> sets;
-            for (int pos = 0; pos + 1 < m; ++pos) sets.push_back(SetDesc{scratch, pos, scratch, pos + 1, 0});
-            std::vector<int64_t> smem;
-            std::vector<int32_t> scount;
-            std::vector<uint8_t> sconv;
-            if (int rc = co.eval(sets, smem, scount, sconv)) return rc;
             int merged_at = -1;
             for (int pos : order) {
                 std::vector<int> sides;

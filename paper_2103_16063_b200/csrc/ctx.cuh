@@ -41,12 +41,16 @@ struct DBuf {
 struct CoarsenBufs {
     DBuf atoms_d, lev_grp, lev_off, lev_at, sets_d, scratch_d, out_d, comp_d, mv_d;
     DBuf refine_d;            // device refinement: pairs, scratch, labels out
+    DBuf gc_d;                // group compute times of a coarsening level
+    char *pout = nullptr;     // pinned read-back staging
+    size_t pout_bytes = 0;
     int lev_cap = 0;          // level slots valid for lev_n atoms
     int lev_n = -1;
     int32_t *pin = nullptr;   // pinned level staging [lev_cap][3 * lev_n + 1]
     size_t pin_bytes = 0;
     ~CoarsenBufs() {
         if (pin) cudaFreeHost(pin);
+        if (pout) cudaFreeHost(pout);
     }
 };
 

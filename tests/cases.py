@@ -136,6 +136,23 @@ def layered_graph(rng, n_layers=None, branch=2):
     return TaskGraph(nodes, edges, ["in"], [produced[-1]])
 
 
+def fan_graph(rng, width):
+    """x -> hub -> width parallel tasks -> sink: a coarsening pass can merge
+    only a few pairs, so the level count grows with the width."""
+    nodes = [_val("x", per_sample=4.0), _task("hub", float(rng.randint(1, 1000))),
+             _val("h", per_sample=rng.randint(1, 64) * 4.0)]
+    edges = [("x", "hub"), ("hub", "h")]
+    outs = []
+    for i in range(width):
+        t, v = f"t{i:03d}", f"v{i:03d}"
+        nodes += [_task(t, float(rng.randint(1, 1000))), _val(v, per_sample=rng.randint(1, 64) * 4.0)]
+        edges += [("h", t), (t, v)]
+        outs.append(v)
+    nodes += [_task("sink", float(rng.randint(1, 1000))), _val("y", per_sample=4.0)]
+    edges += [(v, "sink") for v in outs] + [("sink", "y")]
+    return TaskGraph(nodes, edges, ["x"], ["y"])
+
+
 def weighted_chain(flops_list, sizes=None):
     """pkg/tests/test_blocks.py:31-42."""
     sizes = sizes or [4.0] * len(flops_list)

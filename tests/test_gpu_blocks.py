@@ -97,3 +97,12 @@ def test_bert_smoke_and_atom_level(gpu):
     m = pc.CostModel(p.graph, pc.CostModelConfig(), cl)
     for k in (8, 3, len(p.atoms), 10 ** 6):
         _same(partition_blocks(p, m, k), pc.partition_blocks(p, m, k))
+
+
+@pytest.mark.parametrize("seed,width,k", [(1, 150, 2), (2, 90, 3), (3, 40, 1)])
+def test_fan_graphs_many_levels(gpu, seed, width, k):
+    """Few merges per coarsening pass: up to 76 levels, so a refinement move
+    rewrites dozens of coarser levels (k_refine's per-level splice)."""
+    g = cases.fan_graph(random.Random(seed), width)
+    p, m = cases.blocks_inputs(g)
+    _same(partition_blocks(p, m, k), pc.partition_blocks(p, m, k))
