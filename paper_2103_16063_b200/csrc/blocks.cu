@@ -5,26 +5,28 @@
 // predicates it evaluates: the memory of merged atom sets (a full
 // CostModel.profile each, blocks.py:107-116), convexity (blocks.py:45-70),
 // group compute times (blocks.py:104-105) and cut traffic (blocks.py:118-124).
-// Every candidate of a pass -- all adjacent group pairs of a coarsening level,
-// all (pair, mover, target) moves of an uncoarsening round across all coarser
-// levels -- is independent of the greedy state it is tested in, so the device
-// evaluates the whole pass in one batch; the host then replays the greedy
-// order over the device's answers.  Uncoarsening changes state after an
-// accepted move, so it runs in speculative rounds: evaluate every remaining
-// pair against the current state, accept the first pair with a move, re-run
-// from the next pair (accepted moves are rare: 62 on BERT, 0 on ResNet).
+// Every candidate of a coarsening pass (all adjacent group pairs of a level)
+// is independent of the greedy state it is tested in, so the device evaluates
+// the whole pass in one batch and the host replays the greedy order over the
+// device's answers (one sync per level).  Uncoarsening changes state after
+// every accepted move, so it runs entirely on the device: k_refine walks all
+// levels' pairs in one resident CTA or cluster (accepted moves are rare: 62
+// on BERT, 0 on ResNet).
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
-#include <map>
 #include <queue>
 #include <set>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "ctx.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace pcb {
 
@@ -78,10 +80,6 @@ struct DevLevels {
 // mode 1: group (la, ga) minus group (lb, gb)
 struct SetDesc {
     int32_t la, ga, lb, gb, mode;
-};
-
-struct MoveDesc {
-    int32_t li, mover, dest, top;
 };
 
 __device__ __forceinline__ bool in_set(const DevLevels &L, const SetDesc &s, int x) {
@@ -376,62 +374,17 @@ __global__ void k_group_profiles(DevAtoms A, DevLevels L, int level, int ngroups
     }
 }
 
-// Traffic saving of moving level-li group `mover` into top-level block `dest`
-// (blocks.py:193-201): base_traffic - traffic(moved), summed exactly over the
-// value entries the mover touches (each entry once, at its smallest mover atom).
-__global__ void k_move_savings(DevAtoms A, DevLevels L, const MoveDesc *mv, int nm, int64_t *out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nm) return;
-    const MoveDesc m = mv[i];
-    const int32_t *gl = L.grp + (int64_t)m.li * L.n;
-    const int32_t *gt = L.grp + (int64_t)m.top * L.n;
-    const int32_t *off = L.goff + (int64_t)m.li * (L.n + 1);
-    const int32_t *at = L.gat + (int64_t)m.li * L.n;
-    int64_t saving = 0;
-    for (int j = off[m.mover]; j < off[m.mover + 1]; ++j) {
-        const int x = at[j];
-        for (int q = A.atom_tr_off[x]; q < A.atom_tr_off[x + 1]; ++q) {
-            const int e = A.atom_tr[q];
-            const int owner = A.tr_owner[e];
-            int first = gl[owner] == m.mover ? owner : 0x7fffffff;
-            for (int r = A.tr_cons_off[e]; r < A.tr_cons_off[e + 1]; ++r) {
-                const int c = A.tr_cons[r];
-                if (gl[c] == m.mover && c < first) first = c;
-            }
-            if (first != x) continue;
-            const int home0 = gt[owner];
-            const int home1 = gl[owner] == m.mover ? m.dest : home0;
-            int before = 0, after = 0;
-            const int c0 = A.tr_cons_off[e], c1 = A.tr_cons_off[e + 1];
-            for (int r = c0; r < c1; ++r) {
-                const int c = A.tr_cons[r];
-                const int b0 = gt[c];
-                const int b1 = gl[c] == m.mover ? m.dest : b0;
-                bool seen0 = b0 == home0, seen1 = b1 == home1;
-                for (int u = c0; u < r && !(seen0 && seen1); ++u) {
-                    const int cu = A.tr_cons[u];
-                    if (gt[cu] == b0) seen0 = true;
-                    if ((gl[cu] == m.mover ? m.dest : gt[cu]) == b1) seen1 = true;
-                }
-                before += !seen0;
-                after += !seen1;
-            }
-            saving += A.tr_size[e] * (int64_t)(before - after);
-        }
-    }
-    out[i] = saving;
-}
-
 // ---------------------------------------------------------------- refinement
-// _uncoarsen (blocks.py:173-232) as one resident CTA: no host round trip per
-// pair.  For each transition level li (coarsest first) the pairs are walked
-// in order; a pair moves one side (mover, a level-li group) into a
-// neighbouring level-li group's block when that strictly cuts the top-level
-// traffic and both touched groups stay convex and inside memory at every
-// coarser level.  The reference tests fit first and saving second; the
+// _uncoarsen (blocks.py:173-232) as one resident CTA, or one thread-block
+// cluster (up to 16 CTAs, one per SM) when there are many pairs: no host
+// round trip per pair.  For each transition level li (coarsest first) the
+// pairs are walked in order; a pair moves one side (mover, a level-li group)
+// into a neighbouring level-li group's block when that strictly cuts the
+// top-level traffic and both touched groups stay convex and inside memory at
+// every coarser level.  The reference tests fit first and saving second; the
 // choice is the same if the saving is computed first: the answer is the
 // candidate with the largest positive saving among those that fit, the
-// earliest (side v before w, target index ascending) on ties.  So the CTA
+// earliest (side v before w, target index ascending) on ties.  So the kernel
 //   1. computes, for a window of pairs at once (one warp per pair side), the
 //      best positive-saving candidate of every side -- savings depend only on
 //      the top-level labels, which change only when a move is applied;
@@ -444,28 +397,36 @@ __global__ void k_move_savings(DevAtoms A, DevLevels L, const MoveDesc *mv, int 
 //      level) and restarts the window after the pair; a pair without an
 //      accepted move leaves the state as it was, so the window's other
 //      results stay valid.
-// Member order inside a group is free at levels above li (every set
-// predicate is order-independent), so the splice appends the mover.
+// Every CTA of the cluster runs the same control flow over the same global
+// data (window results, fit verdicts), so all reach the same decisions; the
+// cluster barrier orders the exchanges.  Member order inside a group is free
+// at levels above li (every set predicate is order-independent), so the
+// splice appends the mover.
 constexpr int RF_THREADS = 512;
 constexpr int RF_WARPS = RF_THREADS / 32;
-constexpr int RF_WMAX = 512;          // pairs per window (2 sides each)
+constexpr int RF_WMAX = 1024;         // pairs per window (2 sides each)
+constexpr size_t RF_CLUSTER_MIN_PAIRS = 2048;   // fewer recorded merges: one CTA
+
+struct Cand {
+    long long s;                      // saving; 0 = none
+    int side, ti;
+};
 
 struct RefineArgs {
     int ntrans, top;
     const int32_t *pair_off;          // [ntrans + 1]
     const int2 *pairs;                // level-li group indices (v, w)
     int32_t *grp, *goff, *gat;        // the level arrays (written by moves)
-    uint32_t *bits;                   // [RF_WARPS][words] convexity bitmaps
+    uint32_t *bits;                   // [cluster warps][words] convexity bitmaps
     int words;
-    int32_t *tmp;                     // [RF_WARPS][n] splice scratch
+    int32_t *tmp;                     // [min(cluster warps, top)][n] splice scratch
     int32_t *src, *dst;               // [top] a move's groups per coarser level
+    long long *sav;                   // [2][2 * RF_WMAX] window: best saving per side
+    int32_t *sti;                     // [2][2 * RF_WMAX] window: its target
+    int32_t *ok;                      // [2 * top] a fit test's per-set verdicts
+    Cand *next;                       // [2] next candidates after a rejected one
     int64_t budget;
     long long *stats;                 // windows, side evaluations, fit tests, moves
-};
-
-struct Cand {
-    long long s;                      // saving; 0 = none
-    int side, ti;
 };
 
 // a ranks before b: larger saving, then side v, then smaller target index
@@ -475,8 +436,10 @@ __device__ __forceinline__ bool cand_before(const Cand &a, const Cand &b) {
     return a.ti < b.ti;
 }
 
-// the warp's share of base_traffic - traffic(moved) for level-li group `mover`
-// moving into top-level block `dest` (k_move_savings' sum, lanes over atoms)
+// base_traffic - traffic(moved) for level-li group `mover` moving into
+// top-level block `dest` (blocks.py:193-201), summed exactly over the value
+// entries the mover touches (each entry once, at its smallest mover atom);
+// the warp's lanes split the mover's atoms
 __device__ long long move_saving_warp(const DevAtoms &A, const DevLevels &L, int li, int top,
                                       int mover, int dest) {
     const int lane = threadIdx.x & 31;
@@ -600,41 +563,57 @@ __device__ void splice_warp(int32_t *off, int32_t *at, const int32_t *grp, int s
 }
 
 __global__ void __launch_bounds__(RF_THREADS, 1) k_refine(DevAtoms A, DevLevels L, RefineArgs R) {
-    __shared__ long long s_sav[2 * RF_WMAX];
-    __shared__ int s_ti[2 * RF_WMAX];
-    __shared__ int s_bad, s_first;
-    __shared__ Cand s_next[2];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank(), nct = (int)cluster.num_blocks();
+    // a one-CTA cluster exchanges through its own L1: a CTA barrier suffices
+    // (the cluster barrier's acquire would also drop the L1's atom arrays)
+    auto csync = [&]() {
+        if (nct == 1) __syncthreads();
+        else cluster.sync();
+    };
+    __shared__ int s_first, s_bad;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gw = rank * RF_WARPS + warp, NW = nct * RF_WARPS;     // cluster-wide warp
+    const int gt = rank * RF_THREADS + tid, NT = nct * RF_THREADS;  // cluster-wide thread
     const int n = L.n;
-    uint32_t *bits = R.bits + (int64_t)warp * R.words;
+    const int W0 = max(1, NW / 2);                 // pairs of a window after a move
+    uint32_t *bits = R.bits + (int64_t)gw * R.words;
     long long n_win = 0, n_side = 0, n_fit = 0, n_move = 0;
+    int buf = 0;                                   // window results double-buffered
     for (int li = R.ntrans - 1; li >= 0; --li) {
         const int2 *pairs = R.pairs + R.pair_off[li];
         const int np = R.pair_off[li + 1] - R.pair_off[li];
         const int nlev = R.top - li;
         const int32_t *offl = L.goff + (int64_t)li * (n + 1);
         const int32_t *atl = L.gat + (int64_t)li * n;
-        int p = 0, ws = 0, we = 0, W = RF_WARPS / 2;
+        int p = 0, ws = 0, we = 0, W = W0;
+        long long *sav = R.sav;
+        int *sti = R.sti;
         while (p < np) {
             if (p >= we) {                                       // 1. a new window
+                buf ^= 1;
+                sav = R.sav + buf * 2 * RF_WMAX;
+                sti = R.sti + buf * 2 * RF_WMAX;
                 ws = p;
                 we = min(np, p + W);
-                for (int it = warp; it < 2 * (we - ws); it += RF_WARPS) {
+                for (int it = gw; it < 2 * (we - ws); it += NW) {
                     const int2 pr = pairs[ws + (it >> 1)];
                     const Cand c = side_best(A, L, li, R.top, (it & 1) ? pr.y : pr.x, it & 1,
                                              Cand{-1, 0, 0});
                     if (lane == 0) {
-                        s_sav[it] = c.s;
-                        s_ti[it] = c.ti;
+                        sav[it] = c.s;
+                        sti[it] = c.ti;
                     }
                 }
                 ++n_win;
                 n_side += 2 * (we - ws);
+                csync();
             }
+            // the first pair of the window with a candidate (every CTA alike)
             if (tid == 0) s_first = 0x7fffffff;
             __syncthreads();
             for (int it = 2 * (p - ws) + tid; it < 2 * (we - ws); it += RF_THREADS)
-                if (s_sav[it] > 0) atomicMin(&s_first, it >> 1);
+                if (sav[it] > 0) atomicMin(&s_first, it >> 1);
             __syncthreads();
             const int fq = s_first;
             __syncthreads();                                     // s_first is reset next
@@ -643,23 +622,24 @@ __global__ void __launch_bounds__(RF_THREADS, 1) k_refine(DevAtoms A, DevLevels 
                 W = min(2 * W, RF_WMAX);
                 continue;
             }
-            // 2. the first pair with a candidate: test candidates in rank order
+            // 2. test that pair's candidates in rank order
             const int q = ws + fq;
             const int2 pr = pairs[q];
-            Cand c0{s_sav[2 * fq], 0, s_ti[2 * fq]}, c1{s_sav[2 * fq + 1], 1, s_ti[2 * fq + 1]};
+            Cand c0{sav[2 * fq], 0, sti[2 * fq]}, c1{sav[2 * fq + 1], 1, sti[2 * fq + 1]};
             Cand c = c0.s > 0 && (c1.s <= 0 || cand_before(c0, c1)) ? c0 : c1;
             bool moved = false;
             while (c.s > 0) {
                 const int mv = c.side ? pr.y : pr.x;
-                const int a0 = atl[offl[mv]], t0 = atl[offl[c.ti]];
-                for (int e = tid; e < nlev; e += RF_THREADS) {
-                    const int ell = li + 1 + e;
-                    R.src[e] = L.grp[(int64_t)ell * n + a0];
-                    R.dst[e] = L.grp[(int64_t)ell * n + t0];
+                if (rank == 0) {
+                    const int a0 = atl[offl[mv]], t0 = atl[offl[c.ti]];
+                    for (int e = tid; e < nlev; e += RF_THREADS) {
+                        const int ell = li + 1 + e;
+                        R.src[e] = L.grp[(int64_t)ell * n + a0];
+                        R.dst[e] = L.grp[(int64_t)ell * n + t0];
+                    }
                 }
-                if (tid == 0) s_bad = 0;
-                __syncthreads();
-                for (int k = warp; k < 2 * nlev; k += RF_WARPS) {    // _move_fits (blocks.py:206-221)
+                csync();
+                for (int k = gw; k < 2 * nlev; k += NW) {        // _move_fits (blocks.py:206-221)
                     const int e = k >> 1, ell = li + 1 + e;
                     const SetDesc sd = (k & 1) ? SetDesc{ell, R.dst[e], li, mv, 0}     // grown
                                                : SetDesc{ell, R.src[e], li, mv, 1};    // shrunk
@@ -667,48 +647,53 @@ __global__ void __launch_bounds__(RF_THREADS, 1) k_refine(DevAtoms A, DevLevels 
                     int64_t mem;
                     bool convex;
                     eval_set_warp(A, L, sd, bits, cnt, mem, convex);
-                    const bool ok = convex && mem < R.budget && ((k & 1) || cnt > 0);
-                    if (lane == 0 && !ok) s_bad = 1;
+                    if (lane == 0) R.ok[k] = convex && mem < R.budget && ((k & 1) || cnt > 0);
                 }
                 ++n_fit;
+                csync();
+                if (tid == 0) s_bad = 0;
                 __syncthreads();
-                if (!s_bad) {                                    // 3. _apply_move (blocks.py:224-232)
+                for (int k = tid; k < 2 * nlev; k += RF_THREADS)
+                    if (!R.ok[k]) s_bad = 1;
+                __syncthreads();
+                const bool bad = s_bad;
+                __syncthreads();
+                if (!bad) {                                      // 3. _apply_move (blocks.py:224-232)
                     const int m0 = offl[mv], cnt = offl[mv + 1] - m0;
-                    for (int k = tid; k < nlev * cnt; k += RF_THREADS) {
+                    for (int k = gt; k < nlev * cnt; k += NT) {
                         const int e = k / cnt;
                         R.grp[(int64_t)(li + 1 + e) * n + atl[m0 + k % cnt]] = R.dst[e];
                     }
-                    __syncthreads();
-                    for (int e = warp; e < nlev; e += RF_WARPS) {
+                    csync();
+                    for (int e = gw; e < nlev; e += NW) {
                         const int ell = li + 1 + e;
                         splice_warp(R.goff + (int64_t)ell * (n + 1), R.gat + (int64_t)ell * n,
                                     R.grp + (int64_t)ell * n, R.src[e], R.dst[e], atl + m0, cnt,
-                                    R.tmp + (int64_t)warp * n);
+                                    R.tmp + (int64_t)gw * n);
                     }
-                    __syncthreads();
+                    csync();
                     moved = true;
                     ++n_move;
                     break;
                 }
                 // next candidate of this pair after the rejected one
-                if (warp < 2) {
-                    const Cand b = side_best(A, L, li, R.top, warp ? pr.y : pr.x, warp, c);
-                    if (lane == 0) s_next[warp] = b;
+                if (gw < 2) {
+                    const Cand b = side_best(A, L, li, R.top, gw ? pr.y : pr.x, gw, c);
+                    if (lane == 0) R.next[gw] = b;
                 }
-                __syncthreads();
-                const Cand b0 = s_next[0], b1 = s_next[1];
-                __syncthreads();
+                csync();
+                const Cand b0 = R.next[0], b1 = R.next[1];
                 c = b0.s > 0 && (b1.s <= 0 || cand_before(b0, b1)) ? b0 : b1;
                 n_side += 2;
             }
             p = q + 1;
             if (moved) {                                         // later savings changed
                 we = p;
-                W = RF_WARPS / 2;
+                W = W0;
             }
         }
     }
-    if (tid == 0) {
+    if (rank == 0 && tid == 0) {
         R.stats[0] = n_win;
         R.stats[1] = n_side;
         R.stats[2] = n_fit;
@@ -725,17 +710,16 @@ struct Coarsener {
     DevAtoms A{};
     int n;
     // device buffers and pinned level staging live in the context (cb)
-    DBuf &atoms_d, &lev_grp, &lev_off, &lev_at, &sets_d, &scratch_d, &out_d, &comp_d, &mv_d;
+    DBuf &atoms_d, &lev_grp, &lev_off, &lev_at, &sets_d, &scratch_d, &out_d, &comp_d;
     int &lev_cap;
     int32_t *&pin;                    // [lev_cap][3n + 1] (grp | off | at)
-    std::vector<char> dirty;          // host level differs from its device copy
     std::vector<std::vector<std::vector<int>>> levels;
     std::vector<double> atom_comp;
 
     Coarsener(pc_ctx *c, const pc_atoms *h)
         : ctx(c), H(h), n(h->n), atoms_d(c->cb.atoms_d), lev_grp(c->cb.lev_grp),
           lev_off(c->cb.lev_off), lev_at(c->cb.lev_at), sets_d(c->cb.sets_d),
-          scratch_d(c->cb.scratch_d), out_d(c->cb.out_d), comp_d(c->cb.comp_d), mv_d(c->cb.mv_d),
+          scratch_d(c->cb.scratch_d), out_d(c->cb.out_d), comp_d(c->cb.comp_d),
           lev_cap(c->cb.lev_cap), pin(c->cb.pin) {
         if (c->cb.lev_n != n) {          // slot layout depends on n: re-slice, keep the memory
             cudaStreamSynchronize(c->st);
@@ -870,8 +854,6 @@ struct Coarsener {
         CUDA_TRY(ctx, cudaMemcpyAsync(lev_grp.as<int32_t>() + (size_t)l * n, grp, 4 * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
         CUDA_TRY(ctx, cudaMemcpyAsync(lev_off.as<int32_t>() + (size_t)l * (n + 1), off, 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
         CUDA_TRY(ctx, cudaMemcpyAsync(lev_at.as<int32_t>() + (size_t)l * n, at, 4 * (size_t)n, cudaMemcpyHostToDevice, ctx->st));
-        if ((int)dirty.size() <= l) dirty.resize(l + 1, 0);
-        dirty[l] = 0;
         return PC_OK;
     }
 
@@ -955,30 +937,6 @@ struct Coarsener {
         return PC_OK;
     }
 
-    // launch + async read-back into out (sized by the caller); no sync
-    int savings_async(const std::vector<MoveDesc> &mv, std::vector<int64_t> &out) {
-        const int nm = (int)mv.size();
-        CUDA_TRY(ctx, mv_d.ensure(sizeof(MoveDesc) * nm + 8 * (size_t)nm + 64));
-        MoveDesc *dm = mv_d.as<MoveDesc>();
-        int64_t *ds = (int64_t *)(((uintptr_t)(dm + nm) + 15) & ~uintptr_t(15));
-        CUDA_TRY(ctx, cudaMemcpyAsync(dm, mv.data(), sizeof(MoveDesc) * nm, cudaMemcpyHostToDevice, ctx->st));
-        k_move_savings<<<(nm + 127) / 128, 128, 0, ctx->st>>>(A, dev_levels(), dm, nm, ds);
-        ctx->launches++;
-        if (int rc = check_launch(ctx, "move_savings")) return rc;
-        CUDA_TRY(ctx, cudaMemcpyAsync(out.data(), ds, 8 * (size_t)nm, cudaMemcpyDeviceToHost, ctx->st));
-        return PC_OK;
-    }
-
-    // k_eval_sets and k_move_savings of one speculative round, one sync
-    int eval_moves(const std::vector<SetDesc> &sets, const std::vector<MoveDesc> &mv,
-                   std::vector<int64_t> &mem, std::vector<int32_t> &count,
-                   std::vector<uint8_t> &convex, std::vector<int64_t> &sav) {
-        sav.assign(mv.size(), 0);
-        if (!mv.empty())
-            if (int rc = savings_async(mv, sav)) return rc;
-        return eval(sets, mem, count, convex);      // synchronises the stream
-    }
-
     int profiles(int l, int ngroups, bool single, std::vector<double> &tf, std::vector<double> &tb,
                  std::vector<double> &comp, std::vector<int64_t> &mem) {
         CUDA_TRY(ctx, out_d.ensure(32 * (size_t)ngroups + 64));
@@ -1016,9 +974,6 @@ using Transitions = std::vector<std::vector<std::pair<std::vector<int>, std::vec
 int refine_on_device(Coarsener &co, const Transitions &tr, long long stats[4]) {
     pc_ctx *ctx = co.ctx;
     const int n = co.n, top = (int)co.levels.size() - 1, nt = (int)tr.size();
-    for (int l = 0; l <= top; ++l)
-        if (l < (int)co.dirty.size() && co.dirty[l])
-            if (int rc = co.upload_level(l, co.levels[l])) return rc;
     std::vector<int32_t> head(nt + 1, 0);
     std::vector<int2> pairs;
     for (int li = 0; li < nt; ++li) {
@@ -1026,13 +981,50 @@ int refine_on_device(Coarsener &co, const Transitions &tr, long long stats[4]) {
         for (const auto &vw : tr[li]) pairs.push_back(make_int2(gm[vw.first[0]], gm[vw.second[0]]));
         head[li + 1] = (int32_t)pairs.size();
     }
+    // the cluster: as many CTAs (one per SM) as the device co-schedules, <= 16
+    int &ncl = ctx->cb.refine_cluster;
+    if (ncl == 0) {
+        ncl = 1;
+        if (cudaFuncSetAttribute(k_refine, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+            cudaGetLastError();
+        for (int c = 16; c > 1; c /= 2) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = c;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(c);
+            cfg.blockDim = dim3(RF_THREADS);
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, k_refine, &cfg) == cudaSuccess && nc > 0) {
+                ncl = c;
+                break;
+            }
+            cudaGetLastError();
+        }
+    }
+    // A cluster barrier costs a few microseconds per window or move (its
+    // acquire also drops the L1's atom arrays), one CTA's barrier almost
+    // nothing; the cluster pays off once windows are wide, i.e. on many pairs
+    // (measured, r2be: C1 / C2 with 211 / 931 pairs 1.22 / 1.83 ms on one CTA
+    // vs 1.68 / 1.98 on 16; C4 with 2,531 pairs 2.87 vs 2.43; 15,362 pairs
+    // 12.2 vs 6.6 ms).
+    int cl = pairs.size() >= RF_CLUSTER_MIN_PAIRS ? ncl : 1;
+    if (const char *e = getenv("PIPECUT_B200_REFINE_CLUSTER"))     // tests / A-B
+        cl = std::max(1, std::min(ncl, atoi(e)));
+    const int NW = cl * RF_WARPS;
     const int words = (n + 31) / 32 + 1;
     size_t total = 0;
     auto carve = [&](size_t bytes) { const size_t o = (total + 15) & ~size_t(15); total = o + bytes; return o; };
     const size_t o_stats = carve(4 * sizeof(long long)), o_head = carve(4 * head.size());
     const size_t o_pairs = carve(sizeof(int2) * pairs.size()), o_src = carve(4 * (size_t)top);
-    const size_t o_dst = carve(4 * (size_t)top), o_bits = carve(4 * (size_t)RF_WARPS * words);
-    const size_t o_tmp = carve(4 * (size_t)RF_WARPS * n), o_lab = carve(4 * (size_t)n);
+    const size_t o_dst = carve(4 * (size_t)top), o_bits = carve(4 * (size_t)NW * words);
+    const size_t o_tmp = carve(4 * (size_t)std::min(NW, top) * n);
+    const size_t o_sav = carve(sizeof(long long) * 4 * RF_WMAX), o_sti = carve(4 * 4 * RF_WMAX);
+    const size_t o_ok = carve(4 * 2 * (size_t)top), o_next = carve(2 * sizeof(Cand));
     CUDA_TRY(ctx, ctx->cb.refine_d.ensure(total + 64));
     char *b = ctx->cb.refine_d.as<char>();
     std::vector<char> up(o_src - o_head);
@@ -1052,9 +1044,27 @@ int refine_on_device(Coarsener &co, const Transitions &tr, long long stats[4]) {
     R.tmp = (int32_t *)(b + o_tmp);
     R.src = (int32_t *)(b + o_src);
     R.dst = (int32_t *)(b + o_dst);
+    R.sav = (long long *)(b + o_sav);
+    R.sti = (int32_t *)(b + o_sti);
+    R.ok = (int32_t *)(b + o_ok);
+    R.next = (Cand *)(b + o_next);
     R.budget = co.H->budget;
     R.stats = (long long *)(b + o_stats);
-    k_refine<<<1, RF_THREADS, 0, ctx->st>>>(co.A, co.dev_levels(), R);
+    {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(cl);
+        cfg.blockDim = dim3(RF_THREADS);
+        cfg.stream = ctx->st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const DevLevels L = co.dev_levels();
+        CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k_refine, co.A, L, R));
+    }
     ctx->launches++;
     if (int rc = check_launch(ctx, "refine")) return rc;
     std::vector<int32_t> lab(n);
@@ -1231,136 +1241,13 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
 
     phase("coarsen");
     const int top = (int)co.levels.size() - 1;
-    const bool host_refine = getenv("PIPECUT_B200_HOST_REFINE") != nullptr;
-    if (!transitions.empty() && !host_refine) {
+    if (!transitions.empty()) {
         long long st[4];
         if (int rc = refine_on_device(co, transitions, st)) return rc;
         if (phase_times)
-            fprintf(stderr, "[pipecut_b200] refine (device): %lld windows, %lld side evaluations, "
+            fprintf(stderr, "[pipecut_b200] refine: %lld windows, %lld side evaluations, "
                             "%lld fit tests, %lld moves\n", st[0], st[1], st[2], st[3]);
     }
-    // ---- refinement: speculative rounds over the recorded merges (blocks.py:173-232)
-    long long n_rounds = 0, n_sets = 0, n_moves = 0;
-    std::vector<std::vector<int>> map_cache(co.levels.size());
-    std::vector<char> map_valid(co.levels.size(), 0);
-    double t_dev = 0.0;
-    for (int li = host_refine ? (int)transitions.size() - 1 : -1; li >= 0; --li) {
-        const auto &pairs = transitions[li];
-        // Rounds evaluate a window of pairs from p on (48, doubling while a
-        // window holds no move): pairs past the first move would be evaluated
-        // against a state that move changes, so building their sets is wasted
-        // host and device work.  A window without a move is skipped exactly as
-        // the reference skips those pairs (same state).
-        size_t p = 0, win = 48;
-        while (p < pairs.size()) {
-            const size_t end = std::min(pairs.size(), p + win);
-            for (int l = li; l <= top; ++l)
-                if (co.dirty[l])
-                    if (int rc = co.upload_level(l, co.levels[l])) return rc;
-            // atom -> group maps, rebuilt only for levels a move changed
-            for (int l = li; l <= top; ++l)
-                if (!map_valid[l]) {
-                    map_cache[l] = member_map(n, co.levels[l]);
-                    map_valid[l] = 1;
-                }
-            const std::vector<std::vector<int>> &maps = map_cache;
-            struct Tri { int q, mi, ti, mv; int64_t set0; };
-            std::vector<Tri> tris;
-            std::vector<SetDesc> sets;
-            std::vector<MoveDesc> moves;
-            for (size_t q = p; q < end; ++q) {
-                for (int mi = 0; mi < 2; ++mi) {
-                    const std::vector<int> &mover = mi == 0 ? pairs[q].first : pairs[q].second;
-                    const int here = maps[top][mover[0]];
-                    const int mv = maps[li][mover[0]];
-                    std::vector<int> targets;
-                    for (int a : mover)
-                        for (int r = nbr_off[a]; r < nbr_off[a + 1]; ++r) targets.push_back(maps[li][nbr[r]]);
-                    std::sort(targets.begin(), targets.end());
-                    targets.erase(std::unique(targets.begin(), targets.end()), targets.end());
-                    for (int ti : targets) {
-                        const std::vector<int> &target = co.levels[li][ti];
-                        if (maps[top][target[0]] == here || ti == mv) continue;
-                        tris.push_back(Tri{(int)q, mi, ti, mv, (int64_t)sets.size()});
-                        for (int ell = li + 1; ell <= top; ++ell) {
-                            const int src = maps[ell][mover[0]], dst = maps[ell][target[0]];
-                            sets.push_back(SetDesc{ell, src, li, mv, 1});   // shrunk
-                            sets.push_back(SetDesc{ell, dst, li, mv, 0});   // grown
-                        }
-                        moves.push_back(MoveDesc{li, mv, maps[top][target[0]], top});
-                    }
-                }
-            }
-            std::vector<int64_t> smem, sav;
-            std::vector<int32_t> scount;
-            std::vector<uint8_t> sconv;
-            const auto td0 = std::chrono::steady_clock::now();
-            if (int rc = co.eval_moves(sets, moves, smem, scount, sconv, sav)) return rc;
-            t_dev += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - td0).count();
-            ++n_rounds;
-            n_sets += (long long)sets.size();
-            n_moves += (long long)moves.size();
-            const int nlev = top - li;
-            bool applied = false;
-            size_t ti_ptr = 0;
-            for (size_t q = p; q < end && !applied; ++q) {
-                int64_t best_saving = 0;
-                int best = -1;
-                for (; ti_ptr < tris.size() && tris[ti_ptr].q == (int)q; ++ti_ptr) {
-                    const Tri &t = tris[ti_ptr];
-                    bool fits = true;                           // _move_fits (blocks.py:206-221)
-                    for (int e = 0; e < nlev && fits; ++e) {
-                        const int64_t sh = t.set0 + 2 * e, gr = sh + 1;
-                        if (scount[sh] == 0) fits = false;
-                        else if (!(sconv[gr] && sconv[sh])) fits = false;
-                        else if (!(smem[gr] < budget && smem[sh] < budget)) fits = false;
-                    }
-                    if (!fits) continue;
-                    const int64_t s = sav[ti_ptr];
-                    if (s > 0 && (best < 0 || s > best_saving)) {
-                        best_saving = s;
-                        best = (int)ti_ptr;
-                    }
-                }
-                if (best >= 0) {
-                    // _apply_move (blocks.py:224-232)
-                    const Tri &t = tris[best];
-                    const std::vector<int> mover = t.mi == 0 ? pairs[q].first : pairs[q].second;
-                    const std::vector<int> target = co.levels[li][t.ti];
-                    std::vector<char> in_mover(n, 0);
-                    for (int a : mover) in_mover[a] = 1;
-                    for (int ell = li + 1; ell <= top; ++ell) {
-                        auto &lev = co.levels[ell];
-                        const std::vector<int> &mm = map_cache[ell];   // current until changed below
-                        const int si = mm[mover[0]], di = mm[target[0]];
-                        std::vector<int> shr;
-                        for (int a : lev[si])
-                            if (!in_mover[a]) shr.push_back(a);
-                        lev[si] = shr;
-                        std::vector<int> gr = lev[di];
-                        gr.insert(gr.end(), mover.begin(), mover.end());
-                        std::sort(gr.begin(), gr.end());
-                        lev[di] = gr;
-                        sort_by_first(lev);
-                        co.dirty[ell] = 1;
-                        map_valid[ell] = 0;
-                    }
-                    applied = true;
-                    p = q + 1;
-                    win = 48;
-                }
-            }
-            if (!applied) {
-                if (end == pairs.size()) break;
-                p = end;
-                win *= 2;
-            }
-        }
-    }
-
-    if (phase_times)
-        fprintf(stderr, "[pipecut_b200] refine: %lld rounds, %lld sets, %lld moves, %.2f ms in eval (device + sync)\n",
-                n_rounds, n_sets, n_moves, t_dev);
     phase("refine");
     // ---- dependency order (blocks.py:235-255) and compaction (267-292)
     auto topo = [&](const std::vector<std::vector<int>> &groups) {

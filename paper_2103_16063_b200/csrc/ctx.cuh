@@ -39,8 +39,9 @@ struct DBuf {
 // partition_blocks' device buffers, kept across calls (allocation and the
 // pinned staging would otherwise cost more than a small coarsening)
 struct CoarsenBufs {
-    DBuf atoms_d, lev_grp, lev_off, lev_at, sets_d, scratch_d, out_d, comp_d, mv_d;
+    DBuf atoms_d, lev_grp, lev_off, lev_at, sets_d, scratch_d, out_d, comp_d;
     DBuf refine_d;            // device refinement: pairs, scratch, labels out
+    int refine_cluster = 0;   // k_refine's cluster size (0 = not chosen yet)
     DBuf gc_d;                // group compute times of a coarsening level
     char *pout = nullptr;     // pinned read-back staging
     size_t pout_bytes = 0;

@@ -106,3 +106,26 @@ def test_fan_graphs_many_levels(gpu, seed, width, k):
     g = cases.fan_graph(random.Random(seed), width)
     p, m = cases.blocks_inputs(g)
     _same(partition_blocks(p, m, k), pc.partition_blocks(p, m, k))
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "16"])
+def test_refinement_cluster_sizes(gpu, monkeypatch, cluster):
+    """k_refine spreads a window over a thread-block cluster; a smaller
+    cluster (one CTA: all sequencing inside one SM) gives the same blocks."""
+    monkeypatch.setenv("PIPECUT_B200_REFINE_CLUSTER", cluster)
+    with open(os.path.join(GOLD, "configs.json")) as fh:
+        gold = json.load(fh)["C1"]
+    part, model, k, batch, cl = cases.config_partition("C1")
+    assert [list(g) for g in partition_blocks(part, model, k).block_atoms] == gold["block_atoms"]
+    rng = random.Random(23)
+    for _ in range(10):
+        g = cases.layered_graph(rng)
+        p, m = cases.blocks_inputs(g)
+        try:
+            want = pc.partition_blocks(p, m, 3)
+        except pc.CompactionStuck:
+            continue
+        _same(partition_blocks(p, m, 3), want)
+    g = cases.fan_graph(random.Random(2), 90)
+    p, m = cases.blocks_inputs(g)
+    _same(partition_blocks(p, m, 3), pc.partition_blocks(p, m, 3))
