@@ -965,7 +965,7 @@ struct Coarsener {
 std::vector<int> member_map(int n, const std::vector<std::vector<int>> &level);
 void sort_by_first(std::vector<std::vector<int>> &level);
 
-using Transitions = std::vector<std::vector<std::pair<std::vector<int>, std::vector<int>>>>;
+using Transitions = std::vector<std::vector<int2>>;   // per level: merged (v, w) group indices
 
 // _uncoarsen on the device (k_refine): the recorded merges go up as level
 // group-index pairs, one launch walks every level, and the top level's labels
@@ -977,8 +977,7 @@ int refine_on_device(Coarsener &co, const Transitions &tr, long long stats[4]) {
     std::vector<int32_t> head(nt + 1, 0);
     std::vector<int2> pairs;
     for (int li = 0; li < nt; ++li) {
-        const std::vector<int> gm = member_map(n, co.levels[li]);
-        for (const auto &vw : tr[li]) pairs.push_back(make_int2(gm[vw.first[0]], gm[vw.second[0]]));
+        pairs.insert(pairs.end(), tr[li].begin(), tr[li].end());
         head[li + 1] = (int32_t)pairs.size();
     }
     // the cluster: as many CTAs (one per SM) as the device co-schedules, <= 16
@@ -1143,8 +1142,14 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
 
     phase("level0");
     // ---- coarsening passes (blocks.py:127-166, 371-378)
-    std::vector<std::vector<std::pair<std::vector<int>, std::vector<int>>>> transitions;
+    Transitions transitions;
+    double t_adj = 0, t_dev = 0, t_greedy = 0, t_next = 0;     // PIPECUT_B200_BLOCKS_TIMES split
+    auto tick = [&]() { return phase_times ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point(); };
+    auto since = [&](std::chrono::steady_clock::time_point t) {
+        return phase_times ? std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count() : 0.0;
+    };
     while ((int)co.levels.back().size() > k) {
+        auto tc = tick();
         const int L = (int)co.levels.size() - 1;
         const std::vector<std::vector<int>> &G = co.levels[L];
         const int m = (int)G.size();
@@ -1185,7 +1190,11 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         std::vector<int64_t> smem;
         std::vector<int32_t> scount;
         std::vector<uint8_t> sconv;
+        t_adj += since(tc);
+        tc = tick();
         if (int rc = co.comps_eval(L, m, gc, sets, smem, scount, sconv)) return rc;
+        t_dev += since(tc);
+        tc = tick();
         auto key_less = [&](int a, int b) {
             if (gc[a] != gc[b]) return gc[a] < gc[b];
             return G[a][0] < G[b][0];
@@ -1197,10 +1206,11 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
         std::vector<char> used(m, 0);
         std::vector<int> partner(m, -1);
         int count = m;
+        std::vector<std::pair<int, int>> cands;                 // (group, set)
         for (int gi : order) {
             if (count <= k) break;
             if (used[gi]) continue;
-            std::vector<std::pair<int, int>> cands;             // (group, set)
+            cands.clear();
             for (int e = aoff[gi]; e < aoff[gi + 1]; ++e)
                 if (!used[adj[e]]) cands.push_back({adj[e], aset[e]});
             std::sort(cands.begin(), cands.end(),
@@ -1215,30 +1225,37 @@ extern "C" int pc_partition_blocks(pc_ctx *ctx, const pc_atoms *H, int32_t k, in
                 }
             }
         }
+        t_greedy += since(tc);
+        tc = tick();
         std::vector<char> absorbed(m, 0);
         for (int gi = 0; gi < m; ++gi)
             if (partner[gi] >= 0) absorbed[partner[gi]] = 1;
         std::vector<std::vector<int>> next;
-        std::vector<std::pair<std::vector<int>, std::vector<int>>> merges;
+        std::vector<int2> merges;                               // (v, w) as level-L group indices
+        next.reserve(m);
         for (int gi = 0; gi < m; ++gi) {
             if (absorbed[gi]) continue;
             if (partner[gi] < 0) {
                 next.push_back(G[gi]);
             } else {
-                std::vector<int> u = G[gi];
-                u.insert(u.end(), G[partner[gi]].begin(), G[partner[gi]].end());
-                std::sort(u.begin(), u.end());
-                next.push_back(u);
-                merges.push_back({G[gi], G[partner[gi]]});
+                const std::vector<int> &v = G[gi], &w = G[partner[gi]];
+                std::vector<int> u(v.size() + w.size());
+                std::merge(v.begin(), v.end(), w.begin(), w.end(), u.begin());
+                next.push_back(std::move(u));
+                merges.push_back(make_int2(gi, partner[gi]));
             }
         }
         if (merges.empty()) break;
         sort_by_first(next);
-        co.levels.push_back(next);
-        transitions.push_back(merges);
+        co.levels.push_back(std::move(next));
+        transitions.push_back(std::move(merges));
         if (int rc = co.upload_level(L + 1, co.levels.back())) return rc;
+        t_next += since(tc);
     }
 
+    if (phase_times)
+        fprintf(stderr, "[pipecut_b200] coarsen: %d levels, adjacency %.2f ms, device + sync %.2f ms, "
+                        "greedy %.2f ms, next level %.2f ms\n", (int)co.levels.size(), t_adj, t_dev, t_greedy, t_next);
     phase("coarsen");
     const int top = (int)co.levels.size() - 1;
     if (!transitions.empty()) {
