@@ -1,3 +1,4 @@
+#include <unordered_map>
 // Host-side flattening of an AtomicPartition + CostModel into the atom-level
 // arrays of partition_blocks (paper_2103_16063_b200/flatten.py:
 // _flatten_atoms, blocks.py:73-124), natively: the same traversal of the
@@ -12,6 +13,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cmath>
+#include <unordered_map>
 #include <vector>
 
 namespace py = pybind11;
@@ -91,29 +93,59 @@ py::dict flatten(py::object partition, py::object model) {
 
     // node id -> atom (atoms.py:259-305); duplicates are the Python path's error
     py::dict atom_of;
-    for (int i = 0; i < n; ++i)
-        for (py::handle nid : py::reinterpret_borrow<py::object>(atoms[i].attr("node_ids"))) {
-            if (atom_of.contains(nid)) throw Fallback();
-            atom_of[nid] = py::int_(i);
-        }
+    for (int i = 0; i < n; ++i) {
+        py::int_ idx(i);
+        for (py::handle nid : py::reinterpret_borrow<py::object>(atoms[i].attr("node_ids")))
+            if (PyDict_SetDefault(atom_of.ptr(), nid.ptr(), idx.ptr()) != idx.ptr()) throw Fallback();
+    }
     auto atom_get = [&](py::handle k) -> int {
         PyObject *v = PyDict_GetItem(atom_of.ptr(), k.ptr());
         return v ? (int)PyLong_AsLong(v) : -1;
     };
 
+    // per value node (keyed by the node object): is it a value, a parameter,
+    // its bytes at microbatch 1 -- read once, used by every reader
+    struct VInfo {
+        bool is_value = false, is_param = false, size_ok = false;
+        int64_t size = 0;
+    };
+    std::unordered_map<PyObject *, VInfo> vcache;
+    vcache.reserve(2 * (size_t)py::len(nodes) + 16);
+    auto vinfo = [&](py::handle node) -> const VInfo & {
+        auto it = vcache.find(node.ptr());
+        if (it != vcache.end()) return it->second;
+        VInfo x;
+        py::object value = ga(node, names().value);
+        x.is_value = !value.is_none();
+        if (x.is_value) {
+            x.is_param = PyObject_IsTrue(ga(value, names().is_param).ptr()) == 1;
+            try {
+                x.size = size1(value);
+                x.size_ok = true;
+            } catch (Fallback &) {
+            }
+        }
+        return vcache.emplace(node.ptr(), x).first->second;
+    };
+    auto vsize = [](const VInfo &x) -> int64_t {
+        if (!x.size_ok) throw Fallback();
+        return x.size;
+    };
+
     std::vector<py::object> inputs_of_atom(n);
     py::dict listing;
     for (int a = 0; a < n; ++a) {
+        py::int_ idx(a);
         inputs_of_atom[a] = py::reinterpret_steal<py::object>(
             PyFrozenSet_New(atoms[a].attr("input_values").ptr()));
         for (py::handle v : inputs_of_atom[a]) {
             PyObject *lst = PyDict_GetItem(listing.ptr(), v.ptr());
             if (!lst) {
                 py::list l;
-                l.append(a);
+                l.append(idx);
                 listing[v] = l;
             } else {
-                PyList_Append(lst, py::int_(a).ptr());
+                PyList_Append(lst, idx.ptr());
             }
         }
     }
@@ -124,14 +156,14 @@ py::dict flatten(py::object partition, py::object model) {
     for (size_t i = 0; i < py::len(in_ids); ++i) {
         py::handle v = in_ids[i];
         in_index[v] = py::int_(i);
-        py::object node = nodes[v];
-        if (!node.attr("is_value").cast<bool>()) throw Fallback();
+        const VInfo &vi = vinfo(dget(nodes, v));
+        if (!vi.is_value) throw Fallback();
         const int own = atom_get(v);
         const bool is_input = PySequence_Contains(graph_inputs.ptr(), v.ptr()) == 1;
         in_owner.push_back((is_input || own < 0) ? -1 : own);
-        in_size.push_back(size1(node.attr("value")));
-        for (py::handle a : py::reinterpret_borrow<py::list>(listing[v]))
-            in_atoms.push_back(a.cast<int32_t>());
+        in_size.push_back(vsize(vi));
+        for (py::handle a : py::reinterpret_borrow<py::list>(dget(listing, v)))
+            in_atoms.push_back((int32_t)PyLong_AsLong(a.ptr()));
         in_atoms_off.push_back((int32_t)in_atoms.size());
     }
     auto in_index_of = [&](py::handle v) -> int {
@@ -149,33 +181,33 @@ py::dict flatten(py::object partition, py::object model) {
         const int a = atom_get(nid);
         if (a < 0) continue;
         const Names &N = names();
-        py::object value = ga(node, N.value);
-        if (!value.is_none()) {
-            if (PyObject_IsTrue(ga(value, N.is_param).ptr()))
-                atom_param[a] += as_int(ga(value, N.fixed_bytes).ptr());
+        const VInfo &self = vinfo(node);
+        if (self.is_value) {
+            if (self.is_param)
+                atom_param[a] += as_int(ga(ga(node, N.value), N.fixed_bytes).ptr());
             continue;
         }
         int64_t fp = 0;
         for (py::handle vid : dget(succ_d, nid)) {
-            py::object info = ga(dget(nodes, vid), N.value);
-            if (!info.is_none() && !PyObject_IsTrue(ga(info, N.is_param).ptr())) fp += size1(info);
+            const VInfo &x = vinfo(dget(nodes, vid));
+            if (x.is_value && !x.is_param) fp += vsize(x);
         }
         task_prod1.push_back(fp);
         py::object task = ga(node, N.task);
         tnodes.append(task);
         const py::object &ins = inputs_of_atom[a];
         for (py::handle vid : dget(pred_d, nid)) {
-            py::object info = ga(dget(nodes, vid), N.value);
-            if (info.is_none() || PyObject_IsTrue(ga(info, N.is_param).ptr())) continue;
+            const VInfo &x = vinfo(dget(nodes, vid));
+            if (!x.is_value || x.is_param) continue;
             if (PySet_Contains(ins.ptr(), vid.ptr()) == 1) {
                 const int own = in_owner[in_index_of(vid)];
                 if (own >= 0) {
                     dep_owner.push_back(own);
-                    dep_size.push_back(size1(info));
+                    dep_size.push_back(vsize(x));
                 }
             } else {
                 if (atom_get(vid) != a) throw Fallback();     // cross-atom read: Python raises
-                fp += size1(info);
+                fp += vsize(x);
             }
         }
         dep_off.push_back((int32_t)dep_owner.size());
@@ -190,13 +222,15 @@ py::dict flatten(py::object partition, py::object model) {
     py::dict owner_d = partition.attr("_value_owner");
     py::dict cons_d = partition.attr("_consumer_atoms");
     py::dict ppred_d = pg.attr("_pred");
-    py::object value_size = pg.attr("value_size");
+    py::dict pnodes = pg.attr("nodes");
     std::vector<int64_t> dep_keys;
     std::vector<int32_t> tr_owner;
     std::vector<int64_t> tr_size;
     std::vector<std::vector<int32_t>> tr_cons, atom_tr(n);
-    py::object one = py::int_(1);
-    for (py::handle vid : pg.attr("value_ids")()) {
+    for (auto item : pnodes) {                      // value_ids() (graph.py:140-141)
+        py::handle vid = item.first;
+        const VInfo &vi = vinfo(item.second);
+        if (!vi.is_value) continue;
         const int owner = (int)PyLong_AsLong(dget(owner_d, vid).ptr());
         std::vector<int32_t> cons;
         for (py::handle c : dget(cons_d, vid)) cons.push_back((int32_t)PyLong_AsLong(c.ptr()));
@@ -210,8 +244,7 @@ py::dict flatten(py::object partition, py::object model) {
         if (!foreign.empty()) {
             const int e = (int)tr_owner.size();
             tr_owner.push_back(owner);
-            py::object sz = value_size(vid, one);
-            tr_size.push_back(as_int(sz.ptr()));
+            tr_size.push_back(vsize(vi));                  // value_size(vid, 1) (graph.py:151-155)
             std::vector<int32_t> members(foreign);
             members.push_back(owner);
             std::sort(members.begin(), members.end());
