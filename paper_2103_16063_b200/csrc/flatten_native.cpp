@@ -327,11 +327,40 @@ py::dict flatten_blocks(py::object bs) {
     py::object graph_inputs = g.attr("inputs");
 
     py::dict atom_of;
-    for (int i = 0; i < n_atoms; ++i)
-        for (py::handle nid : py::reinterpret_borrow<py::object>(atoms[i].attr("node_ids"))) {
-            if (atom_of.contains(nid)) throw Fallback();
-            atom_of[nid] = py::int_(i);
+    for (int i = 0; i < n_atoms; ++i) {
+        py::int_ idx(i);
+        for (py::handle nid : py::reinterpret_borrow<py::object>(atoms[i].attr("node_ids")))
+            if (PyDict_SetDefault(atom_of.ptr(), nid.ptr(), idx.ptr()) != idx.ptr()) throw Fallback();
+    }
+    // per value node (keyed by the node object): value?, parameter?, its two
+    // byte counts -- read once, used by every reader
+    struct VInfo {
+        bool is_value = false, is_param = false, ok = false;
+        int64_t fix = 0, ps = 0;
+    };
+    std::unordered_map<PyObject *, VInfo> vcache;
+    vcache.reserve(2 * (size_t)py::len(nodes) + 16);
+    auto vinfo = [&](py::handle node) -> const VInfo & {
+        auto it = vcache.find(node.ptr());
+        if (it != vcache.end()) return it->second;
+        VInfo x;
+        py::object value = ga(node, N.value);
+        x.is_value = !value.is_none();
+        if (x.is_value) {
+            x.is_param = PyObject_IsTrue(ga(value, N.is_param).ptr()) == 1;
+            try {
+                x.fix = as_int(ga(value, N.fixed_bytes).ptr());
+                x.ps = as_int(ga(value, N.bytes_per_sample).ptr());
+                x.ok = true;
+            } catch (Fallback &) {
+            }
         }
+        return vcache.emplace(node.ptr(), x).first->second;
+    };
+    auto need = [](const VInfo &x) -> const VInfo & {
+        if (!x.ok) throw Fallback();
+        return x;
+    };
     std::vector<int> block_of_atom(n_atoms, -1);
     int covered = 0;
     for (int bi = 0; bi < nb; ++bi)
@@ -378,9 +407,8 @@ py::dict flatten_blocks(py::object bs) {
     for (size_t i = 0; i < py::len(in_ids); ++i) {
         py::handle vid = in_ids[i];
         in_index[vid] = py::int_(i);
-        py::handle node = dget(nodes, vid);
-        py::object info = ga(node, N.value);
-        if (info.is_none()) throw Fallback();                 // not a value
+        const VInfo &vi = vinfo(dget(nodes, vid));
+        if (!vi.is_value) throw Fallback();                   // not a value
         std::vector<int32_t> cb = cons_sets[PyLong_AsLong(dget(cons_of, vid).ptr())];
         std::sort(cb.begin(), cb.end());
         cb.erase(std::unique(cb.begin(), cb.end()), cb.end());
@@ -396,8 +424,8 @@ py::dict flatten_blocks(py::object bs) {
         in_ob.push_back(ob);
         in_cons.insert(in_cons.end(), cb.begin(), cb.end());
         in_off.push_back((int32_t)in_cons.size());
-        in_fix.push_back(as_int(ga(info, N.fixed_bytes).ptr()));
-        in_ps.push_back(as_int(ga(info, N.bytes_per_sample).ptr()));
+        in_fix.push_back(need(vi).fix);
+        in_ps.push_back(vi.ps);
     }
     auto in_index_of = [&](py::handle v) -> int {
         PyObject *x = PyDict_GetItem(in_index.ptr(), v.ptr());
@@ -413,16 +441,16 @@ py::dict flatten_blocks(py::object bs) {
         py::handle nid = kv.first, node = kv.second;
         const int b = blk_of(nid);
         if (b < 0) continue;
-        py::object info = ga(node, N.value);
-        if (!info.is_none()) {
-            if (PyObject_IsTrue(ga(info, N.is_param).ptr())) {
-                blk_param[b] += as_int(ga(info, N.fixed_bytes).ptr());
+        const VInfo &self = vinfo(node);
+        if (self.is_value) {
+            if (self.is_param) {
+                blk_param[b] += as_int(ga(ga(node, N.value), N.fixed_bytes).ptr());
             } else if (PyTuple_GET_SIZE(dget(pred_d, nid).ptr()) == 0) {     // no producer
                 const bool span_input = PySequence_Contains(graph_inputs.ptr(), nid.ptr()) == 1 &&
                                         in_index_of(nid) >= 0;
                 if (!span_input) {
-                    blk_res_fix[b] += as_int(ga(info, N.fixed_bytes).ptr());
-                    blk_res_ps[b] += as_int(ga(info, N.bytes_per_sample).ptr());
+                    blk_res_fix[b] += need(self).fix;
+                    blk_res_ps[b] += self.ps;
                 }
             }
             continue;
@@ -431,10 +459,10 @@ py::dict flatten_blocks(py::object bs) {
         const int a = atom_get(nid);
         int64_t pf = 0, pp = 0;
         for (py::handle vid : dget(succ_d, nid)) {
-            py::object vi = ga(dget(nodes, vid), N.value);
-            if (!vi.is_none() && !PyObject_IsTrue(ga(vi, N.is_param).ptr())) {
-                pf += as_int(ga(vi, N.fixed_bytes).ptr());
-                pp += as_int(ga(vi, N.bytes_per_sample).ptr());
+            const VInfo &vi = vinfo(dget(nodes, vid));
+            if (vi.is_value && !vi.is_param) {
+                pf += need(vi).fix;
+                pp += vi.ps;
             }
         }
         blk_res_fix[b] += pf;
@@ -442,10 +470,10 @@ py::dict flatten_blocks(py::object bs) {
         int64_t bf = pf, bp = pp;
         const py::object &ins = inputs_of_atom[a];
         for (py::handle vid : dget(pred_d, nid)) {
-            py::object vi = ga(dget(nodes, vid), N.value);
-            if (vi.is_none() || PyObject_IsTrue(ga(vi, N.is_param).ptr())) continue;
-            const int64_t vf = as_int(ga(vi, N.fixed_bytes).ptr());
-            const int64_t vp = as_int(ga(vi, N.bytes_per_sample).ptr());
+            const VInfo &vi = vinfo(dget(nodes, vid));
+            if (!vi.is_value || vi.is_param) continue;
+            const int64_t vf = need(vi).fix;
+            const int64_t vp = vi.ps;
             const int i = in_index_of(vid);
             if (i < 0) {
                 bf += vf;
