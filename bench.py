@@ -93,16 +93,17 @@ class Clocks:
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}_{index}.csv")
         self.index = index
 
+    QUERY = ["--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+             "--format=csv,noheader,nounits"]
+
     def __enter__(self):
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                ["nvidia-smi", f"--id={self.index}", *self.QUERY, "-lms", "200"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -116,6 +117,14 @@ class Clocks:
             except Exception:
                 self.proc.kill()
             self.fh.close()
+            if os.path.getsize(self.path) == 0:
+                # a region shorter than the sampling period: one sample at its end
+                try:
+                    with open(self.path, "w") as fh:
+                        subprocess.run(["nvidia-smi", f"--id={self.index}", *self.QUERY],
+                                       stdout=fh, stderr=subprocess.DEVNULL, timeout=30)
+                except Exception:
+                    pass
 
     def summary(self):
         try:
@@ -460,7 +469,7 @@ def sweep(arm, dadd_peak, headline, line):
 
 def config_latencies(arm):
     """Reference-semantics partition search on C1-C4 through the public API:
-    partition_blocks + form_stage, median of 5 warm runs + 1 cold, with the
+    partition_blocks + form_stage, median of 10 warm runs + 1 cold, with the
     phase split, beside the reference's own times measured in this run
     (baseline/ref_arm.py configs, one process per config)."""
     from paper_2103_16063_b200 import flatten as _flat
@@ -472,7 +481,7 @@ def config_latencies(arm):
     for name in ("C1", "C2", "C3", "C4"):
         part, model, k, batch, cl = config_partition(name)
         tb, ts, pb_t, fs_t = [], [], [], []
-        for i in range(6):
+        for i in range(11):
             _flat._ATOM_CACHE.clear()
             ctx.problem_owner = None
             ctx.lib.pc_reset_cache(ctx.h)

@@ -671,9 +671,10 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             d_cellpre = d_colpre + (n + 1);
             CUDA_TRY(ctx, cudaMemcpyAsync(d_colpre, col_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
             CUDA_TRY(ctx, cudaMemcpyAsync(d_cellpre, cell_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
-            CUDA_TRY(ctx, ctx->live_d.ensure(8 * (size_t)val_cells + 64));
+            CUDA_TRY(ctx, ctx->live_d.ensure(16 * (size_t)val_cells + 128));
             bt.live_count = ctx->live_d.as<unsigned long long>();
             bt.live = bt.live_count + 8;
+            bt.live_lb = (float2 *)(bt.live + val_cells);
         }
         CUDA_TRY(ctx, cudaMemsetAsync(ob, 0, 64 + 3 * sizeof(unsigned long long) * (size_t)n + 64, ctx->st));
         CUDA_TRY(ctx, ctx->counters_d.ensure((8 + FMAX + 3 * WORK_SLOTS) * sizeof(unsigned long long)));

@@ -208,6 +208,7 @@ struct DPBatch {
     // listed by k_dp_triage, walked by k_dp_level_list
     unsigned long long *live;
     unsigned long long *live_count;  // [0] cells listed, [1] cells taken (k_dp_level_list)
+    float2 *live_lb;                 // each live cell's suffix lower bounds (lbf, lbb), rounded down
     double *pool_tf[2];
     double *pool_tb[2];
     unsigned long long *vpool_used[2];  // [n_calls] per parity

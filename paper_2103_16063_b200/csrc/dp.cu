@@ -279,7 +279,8 @@ __device__ __forceinline__ bool prefix_bounds(const DPBatch &B, const CallDesc &
 // One cell (b, d) = (s + idx / B, s + idx % B) of call c at level s, by one
 // warp (w = its warp in the CTA), frontier capacity 32 * SLOTS.
 template <bool DERIVED, int SLOTS>
-__device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t idx) {
+__device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t idx,
+                                        const float2 *lbp = nullptr) {
     const CallDesc cd = B.calls[c];
     const int w = threadIdx.x >> 5;
     const int bi = (int)(idx / cd.B);
@@ -314,6 +315,10 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
     if (bounded) {
         if (s == cd.S) {
             if (b != nb || d != cd.D) lbf = INFINITY;
+        } else if (lbp) {               // listed by k_dp_triage with its suffix bounds
+            const float2 v = *lbp;
+            lbf = v.x;
+            lbb = v.y;
         } else {
             suffix_bounds<DERIVED>(B, cd, keyidx, s, b, d, lbf, lbb);
         }
@@ -679,7 +684,8 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_LIST_MIN_BLOCKS) k_dp_level_
             if (t >= n) break;
             for (int g = 0; g < PC_LIST_GRAB && t + g < n; ++g) {
                 const unsigned long long e = B.live[t + g];
-                dp_cell<DERIVED, SLOTS>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)));
+                dp_cell<DERIVED, SLOTS>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)),
+                                        B.live_lb + t + g);
             }
         }
     } else {
@@ -687,7 +693,8 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_LIST_MIN_BLOCKS) k_dp_level_
         for (unsigned long long t = (unsigned long long)blockIdx.x * DP_WARPS + (threadIdx.x >> 5);
              t < n; t += stride) {
             const unsigned long long e = B.live[t];
-            dp_cell<DERIVED, SLOTS>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)));
+            dp_cell<DERIVED, SLOTS>(B, s, (int)(e >> 40), (int64_t)(e & ((1ull << 40) - 1)),
+                                    B.live_lb + t);
         }
     }
 }
@@ -705,6 +712,7 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
     bool live = false;
     int c = 0;
     int64_t idx = 0;
+    float2 lb = make_float2(0.f, 0.f);
     if (g < cell_prefix[n_active]) {
         int lo = 0, hi = n_active;
         while (hi - lo > 1) {
@@ -721,12 +729,14 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
         if (cd.U < INFINITY) {
             if (s == cd.S) {
                 dead = b != nb || d != cd.D;
-            } else if (s > 1) {
+            } else {
                 double lbf = 0.0, lbb = 0.0;
                 suffix_bounds<DERIVED>(B, cd, keyidx, s, b, d, lbf, lbb);
                 double plf, plb;
-                if (prefix_bounds<DERIVED>(B, cd, keyidx, s, b, d, plf, plb))
+                if (s > 1 && prefix_bounds<DERIVED>(B, cd, keyidx, s, b, d, plf, plb))
                     dead = __dadd_rn(dmax_ref(plf, lbf), dmax_ref(plb, lbb)) > cd.U;
+                // handed to dp_cell rounded down: still lower bounds
+                lb = make_float2(__double2float_rd(lbf), __double2float_rd(lbb));
             }
         }
         if (dead) {
@@ -760,7 +770,11 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
     unsigned long long base = 0;
     if (lane == 0 && m) base = atomicAdd(B.live_count, (unsigned long long)__popc(m));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (live) B.live[base + __popc(m & ((1u << lane) - 1u))] = ((unsigned long long)c << 40) | (unsigned long long)idx;
+    if (live) {
+        const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
+        B.live[at] = ((unsigned long long)c << 40) | (unsigned long long)idx;
+        B.live_lb[at] = lb;
+    }
 }
 
 void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
