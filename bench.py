@@ -358,7 +358,7 @@ def run_ours(a):
     # schedule (i): widening levels in order, stop at the first
     # feasible one -- the reference's own order, same answer
     lvl = []
-    for i in range(4):
+    for i in range(6):
         arm.fresh()
         arm.barrier()
         t0 = time.perf_counter()

@@ -894,11 +894,18 @@ void launch_plan_bound(const DPBatch &b, int n, const int32_t *pos, const int32_
 // the raw forward time alone passes T (raw times grow with the span).  The
 // DP objective of the plan packed at the smallest T found (max-folded charged
 // times as in k_plan_bound) bounds the optimum; +inf if nothing packs.  One
-// warp per call.
+// CTA per call: the search for the smallest T that packs is GB_WARPS-wide
+// (each warp packs one candidate T per round), so a call needs 1 + GB_ROUNDS
+// + 1 sequential packs instead of the ~16 of a bisection.
+constexpr int GB_WARPS = 8;     // T values a call tries at once
+constexpr int GB_ROUNDS = 5;    // 9^5 = 59049: finer than 14 halvings
 template <bool DERIVED>
-__global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U) {
-    const int w = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+__global__ void __launch_bounds__(GB_WARPS * 32) k_greedy_bound(DPBatch Bt, int n, const int32_t *pos,
+                                                                double *U) {
+    const int w = blockIdx.x;
+    const int wi = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    __shared__ int s_res[GB_WARPS];
     if (w >= n) return;
     const CallDesc cd = Bt.calls[pos[w]];
     const int16_t *keyidx = Bt.keyidx + cd.key_off;
@@ -906,7 +913,7 @@ __global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U)
     const int q = D / S, r = D % S;
     const int kq = keyidx[q], kq1 = r > 0 ? keyidx[q + 1] : kq;
     if (kq < 0 || kq1 < 0) {
-        if (lane == 0) U[w] = INFINITY;
+        if (threadIdx.x == 0) U[w] = INFINITY;
         return;
     }
     // charged times of stage i = [lo, hi) (k_plan_bound's arithmetic)
@@ -979,37 +986,60 @@ __global__ void k_greedy_bound(DPBatch Bt, int n, const int32_t *pos, double *U)
         return 1;
     };
     double obj = INFINITY, dummy;
-    // a T that packs: from the balanced estimate (1 + beta) t(0, nb) / S,
-    // doubling; then bisection down
+    // a T that packs: from the balanced estimate (1 + beta) t(0, nb) / S, the
+    // warps trying its doublings at once (the first that packs wins; a give-up
+    // before it ends the search); then the (GB_WARPS + 1)-ary search down
     const double total = fabs(Bt.key_tf[kq][hm_idx(0, nb)]);
-    double hiT = 1.5 * (1.0 + Bt.beta) * total / S + 1e-300;
-    int tries = 0;
-    for (;;) {
-        const int r = pack(hiT, false, dummy);
-        if (r > 0) break;
-        if (r < 0 || ++tries > 8) {
-            if (lane == 0) U[w] = INFINITY;
-            return;
+    const double T0 = 1.5 * (1.0 + Bt.beta) * total / S + 1e-300;
+    {
+        const int r0 = pack(ldexp(T0, wi), false, dummy);
+        if (lane == 0) s_res[wi] = r0;
+    }
+    __syncthreads();
+    int tries = -1;
+    for (int j = 0; j < GB_WARPS; ++j)
+        if (s_res[j] != 0) {
+            if (s_res[j] > 0) tries = j;
+            break;
         }
-        hiT *= 2.0;
+    if (tries < 0) {
+        if (threadIdx.x == 0) U[w] = INFINITY;
+        return;
     }
+    double hiT = ldexp(T0, tries);
     double loT = tries ? 0.5 * hiT : 0.0;
-    for (int it = 0; it < 14; ++it) {        // T within ~1e-4 relative: ample for a bound
-        const double mid = 0.5 * (loT + hiT);
-        if (pack(mid, false, dummy) > 0) hiT = mid; else loT = mid;
+    for (int round = 0; round < GB_ROUNDS; ++round) {
+        __syncthreads();                        // s_res of the previous round read
+        const double Tw = loT + (hiT - loT) * (double)(wi + 1) / (double)(GB_WARPS + 1);
+        const int r = pack(Tw, false, dummy);
+        if (lane == 0) s_res[wi] = r;
+        __syncthreads();
+        double nlo = loT, nhi = hiT;            // the smallest packing point, the failure below it
+        for (int j = GB_WARPS - 1; j >= 0; --j) {
+            const double Tj = loT + (hiT - loT) * (double)(j + 1) / (double)(GB_WARPS + 1);
+            if (s_res[j] > 0) {
+                nhi = Tj;
+            } else {
+                nlo = Tj;
+                break;
+            }
+        }
+        loT = nlo;
+        hiT = nhi;
     }
-    const bool ok = pack(hiT, true, obj) > 0;
-    if (lane == 0) U[w] = ok ? obj : INFINITY;
+    if (wi == 0) {
+        const bool ok = pack(hiT, true, obj) > 0;
+        if (lane == 0) U[w] = ok ? obj : INFINITY;
+    }
 }
 
 void launch_greedy_bound(const DPBatch &b, int n, const int32_t *pos, double *U, bool derived,
                          cudaStream_t st) {
     if (n <= 0) return;
-    const unsigned blocks = (unsigned)((n * 32 + 127) / 128);
     if (derived)
-        k_greedy_bound<true><<<blocks, 128, 0, st>>>(b, n, pos, U);
+        k_greedy_bound<true><<<n, GB_WARPS * 32, 0, st>>>(b, n, pos, U);
     else
-        k_greedy_bound<false><<<blocks, 128, 0, st>>>(b, n, pos, U);
+        k_greedy_bound<false><<<n, GB_WARPS * 32, 0, st>>>(b, n, pos, U);
 }
 
 // ---------------------------------------------------------------- bound: non-empty prefix
