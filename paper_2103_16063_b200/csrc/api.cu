@@ -315,7 +315,16 @@ static int ensure_keys(pc_ctx *ctx, const std::vector<std::pair<int64_t, int>> &
         CUDA_TRY(ctx, cudaMemcpyAsync(d_pc, pcut.data(), sizeof(double *) * nf, cudaMemcpyHostToDevice, ctx->st));
         CUDA_TRY(ctx, cudaMemcpyAsync(d_pff, pff.data(), sizeof(int32_t *) * nf, cudaMemcpyHostToDevice, ctx->st));
         const double *raw_tf = nullptr, *raw_tb = nullptr;
-        if (!P.monotone) {
+        if (P.monotone) {
+            // per-key task times, read by the span fold (k_span_rows)
+            CUDA_TRY(ctx, ctx->raw_d.ensure(sizeof(double) * 2 * (size_t)nf * P.n_tasks + 64));
+            double *r = ctx->raw_d.as<double>();
+            launch_key_task_times(P, nf, d_km, r, r + (size_t)nf * P.n_tasks, ctx->st);
+            ctx->launches++;
+            if (int rc = check_launch(ctx, "key_task_times")) return rc;
+            raw_tf = r;
+            raw_tb = r + (size_t)nf * P.n_tasks;
+        } else {
             CUDA_TRY(ctx, ctx->raw_d.ensure(sizeof(double) * 2 * (size_t)nf * tri));
             double *r = ctx->raw_d.as<double>();
             launch_span_time_general(P, nf, d_km, r, r + (size_t)nf * tri, ctx->st);

@@ -260,6 +260,8 @@ constexpr int MAX_D_KEY = (1 << 12) - 1;
 void launch_in_tables(const DevProblem &p, int64_t *in_fix, int64_t *in_ps, cudaStream_t st);
 void launch_span_time_general(const DevProblem &p, int n_keys, const int64_t *keys_m,
                               double *raw_tf, double *raw_tb, cudaStream_t st);
+void launch_key_task_times(const DevProblem &p, int n_keys, const int64_t *keys_m, double *x,
+                           double *y, cudaStream_t st);
 void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_m,
                            const int32_t *keys_ckpt, const double *raw_tf, const double *raw_tb,
                            double *const *tf, double *const *tb, double *const *cut,

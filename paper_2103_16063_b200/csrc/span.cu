@@ -106,7 +106,9 @@ void launch_span_time_general(const DevProblem &p, int n_keys, const int64_t *ke
 //   * running max of task footprints (costs.py:150-155), each task's
 //     footprint counting only predecessors owned in blocks >= lo;
 //   * in the monotone case the time fold itself (blocks in sorted-id order,
-//     so extending hi continues the reference's fold exactly);
+//     so extending hi continues the reference's fold exactly) over the key's
+//     task times (raw_tf / raw_tb: [key][task], k_key_task_times); otherwise
+//     raw_tf / raw_tb hold the general fold's span times ([key][tri]);
 //   * memory (costs.py:157-159) -> feasibility (stages.py:230) folded into the
 //     table as NaN;
 //   * its row of the per-key cut-time table (stages.py:147-157).
@@ -125,7 +127,6 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
     const int k = (int)(gid / nb);
     const int lo = (int)(gid % nb);
     const int64_t m = keys_m[k];
-    const double md = (double)m;
     const int ckpt = keys_ckpt[k];
     const int64_t tri = tri_size(nb);
     double *out_f = tf_out[k];
@@ -148,11 +149,9 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
             for (int d = p.dep_off[t]; d < p.dep_off[t + 1]; ++d)
                 if (p.dep_ob[d] >= lo) fp += p.dep_fix[d] + m * p.dep_ps[d];
             run_fp = fp > run_fp ? fp : run_fp;
-            if (MONO) {
-                double x, y;
-                task_times(p, ov, t, md, x, y);
-                tf = __dadd_rn(tf, x);
-                tb = __dadd_rn(tb, y);
+            if (MONO) {                 // this key's task times (k_key_task_times)
+                tf = __dadd_rn(tf, raw_tf[(int64_t)k * p.n_tasks + t]);
+                tb = __dadd_rn(tb, raw_tb[(int64_t)k * p.n_tasks + t]);
             }
         }
         const int64_t idx = row + (hi - lo - 1);
@@ -180,6 +179,27 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
         }
     }
     if (bad) atomicOr(mismatch, 1);
+}
+
+// Per (key, task): the task's forward / backward time at the key's share
+// (task_times, costs.py:130-140).  Monotone graphs fold them along every
+// span row; computing them once per key keeps the fp64 division out of the
+// O(nb^2) fold (same operation, same value).
+__global__ void k_key_task_times(DevProblem p, int n_keys, const int64_t *keys_m, double *x,
+                                 double *y) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (int64_t)n_keys * p.n_tasks) return;
+    const int k = (int)(gid / p.n_tasks);
+    const int t = (int)(gid % p.n_tasks);
+    const int64_t m = keys_m[k];
+    task_times(p, ov_index(p, m), t, (double)m, x[gid], y[gid]);
+}
+
+void launch_key_task_times(const DevProblem &p, int n_keys, const int64_t *keys_m, double *x,
+                           double *y, cudaStream_t st) {
+    const int64_t n = (int64_t)n_keys * p.n_tasks;
+    if (n <= 0) return;
+    k_key_task_times<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, n_keys, keys_m, x, y);
 }
 
 void launch_span_dp_tables(const DevProblem &p, int n_keys, const int64_t *keys_m,
