@@ -1026,9 +1026,21 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     ctx->last_cands = 0;
     ctx->last_inserts = 0;
     ctx->launches = 0;
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const size_t cap = free_b / 2;
+    // free device memory bounds the batch (chunks below).  cudaMemGetInfo
+    // itself sporadically stalls for 5-40 ms (measured on the pool's boxes:
+    // the C1-C4 latencies' outliers), so a batch far below the last reading
+    // reuses it; only a batch that could come near it queries again.
+    size_t est = 0;
+    for (auto &c : calls) {
+        const int64_t A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
+        est += (size_t)A * B * (2 * (5 + 16 * 12) + (size_t)c.S * (5 + 4 * 5));
+    }
+    if (ctx->mem_free == 0 || est > ctx->mem_free / 16) {
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        ctx->mem_free = free_b;
+    }
+    const size_t cap = ctx->mem_free / 2;
     // Objective bound (dp.cu): every call of the batch gets U from a greedy
     // plan (k_greedy_bound; within 1% of the optimum at the median on the C5
     // chains).  PIPECUT_B200_BOUND_WAVES=1 instead runs the calls in waves of

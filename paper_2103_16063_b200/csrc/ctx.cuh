@@ -137,6 +137,7 @@ struct pc_ctx {
     int64_t launches = 0;   // all kernel launches since the last reset
     DBuf counters_d;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
+    size_t mem_free = 0;    // last cudaMemGetInfo reading (run_calls_impl)
 };
 
 namespace pcb {
