@@ -141,12 +141,25 @@ __global__ void k_span_rows(DevProblem p, int n_keys, const int64_t *keys_m,
     int64_t run_fp = 0;
     bool bad = false;
     const int64_t row = tri_row(lo, nb);
+    // The block -> task indirection is loaded one block ahead (the row is a
+    // chain of dependent loads otherwise: offsets, task, its dependencies).
+    int q0 = p.blk_off[lo], q1 = p.blk_off[lo + 1];
+    int t0 = q0 < q1 ? p.blk_tasks[q0] : 0;
+    int e0 = q0 < q1 ? p.dep_off[t0] : 0, e1 = q0 < q1 ? p.dep_off[t0 + 1] : 0;
     for (int hi = lo + 1; hi <= nb; ++hi) {
-        const int blk = hi - 1;
-        for (int q = p.blk_off[blk]; q < p.blk_off[blk + 1]; ++q) {
-            const int t = p.blk_tasks[q];
+        const int c0 = q0, c1 = q1, ct = t0, ce0 = e0, ce1 = e1;
+        if (hi < nb) {
+            q0 = c1;
+            q1 = p.blk_off[hi + 1];
+            t0 = q0 < q1 ? p.blk_tasks[q0] : 0;
+            e0 = q0 < q1 ? p.dep_off[t0] : 0;
+            e1 = q0 < q1 ? p.dep_off[t0 + 1] : 0;
+        }
+        for (int q = c0; q < c1; ++q) {
+            const int t = q == c0 ? ct : p.blk_tasks[q];
             int64_t fp = task_fp(p, ov, t, m);
-            for (int d = p.dep_off[t]; d < p.dep_off[t + 1]; ++d)
+            const int d0 = q == c0 ? ce0 : p.dep_off[t], d1 = q == c0 ? ce1 : p.dep_off[t + 1];
+            for (int d = d0; d < d1; ++d)
                 if (p.dep_ob[d] >= lo) fp += p.dep_fix[d] + m * p.dep_ps[d];
             run_fp = fp > run_fp ? fp : run_fp;
             if (MONO) {                 // this key's task times (k_key_task_times)
