@@ -40,4 +40,16 @@ for _ in range(6):
         partition_blocks(p, m, rng.randint(1, 6))
     except pc.CompactionStuck:
         pass
+# refinement on the device: C1 (moves, rejected candidates), C4 (cluster
+# kernel), a fan graph (dozens of levels); the bounded DP path on a small chain
+from paper_2103_16063_b200.workloads import config_partition
+for name in ("C1", "C4"):
+    part, model, k, batch, cl = config_partition(name)
+    b = partition_blocks(part, model, k)
+    if name == "C1":
+        form_stage(cl.num_nodes, cl.devices_per_node, batch, b)
+p, m = cases.blocks_inputs(cases.fan_graph(random.Random(2), 90))
+partition_blocks(p, m, 3)
+os.environ["PIPECUT_B200_BOUND_MIN_VISITS"] = "0"
+form_stage(4, 8, 256, cases.c5_blockset(128, 32, jitter_seed=3))
 print("sanitize smoke done")
