@@ -586,12 +586,12 @@ __device__ __forceinline__ void dp_cell(const DPBatch &B, int s, int c, int64_t 
         bool zl = false, rl = false;
         for (int dp = base + lane; dp < d; dp += 32) {
             const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
-            const int32_t upto = col[b - 1];
+            const int32_t upto = col[b - 1] & 0xffff;
             if (upto == 0) continue;
             const int kk = keyidx[d - dp];
             if (kk < 0) { zl = true; continue; }
             const int x = max(base, B.key_ffb[kk][b]);
-            if (x <= b - 1 && upto > (x > base ? col[x - 1] : 0)) rl = true;
+            if (x <= b - 1 && upto > (x > base ? col[x - 1] & 0xffff : 0)) rl = true;
         }
         zero = __any_sync(0xffffffffu, zl);
         reach = __any_sync(0xffffffffu, rl);
@@ -735,6 +735,24 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
                 double plf, plb;
                 if (s > 1 && prefix_bounds<DERIVED>(B, cd, keyidx, s, b, d, plf, plb))
                     dead = __dadd_rn(dmax_ref(plf, lbf), dmax_ref(plb, lbb)) > cd.U;
+                if (s > 1 && !dead) {
+                    // no predecessor with entries among the feasible spans of
+                    // any column: dp_cell would load no pair and end empty
+                    // (the reference's emptiness, below, is the same either way)
+                    const int base = s - 1;
+                    const int32_t *rp = B.reach_pre[(s - 1) & 1] + cd.val_off;
+                    bool pred = false;
+                    for (int dp = d - 1; dp >= base && !pred; --dp) {
+                        const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
+                        const int32_t upto = col[b - 1] >> 16;
+                        if (upto == 0) continue;
+                        const int kk = keyidx[d - dp];
+                        if (kk < 0) continue;
+                        const int x = max(base, B.key_ffb[kk][b]);
+                        pred = x <= b - 1 && upto > (x > base ? col[x - 1] >> 16 : 0);
+                    }
+                    dead = !pred;
+                }
                 // handed to dp_cell rounded down: still lower bounds
                 lb = make_float2(__double2float_rd(lbf), __double2float_rd(lbb));
             }
@@ -750,12 +768,12 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
                 const int32_t *rp = B.reach_pre[(s - 1) & 1] + cd.val_off;
                 for (int dp = base; dp < d; ++dp) {
                     const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
-                    const int32_t upto = col[b - 1];
+                    const int32_t upto = col[b - 1] & 0xffff;
                     if (upto == 0) continue;
                     const int kk = keyidx[d - dp];
                     if (kk < 0) { zero = true; continue; }
                     const int x = max(base, B.key_ffb[kk][b]);
-                    if (x <= b - 1 && upto > (x > base ? col[x - 1] : 0)) reach = true;
+                    if (x <= b - 1 && upto > (x > base ? col[x - 1] & 0xffff : 0)) reach = true;
                 }
             }
             const int64_t cell = (int64_t)di * cd.A + bi;
@@ -1064,7 +1082,11 @@ __global__ void k_reach_prefix(DPBatch Bt, int s, int n_active, const int64_t *c
     int32_t run = 0;
     for (int b0 = 0; b0 < cd.A; b0 += 32) {
         const int bi = b0 + lane;
-        const int v = bi < cd.A && (vcol[bi] & CNT_MASK) != 0 ? 1 : 0;
+        // low half: cells the reference holds non-empty (count > 0 or
+        // CNT_REACH); high half: cells with entries (A <= 16383 keeps the
+        // two prefix counts apart)
+        const uint8_t byte = bi < cd.A ? vcol[bi] : 0;
+        const int v = ((byte & CNT_MASK) != 0 ? 1 : 0) | (cnt_entries(byte) > 0 ? 1 << 16 : 0);
         int incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
