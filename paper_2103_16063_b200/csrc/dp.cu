@@ -736,22 +736,39 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
                 if (s > 1 && prefix_bounds<DERIVED>(B, cd, keyidx, s, b, d, plf, plb))
                     dead = __dadd_rn(dmax_ref(plf, lbf), dmax_ref(plb, lbb)) > cd.U;
                 if (s > 1 && !dead) {
-                    // no predecessor with entries among the feasible spans of
-                    // any column: dp_cell would load no pair and end empty
-                    // (the reference's emptiness, below, is the same either way)
+                    // A column can only contribute through a predecessor with
+                    // entries among its feasible spans, and every candidate of
+                    // it is >= the corner of its shortest such span, (b_max, b)
+                    // with b_max the column's last non-empty b' (below b): if
+                    // that corner is already above the bound -- or no column
+                    // has such a predecessor -- dp_cell would load no pair and
+                    // end empty (the reference's emptiness, below, is the
+                    // same either way).
                     const int base = s - 1;
                     const int32_t *rp = B.reach_pre[(s - 1) & 1] + cd.val_off;
-                    bool pred = false;
-                    for (int dp = d - 1; dp >= base && !pred; --dp) {
+                    const int32_t *cmax = B.col_max[(s - 1) & 1] + cd.col_off;
+                    const int64_t row = (int64_t)b * (b - 1) / 2;
+                    const int inter_d = (B.num_nodes > 1 && (unsigned)d % (unsigned)B.dpn == 0) ? 1 : 0;
+                    bool alive = false;
+                    for (int dp = d - 1; dp >= base && !alive; --dp) {
                         const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
                         const int32_t upto = col[b - 1] >> 16;
                         if (upto == 0) continue;
                         const int kk = keyidx[d - dp];
                         if (kk < 0) continue;
                         const int x = max(base, B.key_ffb[kk][b]);
-                        pred = x <= b - 1 && upto > (x > base ? col[x - 1] >> 16 : 0);
+                        if (!(x <= b - 1 && upto > (x > base ? col[x - 1] >> 16 : 0))) continue;
+                        const int bp = min(cmax[dp - base], b - 1);
+                        const double tf = B.key_tf[kk][row + bp];
+                        const double tfc = b < nb ? __dadd_rn(tf, B.key_cut[kk][inter_d * (nb + 1) + b]) : tf;
+                        double tbc = DERIVED ? __dmul_rn(B.beta, tf) : B.key_tb[kk][row + bp];
+                        if (bp > 0) {
+                            const int inter_p = (B.num_nodes > 1 && (unsigned)dp % (unsigned)B.dpn == 0) ? 1 : 0;
+                            tbc = __dadd_rn(tbc, B.key_cut[kk][inter_p * (nb + 1) + bp]);
+                        }
+                        alive = !(__dadd_rn(dmax_ref(tfc, lbf), dmax_ref(tbc, lbb)) > cd.U);
                     }
-                    dead = !pred;
+                    dead = !alive;
                 }
                 // handed to dp_cell rounded down: still lower bounds
                 lb = make_float2(__double2float_rd(lbf), __double2float_rd(lbb));
