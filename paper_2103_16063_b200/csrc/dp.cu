@@ -773,6 +773,23 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
                 // handed to dp_cell rounded down: still lower bounds
                 lb = make_float2(__double2float_rd(lbf), __double2float_rd(lbb));
             }
+        } else if (s > 1) {
+            // an unbounded call of the batch (no greedy plan: typically one
+            // that fits nowhere): a cell without a predecessor holding entries
+            // among its feasible spans ends empty -- settled here as well
+            const int base = s - 1;
+            const int32_t *rp = B.reach_pre[(s - 1) & 1] + cd.val_off;
+            bool pred = false;
+            for (int dp = d - 1; dp >= base && !pred; --dp) {
+                const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
+                const int32_t upto = col[b - 1] >> 16;
+                if (upto == 0) continue;
+                const int kk = keyidx[d - dp];
+                if (kk < 0) continue;
+                const int x = max(base, B.key_ffb[kk][b]);
+                pred = x <= b - 1 && upto > (x > base ? col[x - 1] >> 16 : 0);
+            }
+            dead = !pred;
         }
         if (dead) {
             bool reach = false, zero = false;
