@@ -569,7 +569,13 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
                 std::vector<double> U(ng);
                 CUDA_TRY(ctx, cudaMemcpyAsync(U.data(), d_U, 8 * (size_t)ng, cudaMemcpyDeviceToHost, ctx->st));
                 CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
-                for (int t = 0; t < ng; ++t) cds[gpos[t]].U = U[t];
+                // No greedy plan (nothing packed: most such calls fit nowhere):
+                // U = -inf keeps only what the visit counts need -- the
+                // reference's emptiness of every cell, settled by k_dp_triage
+                // without frontiers.  A call that turns out feasible leaves its
+                // final cell non-empty but without entries (k_backtrack: -1)
+                // and is re-run unbounded below, like any too-tight bound.
+                for (int t = 0; t < ng; ++t) cds[gpos[t]].U = U[t] < INFINITY ? U[t] : -INFINITY;
             }
             // PIPECUT_B200_BOUND_SCALE (tests only): scale U, below 1 forcing the
             // too-tight path (final cell empty, the call re-run unbounded)
