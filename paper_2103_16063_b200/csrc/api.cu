@@ -1118,7 +1118,7 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     if (getenv("PIPECUT_B200_BB_ORACLE") && ctx->bb_U.empty() && !ctx->has_cost_table && ctx->mono_skip) {
         const double dp0 = ctx->last_dp_ms;
         std::vector<CallOut> first = outs;
-        ctx->bb_U.assign(calls.size(), INFINITY);
+        ctx->bb_U.assign(calls.size(), -INFINITY);     // infeasible: reachability only
         for (size_t i = 0; i < calls.size(); ++i)
             if (first[i].feasible) ctx->bb_U[i] = first[i].objective;
         ctx->last_dp_ms = 0;
