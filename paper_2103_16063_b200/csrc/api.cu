@@ -421,7 +421,7 @@ constexpr int64_t OFF_MAX = (int64_t)SPILL_BIT - 1;
 // capped there anyway; fewer chunks means fewer passes over the levels)
 constexpr int64_t CHUNK_HIST_CELLS = 1900000000;
 // objective bound (dp.cu) only for batches of at least this many unpruned visits
-constexpr double BOUND_MIN_VISITS = 2e10;
+constexpr double BOUND_MIN_VISITS = 2e8;
 
 // Runs one batch of DP calls whose buffers fit; fills outs[orig] for each.
 static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::vector<int> &idx,
@@ -1056,7 +1056,9 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     // on 4096 x 256, r2j).  Results are the same either way;
     // PIPECUT_B200_NO_BOUND=1 turns the bound off.
     // Small batches skip it: the waves' extra launches and the greedy plans
-    // cost more than the bound saves below ~2e10 closed-form visits (r2h sweep).
+    // cost more than the bound saves below ~2e8 closed-form visits (r2cj sweep:
+    // nb = 256 searches 3x faster bounded, nb = 64 ones 0.5 ms slower; the
+    // floor was 2e10 before calls without a greedy plan were bounded at -inf).
     double batch_visits = 0;
     for (auto &c : calls) {
         const double A = ctx->nb - c.S + 1, B = c.D - c.S + 1;

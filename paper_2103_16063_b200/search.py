@@ -88,7 +88,7 @@ def device_weights(ctx: _lib.Context, calls, batch_size: int):
 
 # the library bounds the DP of batches from this many closed-form visits up
 # (api.cu: BOUND_MIN_VISITS); their per-call cost then follows the DP cells
-BOUNDED_BATCH_VISITS = 2e10
+BOUNDED_BATCH_VISITS = 2e8
 
 
 def shard_weights(ctx: _lib.Context, calls, batch_size: int, nb: int):
