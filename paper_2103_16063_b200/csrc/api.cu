@@ -559,16 +559,18 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
                 if (!(cds[i].U < INFINITY) && ctx->bb_U.empty()) gpos.push_back(i);
             const int ng = (int)gpos.size();
             if (ng > 0 && getenv("PIPECUT_B200_NO_GREEDY") == nullptr) {
-                CUDA_TRY(ctx, ctx->bound_d.ensure(12 * (size_t)ng + 64));
-                double *d_U = ctx->bound_d.as<double>();
-                int32_t *d_pos = (int32_t *)(d_U + ng);
+                CUDA_TRY(ctx, ctx->bound_d.ensure((8 * GB_SPLITS + 4) * (size_t)ng + 64));
+                double *d_U = ctx->bound_d.as<double>();          // [GB_SPLITS][ng]
+                int32_t *d_pos = (int32_t *)(d_U + GB_SPLITS * ng);
                 CUDA_TRY(ctx, cudaMemcpyAsync(d_pos, gpos.data(), 4 * (size_t)ng, cudaMemcpyHostToDevice, ctx->st));
                 launch_greedy_bound(bt, ng, d_pos, d_U, ctx->derived, ctx->st);
                 ctx->launches++;
                 if (int rc = check_launch(ctx, "greedy_bound")) return rc;
-                std::vector<double> U(ng);
-                CUDA_TRY(ctx, cudaMemcpyAsync(U.data(), d_U, 8 * (size_t)ng, cudaMemcpyDeviceToHost, ctx->st));
+                std::vector<double> U(GB_SPLITS * (size_t)ng);
+                CUDA_TRY(ctx, cudaMemcpyAsync(U.data(), d_U, 8 * GB_SPLITS * (size_t)ng, cudaMemcpyDeviceToHost, ctx->st));
                 CUDA_TRY(ctx, cudaStreamSynchronize(ctx->st));
+                for (int t = 0; t < ng; ++t)                        // the best device split
+                    for (int k = 1; k < GB_SPLITS; ++k) U[t] = std::min(U[t], U[(size_t)k * ng + t]);
                 // No greedy plan (nothing packed: most such calls fit nowhere):
                 // U = -inf keeps only what the visit counts need -- the
                 // reference's emptiness of every cell, settled by k_dp_triage

@@ -275,6 +275,7 @@ void launch_plan_bound(const DPBatch &b, int n, const int32_t *pos, const int32_
                        bool derived, cudaStream_t st);
 void launch_reach_prefix(const DPBatch &b, int s, int n_active, int64_t n_cols,
                          const int64_t *col_prefix, cudaStream_t st);
+constexpr int GB_SPLITS = 2;    // greedy-bound device splits per call (extras first / last; spread: r2cm, no gain)
 void launch_greedy_bound(const DPBatch &b, int n, const int32_t *pos, double *U, bool derived,
                          cudaStream_t st);
 void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,

@@ -964,14 +964,24 @@ __global__ void __launch_bounds__(GB_WARPS * 32) k_greedy_bound(DPBatch Bt, int 
     const int nb = Bt.nb, S = cd.S, D = cd.D;
     const int q = D / S, r = D % S;
     const int kq = keyidx[q], kq1 = r > 0 ? keyidx[q + 1] : kq;
+    // the D % S extra devices go to the first stages (blockIdx.y == 0), the
+    // last ones (1) or spread evenly (2); the host keeps the best plan
+    const int pat = blockIdx.y;
+    U += (int64_t)pat * n;
     if (kq < 0 || kq1 < 0) {
         if (threadIdx.x == 0) U[w] = INFINITY;
         return;
     }
+    auto extras_before = [&](int i) {          // extra devices among stages < i
+        return pat == 0 ? min(i, r) : pat == 1 ? max(0, i - (S - r))
+                                               : (int)(((int64_t)i * r) / S);
+    };
+    auto extra = [&](int i) { return extras_before(i + 1) > extras_before(i); };
+    auto before_devs = [&](int i) { return i * q + extras_before(i); };
     // charged times of stage i = [lo, hi) (k_plan_bound's arithmetic)
     auto charged = [&](int i, int lo, int hi, double &tfc, double &tbc, double &raw) -> bool {
-        const int kk = i < r ? kq1 : kq;
-        const int before = i * q + min(i, r), after = before + q + (i < r ? 1 : 0);
+        const int kk = extra(i) ? kq1 : kq;
+        const int before = before_devs(i), after = before + q + (extra(i) ? 1 : 0);
         const int64_t o = hm_idx(lo, hi);
         const double tf = Bt.key_tf[kk][o];
         raw = fabs(tf);
@@ -1088,10 +1098,11 @@ __global__ void __launch_bounds__(GB_WARPS * 32) k_greedy_bound(DPBatch Bt, int 
 void launch_greedy_bound(const DPBatch &b, int n, const int32_t *pos, double *U, bool derived,
                          cudaStream_t st) {
     if (n <= 0) return;
+    const dim3 grid((unsigned)n, GB_SPLITS);     // U holds [GB_SPLITS][n]
     if (derived)
-        k_greedy_bound<true><<<n, GB_WARPS * 32, 0, st>>>(b, n, pos, U);
+        k_greedy_bound<true><<<grid, GB_WARPS * 32, 0, st>>>(b, n, pos, U);
     else
-        k_greedy_bound<false><<<n, GB_WARPS * 32, 0, st>>>(b, n, pos, U);
+        k_greedy_bound<false><<<grid, GB_WARPS * 32, 0, st>>>(b, n, pos, U);
 }
 
 // ---------------------------------------------------------------- bound: non-empty prefix
