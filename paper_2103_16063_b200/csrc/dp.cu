@@ -700,11 +700,15 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_LIST_MIN_BLOCKS) k_dp_level_
 }
 
 // One thread per cell of the active calls of a bounded batch at level s: a
-// cell of a bounded call whose whole frontier is above the bound (the same
-// tests as dp_cell: level S off the final cell, or the prefix lower bound) gets
-// its count byte here -- CNT_REACH or 0 for the reference's emptiness, plus the
-// zero-share flag, from the previous level's non-empty prefix counts -- and
-// every other cell is appended to the live list (warp-aggregated).
+// cell that can only end without entries gets its count byte here --
+// CNT_REACH or 0 for the reference's emptiness, plus the zero-share flag, from
+// the previous level's non-empty prefix counts -- and every other cell is
+// appended to the live list (warp-aggregated).  "Only without entries": for a
+// bounded call, level S off the final cell, the prefix lower bound above U, or
+// no column whose shortest feasible last stage from a predecessor with
+// entries stays within U; for an unbounded call of the batch, no predecessor
+// with entries in any column's feasible range.  (U = -inf, a call without a
+// greedy plan, settles every cell but level 1's and the final one here.)
 template <bool DERIVED>
 __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_prefix) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
