@@ -688,10 +688,12 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             d_cellpre = d_colpre + (n + 1);
             CUDA_TRY(ctx, cudaMemcpyAsync(d_colpre, col_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
             CUDA_TRY(ctx, cudaMemcpyAsync(d_cellpre, cell_prefix.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, ctx->st));
-            CUDA_TRY(ctx, ctx->live_d.ensure(16 * (size_t)val_cells + 128));
+            CUDA_TRY(ctx, ctx->live_d.ensure(16 * (size_t)val_cells + 20 * (size_t)col_total + 256));
             bt.live_count = ctx->live_d.as<unsigned long long>();
             bt.live = bt.live_count + 8;
             bt.live_lb = (float2 *)(bt.live + val_cells);
+            bt.lvl_kk = (double2 *)(((uintptr_t)(bt.live_lb + val_cells) + 15) & ~uintptr_t(15));
+            bt.lvl_kx = (short2 *)(bt.lvl_kk + col_total);
         }
         CUDA_TRY(ctx, cudaMemsetAsync(ob, 0, 64 + 3 * sizeof(unsigned long long) * (size_t)n + 64, ctx->st));
         CUDA_TRY(ctx, ctx->counters_d.ensure((8 + FMAX + 3 * WORK_SLOTS) * sizeof(unsigned long long)));
@@ -732,9 +734,10 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
                 // settle the cells above the bound by a thread each, then a
                 // persistent grid of warps over the live ones (dp.cu)
                 CUDA_TRY(ctx, cudaMemsetAsync(bt.live_count, 0, 2 * sizeof(unsigned long long), ctx->st));
+                launch_level_factors(bt, s, n_active, col_prefix[n_active], d_colpre, ctx->st);
                 launch_dp_triage(bt, s, n_active, cell_prefix[n_active], d_cellpre, ctx->derived, ctx->st);
                 launch_dp_level_list(bt, s, ctx->sm_count * DP_MIN_CTAS, ctx->derived, big, ctx->st);
-                ctx->launches += 2;
+                ctx->launches += 3;
             } else {
                 launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, big, ctx->st);
                 ctx->launches++;

@@ -209,6 +209,10 @@ struct DPBatch {
     unsigned long long *live;
     unsigned long long *live_count;  // [0] cells listed, [1] cells taken (k_dp_level_list)
     float2 *live_lb;                 // each live cell's suffix lower bounds (lbf, lbb), rounded down
+    // bounded batches, per level: per (call, column) the suffix / prefix
+    // group-bound factors and keys (k_level_factors; group_bounds' arithmetic)
+    double2 *lvl_kk;                 // [col_total] (suffix, prefix) factor
+    short2 *lvl_kx;                  // [col_total] (suffix, prefix) key, -1: no bound
     double *pool_tf[2];
     double *pool_tb[2];
     unsigned long long *vpool_used[2];  // [n_calls] per parity
@@ -278,6 +282,8 @@ void launch_reach_prefix(const DPBatch &b, int s, int n_active, int64_t n_cols,
 constexpr int GB_SPLITS = 2;    // greedy-bound device splits per call (extras first / last; spread: r2cm, no gain)
 void launch_greedy_bound(const DPBatch &b, int n, const int32_t *pos, double *U, bool derived,
                          cudaStream_t st);
+void launch_level_factors(const DPBatch &b, int s, int n_active, int64_t n_cols,
+                          const int64_t *col_prefix, cudaStream_t st);
 void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
                       const int64_t *cell_prefix, bool derived, cudaStream_t st);
 void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, bool big,

@@ -709,21 +709,52 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_LIST_MIN_BLOCKS) k_dp_level_
 // entries stays within U; for an unbounded call of the batch, no predecessor
 // with entries in any column's feasible range.  (U = -inf, a call without a
 // greedy plan, settles every cell but level 1's and the final one here.)
+constexpr int TRIAGE_CALLS = 64;     // calls a triage CTA caches (cells of more: global search)
 template <bool DERIVED>
 __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_prefix) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
+    // the calls this CTA's cells belong to: their range of cell_prefix, found
+    // once, then searched in shared memory
+    __shared__ int s_c0, s_c1;
+    __shared__ int64_t s_pre[TRIAGE_CALLS + 1];
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+    if (threadIdx.x == 0) {
+        int lo = 0, hi = n_active;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (cell_prefix[mid] <= g0) lo = mid; else hi = mid;
+        }
+        int c1 = lo;
+        while (c1 + 1 < n_active && cell_prefix[c1 + 1] < g0 + blockDim.x && c1 - lo < TRIAGE_CALLS - 1) ++c1;
+        s_c0 = lo;
+        s_c1 = c1;
+    }
+    __syncthreads();
+    const int c0 = s_c0, c1 = s_c1;
+    for (int i = threadIdx.x; i <= c1 - c0 + 1; i += blockDim.x) s_pre[i] = cell_prefix[c0 + i];
+    __syncthreads();
     bool live = false;
     int c = 0;
     int64_t idx = 0;
     float2 lb = make_float2(0.f, 0.f);
     if (g < cell_prefix[n_active]) {
-        int lo = 0, hi = n_active;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (cell_prefix[mid] <= g) lo = mid; else hi = mid;
+        int lo = 0, hi = c1 - c0 + 1;
+        if (g >= s_pre[hi]) {                      // past the cached calls (rare: many tiny calls)
+            lo = c1 + 1;
+            hi = n_active;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (cell_prefix[mid] <= g) lo = mid; else hi = mid;
+            }
+            c = lo;
+        } else {
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_pre[mid] <= g) lo = mid; else hi = mid;
+            }
+            c = c0 + lo;
         }
-        c = lo;
         const CallDesc cd = B.calls[c];
         idx = (int64_t)cd.A * cd.B - 1 - (g - cell_prefix[c]);     // heaviest first
         const int bi = (int)(idx / cd.B), di = (int)(idx % cd.B);
@@ -734,11 +765,21 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
             if (s == cd.S) {
                 dead = b != nb || d != cd.D;
             } else {
+                // suffix_bounds / prefix_bounds with this level's factors
+                const double2 fk = B.lvl_kk[cd.col_off + di];
+                const short2 fx = B.lvl_kx[cd.col_off + di];
                 double lbf = 0.0, lbb = 0.0;
-                suffix_bounds<DERIVED>(B, cd, keyidx, s, b, d, lbf, lbb);
-                double plf, plb;
-                if (s > 1 && prefix_bounds<DERIVED>(B, cd, keyidx, s, b, d, plf, plb))
+                if (fx.x >= 0) {
+                    const int64_t o = hm_idx(b, nb);
+                    lbf = __dmul_rn(fabs(B.key_tf[fx.x][o]), fk.x);
+                    lbb = DERIVED ? __dmul_rn(B.beta, lbf) : __dmul_rn(fabs(B.key_tb[fx.x][o]), fk.x);
+                }
+                if (s > 1 && fx.y >= 0) {
+                    const int64_t o = hm_idx(0, b);
+                    const double plf = __dmul_rn(fabs(B.key_tf[fx.y][o]), fk.y);
+                    const double plb = DERIVED ? __dmul_rn(B.beta, plf) : __dmul_rn(fabs(B.key_tb[fx.y][o]), fk.y);
                     dead = __dadd_rn(dmax_ref(plf, lbf), dmax_ref(plb, lbb)) > cd.U;
+                }
                 if (s > 1 && !dead) {
                     // A column can only contribute through a predecessor with
                     // entries among its feasible spans, and every candidate of
@@ -804,14 +845,19 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
             } else {
                 const int base = s - 1;
                 const int32_t *rp = B.reach_pre[(s - 1) & 1] + cd.val_off;
-                for (int dp = base; dp < d; ++dp) {
-                    const int32_t *col = rp + (int64_t)(dp - base) * cd.A - base;
+                // columns by share: m == 0 exactly for the widest last stages
+                // (dev above a threshold), so the zero-share ones come first
+                // in d' ascending -- each test stops at its first hit
+                int dp = base;
+                for (; dp < d && keyidx[d - dp] < 0; ++dp)
+                    if (!zero) zero = (rp[(int64_t)(dp - base) * cd.A - base + b - 1] & 0xffff) != 0;
+                for (int dq = d - 1; dq >= dp && !reach; --dq) {
+                    const int32_t *col = rp + (int64_t)(dq - base) * cd.A - base;
                     const int32_t upto = col[b - 1] & 0xffff;
                     if (upto == 0) continue;
-                    const int kk = keyidx[d - dp];
-                    if (kk < 0) { zero = true; continue; }
+                    const int kk = keyidx[d - dq];
                     const int x = max(base, B.key_ffb[kk][b]);
-                    if (x <= b - 1 && upto > (x > base ? col[x - 1] & 0xffff : 0)) reach = true;
+                    reach = x <= b - 1 && upto > (x > base ? col[x - 1] & 0xffff : 0);
                 }
             }
             const int64_t cell = (int64_t)di * cd.A + bi;
@@ -831,6 +877,47 @@ __global__ void k_dp_triage(DPBatch B, int s, int n_active, const int64_t *cell_
         B.live[at] = ((unsigned long long)c << 40) | (unsigned long long)idx;
         B.live_lb[at] = lb;
     }
+}
+
+// Per (active call, column d) of level s: group_bounds' key and factor for
+// the suffix (S - s stages over [b, nb) on D - d devices) and the prefix (s
+// stages over [0, b) on d devices) -- they do not depend on b, so the
+// triage's cells read them instead of recomputing three divisions each.
+__global__ void k_level_factors(DPBatch B, int s, int n_active, const int64_t *col_prefix) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= col_prefix[n_active]) return;
+    int lo = 0, hi = n_active;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (col_prefix[mid] <= g) lo = mid; else hi = mid;
+    }
+    const CallDesc cd = B.calls[lo];
+    const int di = (int)(g - col_prefix[lo]);
+    const int d = s + di;
+    const int16_t *keyidx = B.keyidx + cd.key_off;
+    auto factor = [&](int k, int dev, double &kk) -> int {
+        const int devmax = dev - (k - 1);
+        if (k < 1 || devmax < 1) return -1;
+        const int kx = keyidx[devmax];
+        if (kx < 0) return -1;
+        const int64_t q = (int64_t)cd.MB * cd.R;
+        const int64_t mx = B.batch_size / (q * devmax);
+        const double k1 = 1.0 / (double)k;
+        const double k2 = (double)(B.batch_size - q * devmax + 1) / ((double)(q * dev) * (double)mx);
+        kk = (1.0 - 1e-9) * (k1 > k2 ? k1 : k2);
+        return kx;
+    };
+    double ks = 0.0, kp = 0.0;
+    const int xs = s < cd.S ? factor(cd.S - s, cd.D - d, ks) : -1;
+    const int xp = factor(s, d, kp);
+    B.lvl_kk[cd.col_off + di] = make_double2(ks, kp);
+    B.lvl_kx[cd.col_off + di] = make_short2((short)xs, (short)xp);
+}
+
+void launch_level_factors(const DPBatch &b, int s, int n_active, int64_t n_cols,
+                          const int64_t *col_prefix, cudaStream_t st) {
+    if (n_cols > 0)
+        k_level_factors<<<(unsigned)((n_cols + 255) / 256), 256, 0, st>>>(b, s, n_active, col_prefix);
 }
 
 void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
