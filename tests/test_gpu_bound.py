@@ -68,6 +68,10 @@ def test_bound_on_off_too_tight_agree(gpu, env, nb, D, seed):
     tight = _records(run_calls(ctx, calls, 8 * D, False, True), 8 * D)
     bounded, reruns = _bound_info(ctx)
     assert tight == ref and reruns > 0
+    env(PIPECUT_B200_BOUND_SCALE=-1)         # U < 0: reachability only, as for calls
+    reach_only = _records(run_calls(ctx, calls, 8 * D, False, True), 8 * D)  # without a greedy plan
+    bounded, reruns = _bound_info(ctx)
+    assert reach_only == ref and reruns > 0
     env(PIPECUT_B200_BOUND_SCALE=None, PIPECUT_B200_BOUND_WAVES=1)   # partner-plan bounds
     waves = _records(run_calls(ctx, calls, 8 * D, False, True), 8 * D)
     assert waves == ref and _bound_info(ctx)[0] > 0
