@@ -736,7 +736,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
                 CUDA_TRY(ctx, cudaMemsetAsync(bt.live_count, 0, 2 * sizeof(unsigned long long), ctx->st));
                 launch_level_factors(bt, s, n_active, col_prefix[n_active], d_colpre, ctx->st);
                 launch_dp_triage(bt, s, n_active, cell_prefix[n_active], d_cellpre, ctx->derived, ctx->st);
-                launch_dp_level_list(bt, s, ctx->sm_count * DP_MIN_CTAS, ctx->derived, big, ctx->st);
+                launch_dp_level_list(bt, s, ctx->sm_count, maxS >= DP_DEEP_LEVELS, ctx->derived, big, ctx->st);
                 ctx->launches += 3;
             } else {
                 launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, big, ctx->st);

@@ -173,6 +173,8 @@ constexpr int DP_WARPS = PC_DP_WARPS;
 #define DP_LIST_MIN_BLOCKS 8
 #endif
 constexpr int DP_MIN_CTAS = DP_LIST_MIN_BLOCKS;   // resident list-kernel CTAs per SM
+constexpr int DP_LIST_MIN_BLOCKS_DEEP = 10;       // ... on batches of DP_DEEP_LEVELS levels or more
+constexpr int DP_DEEP_LEVELS = 512;
 constexpr int WORK_SLOTS = 64;  // work counters spread over slots (no same-address atomics)
 constexpr int FMAX = 64;       // Pareto frontier capacity per cell (two slots per lane)
 constexpr int FMAX_BIG = 126;  // the re-run variant (four slots per lane; 127 = CNT_REACH)
@@ -286,7 +288,7 @@ void launch_level_factors(const DPBatch &b, int s, int n_active, int64_t n_cols,
                           const int64_t *col_prefix, cudaStream_t st);
 void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
                       const int64_t *cell_prefix, bool derived, cudaStream_t st);
-void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, bool big,
+void launch_dp_level_list(const DPBatch &b, int s, int sm_count, bool deep, bool derived, bool big,
                           cudaStream_t st);
 void launch_profile_queries(const DevProblem &p, int n, const int32_t *lo, const int32_t *hi,
                             const int64_t *m, const int32_t *ckpt, double *tf, double *tb,

@@ -672,8 +672,8 @@ __global__ void __launch_bounds__(DP_WARPS * 32, DP_MIN_BLOCKS) k_dp_level(DPBat
 #ifndef PC_LIST_GRAB
 #define PC_LIST_GRAB 1          // consecutive list cells a warp takes per pop
 #endif
-template <bool DERIVED, int SLOTS>
-__global__ void __launch_bounds__(DP_WARPS * 32, DP_LIST_MIN_BLOCKS) k_dp_level_list(DPBatch B, int s) {
+template <bool DERIVED, int SLOTS, int MINB>
+__global__ void __launch_bounds__(DP_WARPS * 32, MINB) k_dp_level_list(DPBatch B, int s) {
     const unsigned long long n = B.live_count[0];
     const int lane = threadIdx.x & 31;
     if (PC_LIST_ATOMIC) {
@@ -930,15 +930,25 @@ void launch_dp_triage(const DPBatch &b, int s, int n_active, int64_t n_cells,
         k_dp_triage<false><<<blocks, 256, 0, st>>>(b, s, n_active, cell_prefix);
 }
 
-void launch_dp_level_list(const DPBatch &b, int s, int n_ctas, bool derived, bool big,
+// Resident CTAs per SM of the list kernel: 8 (64 registers) on the headline's
+// batches, 10 (48 registers, more spills, more warps to hide the loads) on
+// batches with very many levels -- r2db: 4096 x 256 499 vs 502 ms, 4096 x
+// 1024 3450 vs 3258 ms of DP.
+void launch_dp_level_list(const DPBatch &b, int s, int sm_count, bool deep, bool derived, bool big,
                           cudaStream_t st) {
     const int tpb = DP_WARPS * 32;
     if (big) {
-        if (derived) k_dp_level_list<true, 4><<<n_ctas, tpb, 0, st>>>(b, s);
-        else k_dp_level_list<false, 4><<<n_ctas, tpb, 0, st>>>(b, s);
+        const int n = sm_count * DP_LIST_MIN_BLOCKS;
+        if (derived) k_dp_level_list<true, 4, DP_LIST_MIN_BLOCKS><<<n, tpb, 0, st>>>(b, s);
+        else k_dp_level_list<false, 4, DP_LIST_MIN_BLOCKS><<<n, tpb, 0, st>>>(b, s);
+    } else if (deep) {
+        const int n = sm_count * DP_LIST_MIN_BLOCKS_DEEP;
+        if (derived) k_dp_level_list<true, 2, DP_LIST_MIN_BLOCKS_DEEP><<<n, tpb, 0, st>>>(b, s);
+        else k_dp_level_list<false, 2, DP_LIST_MIN_BLOCKS_DEEP><<<n, tpb, 0, st>>>(b, s);
     } else {
-        if (derived) k_dp_level_list<true, 2><<<n_ctas, tpb, 0, st>>>(b, s);
-        else k_dp_level_list<false, 2><<<n_ctas, tpb, 0, st>>>(b, s);
+        const int n = sm_count * DP_LIST_MIN_BLOCKS;
+        if (derived) k_dp_level_list<true, 2, DP_LIST_MIN_BLOCKS><<<n, tpb, 0, st>>>(b, s);
+        else k_dp_level_list<false, 2, DP_LIST_MIN_BLOCKS><<<n, tpb, 0, st>>>(b, s);
     }
 }
 
