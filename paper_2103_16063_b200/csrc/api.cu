@@ -723,6 +723,10 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
             for (auto &e : lev_ev) cudaEventCreate(&e);
             cudaEventRecord(lev_ev[0], ctx->st);
         }
+        // PIPECUT_B200_DEEP_LEVELS (tests): the level count from which the
+        // 10-CTA list kernel runs
+        const char *deep_env = getenv("PIPECUT_B200_DEEP_LEVELS");
+        const int deep_levels = deep_env ? atoi(deep_env) : DP_DEEP_LEVELS;
         for (int s = 1; s <= maxS; ++s) {
             int n_active = 0;
             while (n_active < n && cds[n_active].S >= s) ++n_active;
@@ -736,7 +740,7 @@ static int run_chunk(pc_ctx *ctx, const std::vector<pc_call> &calls, const std::
                 CUDA_TRY(ctx, cudaMemsetAsync(bt.live_count, 0, 2 * sizeof(unsigned long long), ctx->st));
                 launch_level_factors(bt, s, n_active, col_prefix[n_active], d_colpre, ctx->st);
                 launch_dp_triage(bt, s, n_active, cell_prefix[n_active], d_cellpre, ctx->derived, ctx->st);
-                launch_dp_level_list(bt, s, ctx->sm_count, maxS >= DP_DEEP_LEVELS, ctx->derived, big, ctx->st);
+                launch_dp_level_list(bt, s, ctx->sm_count, maxS >= deep_levels, ctx->derived, big, ctx->st);
                 ctx->launches += 3;
             } else {
                 launch_dp_level(bt, s, n_active, cta_prefix[n_active], ctx->derived, big, ctx->st);

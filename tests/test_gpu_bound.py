@@ -127,3 +127,24 @@ def test_bound_engages_on_the_search_path(gpu, env):
     env(PIPECUT_B200_NO_BOUND=1)
     b = result_doc(form_stage(32, 8, 2048, bs, speculative=True))
     assert a == b
+
+
+def test_deep_batch_list_kernel_matches_goldens(gpu, env):
+    """Batches of many levels take the 10-CTA instantiation of the list
+    kernel (DP_DEEP_LEVELS); forced on every bounded batch it gives the
+    oracle-pinned first-level answers."""
+    with open(os.path.join(GOLD, "c5_first_level.json")) as fh:
+        first = json.load(fh)
+    env(PIPECUT_B200_BOUND_MIN_VISITS=0, PIPECUT_B200_DEEP_LEVELS=1)
+    n = 0
+    for key, doc in sorted(first.items()):
+        if doc["nb"] != 1024 or doc["seed"] > 1:
+            continue
+        bs = cases.c5_blockset(doc["nb"], doc["D"], jitter_seed=doc["seed"])
+        res = form_stage(doc["nodes"], doc["dpn"], doc["batch"], bs)
+        a = doc["answer"]
+        assert res.stats.visits == doc["visits"] and res.stats.dp_calls == doc["dp_calls"]
+        assert res.plan.objective.hex() == a["objective"]
+        assert [s.devices for s in res.plan.stages] == a["devices"]
+        n += 1
+    assert n >= 4
