@@ -1043,14 +1043,16 @@ static int run_calls_impl(pc_ctx *ctx, const std::vector<pc_call> &calls, int64_
     ctx->launches = 0;
     // free device memory bounds the batch (chunks below).  cudaMemGetInfo
     // itself sporadically stalls for 5-40 ms (measured on the pool's boxes:
-    // the C1-C4 latencies' outliers), so a batch far below the last reading
-    // reuses it; only a batch that could come near it queries again.
+    // the C1-C4 latencies' outliers, and up to ~25 ms of a headline step), so
+    // a batch well below the last reading (under a quarter: 4096 x 256's
+    // estimate is 22 GB) reuses it; only a batch that could come near it
+    // queries again.
     size_t est = 0;
     for (auto &c : calls) {
         const int64_t A = ctx->nb - c.S + 1, B = c.D - c.S + 1;
         est += (size_t)A * B * (2 * (5 + 16 * 12) + (size_t)c.S * (5 + 4 * 5));
     }
-    if (ctx->mem_free == 0 || est > ctx->mem_free / 16) {
+    if (ctx->mem_free == 0 || est > ctx->mem_free / 4) {
         size_t free_b = 0, total_b = 0;
         cudaMemGetInfo(&free_b, &total_b);
         ctx->mem_free = free_b;
